@@ -1,0 +1,158 @@
+/*
+ * hlu_b200.h — C ABI of the B200-native H-LU hot path (sm_100a).
+ *
+ * The reference (hluflow, pure Python) has no FFI; its hot path is the set of
+ * LAPACK/BLAS call sites under the H-recursion.  Each entry point below
+ * replaces a family of those call sites, batched over one level of the leaf
+ * DAG:
+ *
+ *   hlu_getrf_batched_f64   <- lu_nopivot            lowrank.py:183-231, called at hlu.py:635-637
+ *   hlu_trsm_batched_f64    <- trsm_lower_unit        lowrank.py:234-239 (hlu.py:407,450)
+ *                              trsm_upper_right       lowrank.py:242-247 (hlu.py:487,534)
+ *                              Rk-factor solves       hlu.py:415-418, 495-498, 531
+ *                              (+ backward vector solve U x = y, absent in the reference)
+ *   hlu_gemm_batched_f64    <- gemm_update            lowrank.py:250-261 (hlu.py:217..604)
+ *                              _op_matmat/_op_t_matmat/_op_*gemm_into  hlu.py:160-255
+ *   hlu_rk_update_batched_f64 <- add_truncated        lowrank.py:148-168
+ *                              recompress             lowrank.py:137-145 (incl. _merge_lowrank hlu.py:294-309)
+ *                              compress_dense         lowrank.py:171-175 (dense x dense products, hlu.py:269-270)
+ *                              _truncate_svd          lowrank.py:127-134
+ *   hlu_schedule_*          <- the sequential/OmpSs executor (hlu.py:315-354, runtime.py):
+ *                              a precomputed level-set schedule replayed as one CUDA graph.
+ *
+ * Conventions: all matrices live in ONE fp64 device pool; a view addresses
+ * element (i,j) at pool[off + i*rs + j*cs].  Dimensions flagged dynamic read
+ * the current rank of an Rk object from the int32 rank table at kernel time,
+ * so ranks can grow and shrink in place.  Every call is stream-ordered and
+ * returns 0 or a negative error code; device-side failures (small pivot,
+ * rank-capacity overflow) land in the error words of hlu_ctx.err.
+ */
+#ifndef HLU_B200_H
+#define HLU_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* element (i,j) at pool[off + i*rs + j*cs]; rdyn/cdyn >= 0 -> dimension is ranks[slot] */
+typedef struct {
+  int64_t off;
+  int32_t rows, cols;
+  int32_t rs, cs;
+  int32_t rdyn, cdyn;
+} hlu_view; /* 32 bytes */
+
+/* device pointers shared by every kernel */
+typedef struct {
+  double *pool;    /* all payloads, temps and workspaces */
+  int32_t *ranks;  /* current rank per Rk object */
+  int32_t *log;    /* dynamic values logged for the effective-flop counter */
+  int32_t *err;    /* [0] overflow count, [1] first failing LU op (INT32_MAX = none),
+                      [2] unsupported-shape count, [3] reserved */
+  double *dlog;    /* per-LU (pivot, tol) of a failure: dlog[2*lu_index] */
+  double eps;      /* TruncationControl.eps */
+  int32_t kmax;    /* TruncationControl.kmax, -1 = none */
+  int32_t pad;
+} hlu_ctx;
+
+/* In-place unpivoted LU of a square block (n <= 128). */
+typedef struct {
+  hlu_view a;
+  int32_t op_id;   /* program-order index, for the SingularBlockError label */
+  int32_t lu_index;
+} hlu_getrf_desc; /* 40 bytes */
+
+enum {
+  HLU_TRSM_LEFT_LOWER_UNIT = 0, /* X <- L^-1 X   */
+  HLU_TRSM_RIGHT_UPPER = 1,     /* X <- X U^-1   */
+  HLU_TRSM_LEFT_UPPER = 2       /* X <- U^-1 X   */
+};
+
+typedef struct {
+  hlu_view t, x;
+  int32_t mode;
+  int32_t log;     /* >= 0: log[log] = dynamic RHS count */
+} hlu_trsm_desc; /* 72 bytes */
+
+enum { HLU_TERM_ZERO = 0, HLU_TERM_GEMM = 1, HLU_TERM_TRIPLE = 2 };
+
+/* one term of an ordered accumulation chain:
+ *   ZERO:   C = 0
+ *   GEMM:   C += alpha * A B
+ *   TRIPLE: C += alpha * A (M B)   (assoc 0)   or   alpha * (A M) B   (assoc 1) */
+typedef struct {
+  hlu_view c, a, m, b;
+  double alpha;
+  int32_t kind, assoc;
+} hlu_term; /* 144 bytes */
+
+typedef struct {
+  int32_t term_begin, term_count;
+  int32_t log, log_slot; /* log[log] = ranks[log_slot] at execution, if log >= 0 */
+} hlu_gemm_desc; /* 16 bytes */
+
+/* one factor pair of a truncation input, placed at (roff, coff) of the output frame */
+typedef struct {
+  hlu_view a, b;   /* a: m_p x k, b: n_p x k (k may be dynamic) */
+  double sign;     /* applied to a */
+  int32_t roff, coff;
+} hlu_rkpart; /* 80 bytes */
+
+enum {
+  HLU_RK_ADD = 0,        /* add_truncated(part0, part1) with the reference shortcuts */
+  HLU_RK_RECOMPRESS = 1  /* recompress(concat(parts)) ; also compress_dense(A@B) as part (A, B^T) */
+};
+
+typedef struct {
+  int32_t mode, part_begin, part_count;
+  int32_t m, n, cap;
+  int32_t out_slot, log;
+  int64_t out_a, out_b;  /* column-major outputs, ld = m / n, capacity cap columns */
+  int64_t ws;            /* workspace offset in the pool (TSQR reflectors) */
+} hlu_rkt_desc; /* 56 bytes */
+
+/* launch kinds of a schedule entry */
+enum { HLU_K_GETRF = 0, HLU_K_TRSM = 1, HLU_K_GEMM = 2, HLU_K_RKT32 = 3, HLU_K_RKT64 = 4 };
+
+typedef struct {
+  int32_t kind;
+  int32_t count;
+  int64_t first;     /* index of the first descriptor of this launch */
+  int32_t smem_dim;  /* largest square dimension (getrf / trsm) */
+  int32_t pad;
+} hlu_launch; /* 24 bytes */
+
+/* --- batched kernels (descriptor arrays are device pointers) --- */
+int hlu_getrf_batched_f64(const hlu_ctx *ctx, const hlu_getrf_desc *d, int count, int max_n, void *stream);
+int hlu_trsm_batched_f64(const hlu_ctx *ctx, const hlu_trsm_desc *d, int count, int max_n, void *stream);
+int hlu_gemm_batched_f64(const hlu_ctx *ctx, const hlu_gemm_desc *d, const hlu_term *terms, int count,
+                         void *stream);
+int hlu_rk_update_batched_f64(const hlu_ctx *ctx, const hlu_rkt_desc *d, const hlu_rkpart *parts,
+                              int count, int kclass, void *stream);
+
+/* TSQR workspace (doubles) one truncation needs for an m-row factor of width <= K */
+int64_t hlu_rkt_ws_doubles(int32_t m, int32_t kbound);
+
+/* --- level-set schedule runtime (one CUDA graph per factorization) --- */
+typedef struct hlu_schedule hlu_schedule;
+
+/* launches: host array (copied); descriptor arrays: device pointers that must
+ * outlive the schedule; use_graph: capture the launch sequence into a CUDA graph */
+int hlu_schedule_create(hlu_schedule **out, const hlu_ctx *ctx, const hlu_launch *launches, int64_t nlaunch,
+                        const hlu_getrf_desc *getrf, const hlu_trsm_desc *trsm, const hlu_gemm_desc *gemm,
+                        const hlu_term *terms, const hlu_rkt_desc *rkt, const hlu_rkpart *parts,
+                        int use_graph, void *stream);
+int hlu_schedule_launch(hlu_schedule *s, void *stream);
+int hlu_schedule_destroy(hlu_schedule *s);
+
+/* library identity / sanity */
+const char *hlu_version(void);
+int hlu_device_check(void); /* 0 when a sm_100 device is present */
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* HLU_B200_H */

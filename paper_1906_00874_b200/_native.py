@@ -1,0 +1,79 @@
+"""ctypes binding of the C ABI (``include/hlu_b200.h``).
+
+The library is built in-tree (``make`` / ``__graft_entry__.build()``) as
+``paper_1906_00874_b200/libhlu_b200.so``.  There is no fallback: if it is
+missing, every device entry point raises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libhlu_b200.so")
+
+SYMBOLS = (
+    "hlu_getrf_batched_f64",
+    "hlu_trsm_batched_f64",
+    "hlu_gemm_batched_f64",
+    "hlu_rk_update_batched_f64",
+    "hlu_rkt_ws_doubles",
+    "hlu_schedule_create",
+    "hlu_schedule_launch",
+    "hlu_schedule_destroy",
+    "hlu_version",
+    "hlu_device_check",
+)
+
+
+class HluCtx(ctypes.Structure):
+    _fields_ = [
+        ("pool", ctypes.c_void_p),
+        ("ranks", ctypes.c_void_p),
+        ("log", ctypes.c_void_p),
+        ("err", ctypes.c_void_p),
+        ("dlog", ctypes.c_void_p),
+        ("eps", ctypes.c_double),
+        ("kmax", ctypes.c_int32),
+        ("pad", ctypes.c_int32),
+    ]
+
+
+_lib = None
+
+
+def lib():
+    """Load the sm_100a library (raises when it has not been built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise RuntimeError(
+            f"CUDA library {LIB_PATH} is missing: run `make` (or __graft_entry__.build()); "
+            "there is no CPU fallback"
+        )
+    L = ctypes.CDLL(LIB_PATH)
+    vp, i32, i64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64
+    L.hlu_getrf_batched_f64.argtypes = [ctypes.POINTER(HluCtx), vp, i32, i32, vp]
+    L.hlu_trsm_batched_f64.argtypes = [ctypes.POINTER(HluCtx), vp, i32, i32, vp]
+    L.hlu_gemm_batched_f64.argtypes = [ctypes.POINTER(HluCtx), vp, vp, i32, vp]
+    L.hlu_rk_update_batched_f64.argtypes = [ctypes.POINTER(HluCtx), vp, vp, i32, i32, vp]
+    L.hlu_rkt_ws_doubles.argtypes = [i32, i32]
+    L.hlu_rkt_ws_doubles.restype = i64
+    L.hlu_schedule_create.argtypes = [ctypes.POINTER(vp), ctypes.POINTER(HluCtx), vp, i64,
+                                      vp, vp, vp, vp, vp, vp, i32, vp]
+    L.hlu_schedule_launch.argtypes = [vp, vp]
+    L.hlu_schedule_destroy.argtypes = [vp]
+    L.hlu_version.restype = ctypes.c_char_p
+    for name in ("hlu_getrf_batched_f64", "hlu_trsm_batched_f64", "hlu_gemm_batched_f64",
+                 "hlu_rk_update_batched_f64", "hlu_schedule_create", "hlu_schedule_launch",
+                 "hlu_schedule_destroy", "hlu_device_check"):
+        getattr(L, name).restype = ctypes.c_int
+    _lib = L
+    return L
+
+
+def check(rc, what):
+    if rc != 0:
+        raise RuntimeError(f"{what} failed with status {rc}")

@@ -1,0 +1,68 @@
+// Shared device helpers for the H-LU kernels (sm_100a, fp64).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "hlu_b200.h"
+
+#define HLU_NT 256  // threads per CTA for every batched kernel
+#define HLU_NWARP (HLU_NT / 32)
+
+namespace hlu {
+
+// A resolved view: element (i,j) at p[i*rs + j*cs].  p may point to global or
+// shared memory (generic addressing), so the same tile routines serve both.
+struct Mat {
+  double *p;
+  int rows, cols;
+  long long rs, cs;
+  __device__ __forceinline__ double &at(int i, int j) const { return p[i * rs + j * cs]; }
+  __device__ __forceinline__ double get(int i, int j) const { return p[i * rs + j * cs]; }
+};
+
+__device__ __forceinline__ Mat resolve(const hlu_ctx &c, const hlu_view &v) {
+  Mat m;
+  m.p = c.pool + v.off;
+  m.rows = v.rdyn >= 0 ? c.ranks[v.rdyn] : v.rows;
+  m.cols = v.cdyn >= 0 ? c.ranks[v.cdyn] : v.cols;
+  m.rs = v.rs;
+  m.cs = v.cs;
+  return m;
+}
+
+__device__ __forceinline__ Mat smat(double *p, int rows, int cols, int ld) {
+  Mat m;
+  m.p = p;
+  m.rows = rows;
+  m.cols = cols;
+  m.rs = 1;
+  m.cs = ld;
+  return m;
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// block-wide max over HLU_NT threads; red must hold HLU_NWARP doubles
+__device__ __forceinline__ double block_max(double v, double *red) {
+  v = warp_max(v);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  double r = red[0];
+#pragma unroll
+  for (int i = 1; i < HLU_NWARP; ++i) r = fmax(r, red[i]);
+  __syncthreads();
+  return r;
+}
+
+}  // namespace hlu
