@@ -1,0 +1,161 @@
+"""Device runtime: pools in HBM, descriptor upload, one CUDA graph per call.
+
+PyTorch provides the device memory and the stream; all arithmetic runs in
+``libhlu_b200.so`` through the C ABI.  A ``DeviceCall`` owns
+
+* the fp64 pool: leaf payloads (dense leaves, Rk factor slabs) followed by the
+  temp/workspace arena planned by ``schedule.allocate_temps``,
+* the rank table, the flop log and the error words,
+* the packed descriptor arrays and the captured schedule (CUDA graph).
+
+No CPU fallback exists: without the library or a GPU, construction raises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _native
+from .hmatrix import StructureError  # noqa: F401  (re-exported for callers)
+from .lowrank import SingularBlockError
+from .pool import fill_pool, read_extra, read_pool
+from .schedule import Packed, effective_flops, pack
+
+INT32_MAX = np.iinfo(np.int32).max
+
+
+class RankOverflow(RuntimeError):
+    """An Rk result exceeded the reserved per-block capacity (re-plan larger)."""
+
+
+def _torch():
+    import torch
+
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_1906_00874_b200 needs a CUDA device (sm_100a); no CPU fallback")
+    return torch
+
+
+def _dev_bytes(torch, arr, device):
+    t = torch.from_numpy(np.ascontiguousarray(arr).view(np.uint8)).to(device)
+    return t
+
+
+class DeviceCall:
+    """One planned H-arithmetic call resident on the GPU."""
+
+    def __init__(self, layout, planner, ctl, device=None, use_graph=True, extras=None):
+        torch = _torch()
+        self.torch = torch
+        self.device = torch.device(device if device is not None else "cuda")
+        self.L = layout
+        self.pl = planner
+        self.ctl = ctl
+        lib = _native.lib()
+        self.lib = lib
+        self.packed: Packed = pack(planner, layout.payload_doubles)
+        p = self.packed
+        self.total = layout.payload_doubles + p.arena_doubles
+        host_pool = np.zeros(layout.payload_doubles, dtype=np.float64)
+        host_ranks = np.zeros(p.nranks, dtype=np.int32)
+        fill_pool(layout, host_pool, host_ranks, extras)
+        self.h2d_bytes = host_pool.nbytes + host_ranks.nbytes
+        with torch.cuda.device(self.device):
+            self.pool = torch.empty(self.total, dtype=torch.float64, device=self.device)
+            self.host_pool = torch.from_numpy(host_pool).pin_memory()
+            self.host_ranks = torch.from_numpy(host_ranks).pin_memory()
+            self.ranks = torch.empty(p.nranks, dtype=torch.int32, device=self.device)
+            self.log = torch.zeros(p.nlog, dtype=torch.int32, device=self.device)
+            self.err = torch.tensor([0, INT32_MAX, 0, 0], dtype=torch.int32, device=self.device)
+            self.dlog = torch.zeros(2 * max(len(p.lu_labels), 1), dtype=torch.float64, device=self.device)
+            self.d_getrf = _dev_bytes(torch, p.getrf, self.device)
+            self.d_trsm = _dev_bytes(torch, p.trsm, self.device)
+            self.d_gemm = _dev_bytes(torch, p.gemm, self.device)
+            self.d_terms = _dev_bytes(torch, p.terms, self.device)
+            self.d_rkt = _dev_bytes(torch, p.rkt, self.device)
+            self.d_parts = _dev_bytes(torch, p.parts, self.device)
+            self.upload()
+            self.ctx = _native.HluCtx(
+                self.pool.data_ptr(), self.ranks.data_ptr(), self.log.data_ptr(), self.err.data_ptr(),
+                self.dlog.data_ptr(), float(ctl.eps), -1 if ctl.kmax is None else int(ctl.kmax), 0,
+            )
+            self.stream = torch.cuda.current_stream(self.device)
+            handle = ctypes.c_void_p()
+            launches = np.ascontiguousarray(p.launches)
+            rc = lib.hlu_schedule_create(
+                ctypes.byref(handle), ctypes.byref(self.ctx), launches.ctypes.data, len(launches),
+                self.d_getrf.data_ptr(), self.d_trsm.data_ptr(), self.d_gemm.data_ptr(),
+                self.d_terms.data_ptr(), self.d_rkt.data_ptr(), self.d_parts.data_ptr(),
+                1 if use_graph else 0, ctypes.c_void_p(self.stream.cuda_stream),
+            )
+            _native.check(rc, "hlu_schedule_create")
+            self.handle = handle
+        self.nkernels = int(p.launches["count"].astype(bool).sum()) if len(p.launches) else 0
+
+    # -- data movement
+    def upload(self):
+        """Host (pinned) -> device copy of payloads and ranks; resets error words."""
+        n = self.L.payload_doubles
+        self.pool[:n].copy_(self.host_pool, non_blocking=True)
+        self.ranks.copy_(self.host_ranks, non_blocking=True)
+        self.err.copy_(self.torch.tensor([0, INT32_MAX, 0, 0], dtype=self.torch.int32), non_blocking=True)
+
+    def snapshot(self):
+        """Device-resident pristine copy, for repeated timed runs."""
+        n = self.L.payload_doubles
+        self._pristine = (self.pool[:n].clone(), self.ranks.clone())
+
+    def restore(self):
+        n = self.L.payload_doubles
+        self.pool[:n].copy_(self._pristine[0])
+        self.ranks.copy_(self._pristine[1])
+        self.err[0] = 0
+        self.err[1] = INT32_MAX
+        self.err[2] = 0
+
+    def launch(self):
+        rc = self.lib.hlu_schedule_launch(self.handle, ctypes.c_void_p(self.stream.cuda_stream))
+        _native.check(rc, "hlu_schedule_launch")
+
+    def check_errors(self):
+        err = self.err.cpu().numpy()
+        if err[1] != INT32_MAX:
+            op_id = int(err[1])
+            idx = int(np.nonzero(self.packed.lu_op_ids == op_id)[0][0])
+            p, tol = self.dlog[2 * idx : 2 * idx + 2].cpu().numpy()
+            label = self.packed.lu_labels[idx]
+            raise SingularBlockError(
+                f"pivot {p:.3e} below tolerance {tol:.3e} in block {label or '<root>'}", label
+            )
+        if err[2]:
+            raise RuntimeError(f"{int(err[2])} truncations exceeded the supported stacked rank (64)")
+        if err[0]:
+            raise RankOverflow(f"{int(err[0])} Rk results exceeded capacity {self.L.cap}")
+
+    def download(self):
+        """Device -> host: install results into the H-matrix; returns d2h bytes."""
+        n = self.L.payload_doubles
+        pool = self.pool[:n].cpu().numpy()
+        ranks = self.ranks.cpu().numpy()
+        read_pool(self.L, pool, ranks)
+        self._last_pool = pool
+        return pool.nbytes + ranks.nbytes
+
+    def extra(self, name):
+        return read_extra(self.L, self._last_pool, name)
+
+    def flops(self):
+        return effective_flops(self.packed, self.log.cpu().numpy())
+
+    def close(self):
+        if getattr(self, "handle", None):
+            self.lib.hlu_schedule_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

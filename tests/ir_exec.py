@@ -60,12 +60,15 @@ class CpuMachine:
             self.log[int(d["log"])] = x.shape[0] if mode == 1 else x.shape[1]
         if x.size == 0:
             return
-        if mode == ir.TRSM_LOWER_UNIT:
-            x[:] = scipy.linalg.solve_triangular(t, x, lower=True, unit_diagonal=True)
-        elif mode == ir.TRSM_RIGHT_UPPER:
-            x[:] = scipy.linalg.solve_triangular(t, x.T, lower=False, trans="T").T
-        else:
-            x[:] = scipy.linalg.solve_triangular(t, x, lower=False)
+        try:
+            if mode == ir.TRSM_LOWER_UNIT:
+                x[:] = scipy.linalg.solve_triangular(t, x, lower=True, unit_diagonal=True)
+            elif mode == ir.TRSM_RIGHT_UPPER:
+                x[:] = scipy.linalg.solve_triangular(t, x.T, lower=False, trans="T").T
+            else:
+                x[:] = scipy.linalg.solve_triangular(t, x, lower=False)
+        except np.linalg.LinAlgError:  # singular factor after a failed LU: garbage, like the GPU
+            x[:] = np.nan
 
     def gemm(self, d, terms):
         if int(d["log"]) >= 0:

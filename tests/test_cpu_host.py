@@ -1,0 +1,112 @@
+"""CPU-side checks: the C ABI library loads and exports every symbol of
+include/hlu_b200.h; descriptor layouts match the header; the planner + level
+schedule + arena reproduce the oracle exactly when the packed IR is executed
+with numpy (tests/ir_exec.py); schedule hazards against a brute-force check."""
+
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+import cases
+from ir_exec import CpuMachine
+from paper_1906_00874_b200 import _native, ir
+from paper_1906_00874_b200.lowrank import TruncationControl
+from paper_1906_00874_b200.planner import Layout, Planner
+from paper_1906_00874_b200.pool import fill_pool, read_pool
+from paper_1906_00874_b200.schedule import assign_levels, effective_flops, pack
+
+HDR = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "include", "hlu_b200.h")
+
+
+def test_library_exports_header_symbols():
+    lib = ctypes.CDLL(_native.LIB_PATH)
+    text = open(HDR).read()
+    names = set(re.findall(r"^(?:int|int64_t|const char \*)\s*(hlu_\w+)\(", text, re.M))
+    assert names == set(_native.SYMBOLS)
+    for nm in names:
+        assert hasattr(lib, nm), nm
+    assert _native.lib().hlu_version().startswith(b"hlu_b200")
+
+
+def test_workspace_formula_mirrors_library():
+    L = _native.lib()
+    for m in (1, 17, 64, 80, 112, 113, 257, 2049, 9000):
+        for k in (1, 8, 31, 32, 33, 64, 80):
+            assert L.hlu_rkt_ws_doubles(m, k) == ir.rkt_ws_doubles(m, k)
+
+
+def _run_ir(name, cap=32):
+    build, ctl = cases.CASES[name]
+    h, _ = build()
+    L = Layout(h, cap=cap)
+    pl = Planner(L)
+    pl.factor(h)
+    p = pack(pl, L.payload_doubles)
+    pool = np.zeros(L.payload_doubles + p.arena_doubles)
+    ranks = np.zeros(p.nranks, np.int32)
+    fill_pool(L, pool, ranks)
+    M = CpuMachine(pool, ranks, p.nlog, ctl[0], ctl[1])
+    M.run(p)
+    read_pool(L, pool, ranks)
+    return h, p, M, pl
+
+
+@pytest.mark.parametrize("name", ["mixed_192", "mixed_256_kmax", "dense2x2_256_r3", "bem1d_1024"])
+def test_packed_ir_reproduces_reference(name):
+    g = cases.golden(name)
+    h, p, M, _ = _run_ir(name)
+    assert M.err[0] == 0 and M.err[1] == np.iinfo(np.int32).max
+    assert np.array_equal(cases.ranks(h), g["ranks_out"])
+    assert abs(effective_flops(p, M.log) - float(g["flops"])) <= 1e-12 * float(g["flops"])
+    gn = g["norms_out"]
+    assert np.max(np.abs(cases.leaf_norms(h) - gn) / np.maximum(gn, 1e-300)) <= 1e-12
+
+
+def test_levels_respect_program_order_hazards():
+    """Brute force: every conflicting op pair keeps program order in levels."""
+    build, _ = cases.CASES["mixed_192"]
+    h, _ = build()
+    L = Layout(h)
+    pl = Planner(L)
+    pl.factor(h)
+    lv = assign_levels(pl)
+    base = L.nslots
+    n = len(pl.ops)
+    R, W = [], []
+    for op in pl.ops:
+        r = set()
+        for lo, hi in op.reads:
+            r.update(range(lo, hi))
+        r.update(base + t for t in op.temps_in)
+        w = set()
+        for lo, hi in op.writes:
+            w.update(range(lo, hi))
+        w.update(base + t for t in op.temps_out)
+        R.append(r)
+        W.append(w)
+    for j in range(n):
+        for i in range(j):
+            if (W[i] & (R[j] | W[j])) or (R[i] & W[j]):
+                assert lv[i] < lv[j], (i, j, pl.ops[i].kind, pl.ops[j].kind)
+
+
+def test_singular_block_label_in_plan():
+    from paper_1906_00874_b200.blocks import build_diagonal_2x2_tree
+    from paper_1906_00874_b200.hmatrix import build_hmatrix
+
+    h = build_hmatrix(build_diagonal_2x2_tree(8, 1)[0])
+    L = Layout(h)
+    pl = Planner(L)
+    pl.factor(h)
+    p = pack(pl, L.payload_doubles)
+    pool = np.zeros(L.payload_doubles + p.arena_doubles)
+    ranks = np.zeros(p.nranks, np.int32)
+    fill_pool(L, pool, ranks)
+    M = CpuMachine(pool, ranks, p.nlog, 1e-8, None)
+    M.run(p)
+    first = int(M.err[1])
+    idx = int(np.nonzero(p.lu_op_ids == first)[0][0])
+    assert p.lu_labels[idx] == "lu[0:4)x[0:4)"

@@ -1,0 +1,174 @@
+"""GPU parity: the sm_100a path against the CPU oracle and the reference's
+golden fixtures.  Everything here goes through the C ABI (libhlu_b200.so)."""
+
+import numpy as np
+import pytest
+
+import cases
+from oracle import hlu_oracle as orc
+from paper_1906_00874_b200 import device_ops, hmatrix
+from paper_1906_00874_b200.hlu import forward_solve, hlu_factorize, hlu_solve, make_plan
+from paper_1906_00874_b200.lowrank import LowRank, SingularBlockError, TruncationControl
+
+pytestmark = pytest.mark.gpu
+
+GOLDEN_CASES = ["mixed_192", "mixed_256_kmax", "dense2x2_256_r3", "bem1d_1024", "sphere_1024",
+                "sphere_2048_l64", "cfg1"]
+
+
+def _lr(rng, m, n, k):
+    return LowRank(rng.standard_normal((m, k)), rng.standard_normal((n, k)))
+
+
+def _spec(a):
+    return np.linalg.svd(a, compute_uv=False)[0] if a.size else 0.0
+
+
+# ---- single-op kernels vs the oracle (reference lowrank.py semantics) -------------
+
+
+def test_lu_known_answers():
+    a = np.array([[2.0, 1.0], [4.0, 5.0]])
+    device_ops.lu_nopivot(a)
+    assert np.array_equal(a, np.array([[2.0, 1.0], [2.0, 3.0]]))
+    e = np.eye(5)
+    device_ops.lu_nopivot(e)
+    assert np.array_equal(e, np.eye(5))
+    with pytest.raises(SingularBlockError) as err:
+        device_ops.lu_nopivot(np.array([[1.0, 1.0], [1.0, 1.0]]), block_path="diag")
+    assert err.value.block_path == "diag"
+
+
+@pytest.mark.parametrize("n", [15, 32, 48, 64, 96, 128])
+def test_lu_vs_oracle(rng, n):
+    a = rng.standard_normal((n, n)) + n * np.eye(n)
+    want = orc.lu_nopivot(a.copy())
+    got = device_ops.lu_nopivot(a.copy())
+    assert np.linalg.norm(got - want) <= 1e-13 * np.linalg.norm(want)
+
+
+def test_trsm_vs_oracle(rng):
+    for n, r in [(16, 7), (64, 64), (64, 130), (33, 1)]:
+        l = np.tril(rng.standard_normal((n, n)), -1) + np.eye(n)
+        b = rng.standard_normal((n, r))
+        want = orc.trsm_lower_unit(l, b.copy())
+        got = device_ops.trsm_lower_unit(l, b.copy())
+        assert np.linalg.norm(got - want) <= 1e-12 * np.linalg.norm(want)
+        u = np.triu(rng.standard_normal((n, n))) + 4 * np.eye(n)
+        b2 = rng.standard_normal((r, n))
+        want = orc.trsm_upper_right(u, b2.copy())
+        got = device_ops.trsm_upper_right(u, b2.copy())
+        assert np.linalg.norm(got - want) <= 1e-11 * np.linalg.norm(want)
+        want = np.linalg.solve(u, b)
+        got = device_ops.trsm_upper_left(u, b.copy())
+        assert np.linalg.norm(got - want) <= 1e-11 * np.linalg.norm(want)
+
+
+def test_gemm_update_vs_oracle(rng):
+    for m, n, k in [(6, 5, 4), (64, 64, 64), (130, 70, 33), (1, 200, 3)]:
+        c, a, b = rng.standard_normal((m, n)), rng.standard_normal((m, k)), rng.standard_normal((k, n))
+        want = c - a @ b
+        got = device_ops.gemm_update(c.copy(), a, b)
+        assert np.linalg.norm(got - want) <= 1e-14 * np.linalg.norm(want)
+
+
+def test_add_truncated_shortcuts(rng):
+    x = _lr(rng, 8, 7, 3)
+    z = LowRank.zeros(8, 7)
+    got = device_ops.add_truncated(x, z, TruncationControl(1e-12))
+    assert np.array_equal(got.value(), x.value())
+    got = device_ops.add_truncated(z, x, TruncationControl(1e-12))
+    assert got.k == 3 and np.array_equal(got.value(), x.value())
+
+
+def test_add_truncated_parallel_outer(rng):
+    a = rng.standard_normal((8, 1))
+    b = rng.standard_normal((5, 1))
+    got = device_ops.add_truncated(LowRank(a, b), LowRank(a.copy(), b.copy()), TruncationControl(1e-10))
+    assert got.k == 1
+    assert np.linalg.norm(got.value() - 2 * a @ b.T) <= 1e-13 * np.linalg.norm(a @ b.T)
+
+
+def test_truncation_exact_rank_13(rng):
+    q1, _ = np.linalg.qr(rng.standard_normal((32, 32)))
+    q2, _ = np.linalg.qr(rng.standard_normal((32, 32)))
+    d = (q1 * 3.0 ** -np.arange(32.0)) @ q2.T
+    got = device_ops.compress_dense(d, TruncationControl(1e-6))
+    assert got.k == 13
+    assert _spec(got.value() - d) <= 1e-6 * _spec(d)
+
+
+def test_add_truncated_contract_matches_oracle_ranks():
+    """Criterion 2 of the reference acceptance suite (500 random additions,
+    seed 2024), plus rank equality with the oracle on every case."""
+    rng = np.random.default_rng(2024)
+    for i in range(500):
+        eps = 1e-4 if i % 2 == 0 else 1e-8
+        m, n = int(rng.integers(8, 257)), int(rng.integers(8, 257))
+        k1, k2 = int(rng.integers(0, 9)), int(rng.integers(0, 9))
+        x1 = _lr(rng, m, n, k1)
+        x2 = _lr(rng, m, n, k2)
+        ctl = TruncationControl(eps)
+        got = device_ops.add_truncated(x1, x2, ctl)
+        ref = orc.add_truncated(x1, x2, ctl)
+        assert got.k == ref.k, f"case {i}: rank {got.k} vs {ref.k}"
+        exact = x1.value() + x2.value()
+        assert _spec(got.value() - exact) <= eps * _spec(exact) + 1e-300
+
+
+def test_recompress_tall(rng):
+    """Multi-chunk TSQR path (m, n up to 2500 rows)."""
+    for m, n, k in [(2500, 300, 20), (700, 1900, 31), (90, 90, 40)]:
+        x = LowRank(rng.standard_normal((m, k)) @ np.diag(2.0 ** -np.arange(k)), rng.standard_normal((n, k)))
+        ctl = TruncationControl(1e-6)
+        got = device_ops.recompress(x, ctl)
+        ref = orc.recompress(x, ctl)
+        assert got.k == ref.k
+        assert np.linalg.norm(got.value() - ref.value()) <= 1e-10 * np.linalg.norm(ref.value())
+
+
+# ---- whole factorizations vs the reference fixtures ------------------------------
+
+
+@pytest.mark.parametrize("name", GOLDEN_CASES)
+def test_factorization_parity(name):
+    g = cases.golden(name)
+    build, ctl = cases.CASES[name]
+    h, _ = build()
+    plan = make_plan(h, TruncationControl(*ctl))
+    hlu_factorize(plan)
+    ranks = cases.ranks(h)
+    assert np.array_equal(ranks, g["ranks_out"]), f"{int((ranks != g['ranks_out']).sum())} ranks differ"
+    assert abs(plan.flops.total - float(g["flops"])) <= 1e-12 * float(g["flops"])
+    nrm, gn = cases.leaf_norms(h), g["norms_out"]
+    assert np.max(np.abs(nrm - gn) / np.maximum(gn, 1e-300)) <= 1e-8
+    if "flat_out" in g:
+        f = hmatrix.flatten(h)
+        assert np.linalg.norm(f - g["flat_out"]) <= 1e-11 * np.linalg.norm(g["flat_out"])
+    # forward solve on the GPU factors vs the reference forward solve on its factors
+    y = forward_solve(h, g["rhs"])
+    rel = np.linalg.norm(y - g["y_forward"]) / np.linalg.norm(g["y_forward"])
+    assert rel <= 1e-8, rel
+
+
+@pytest.mark.parametrize("name", ["sphere_1024", "bem1d_1024", "mixed_192"])
+def test_solve_parity(name):
+    build, ctl = cases.CASES[name]
+    h, _ = build()
+    ref = h.copy()
+    orc.hlu_factorize(ref, TruncationControl(*ctl))
+    hlu_factorize(make_plan(h, TruncationControl(*ctl)))
+    b = np.random.default_rng(0).standard_normal(h.rows)
+    x = hlu_solve(h, b)
+    xr = orc.hlu_solve(ref, b)
+    assert np.linalg.norm(x - xr) <= 1e-8 * np.linalg.norm(xr)
+
+
+def test_singular_pivot_names_block():
+    from paper_1906_00874_b200.blocks import build_diagonal_2x2_tree
+    from paper_1906_00874_b200.hmatrix import build_hmatrix
+
+    h = build_hmatrix(build_diagonal_2x2_tree(8, 1)[0])
+    with pytest.raises(SingularBlockError) as err:
+        hlu_factorize(make_plan(h))
+    assert "lu[0:4)" in str(err.value)
