@@ -111,7 +111,10 @@ typedef struct {
   int32_t out_slot, log;
   int64_t out_a, out_b;  /* column-major outputs, ld = m / n, capacity cap columns */
   int64_t ws;            /* workspace offset in the pool (TSQR reflectors) */
-} hlu_rkt_desc; /* 56 bytes */
+  int32_t handoff;       /* scratch: set by the KM=32 kernel when the op's runtime stacked rank
+                            exceeds 32, consumed (and reset to 0) by the KM=64 kernel */
+  int32_t pad;
+} hlu_rkt_desc; /* 64 bytes */
 
 /* launch kinds of a schedule entry */
 enum { HLU_K_GETRF = 0, HLU_K_TRSM = 1, HLU_K_GEMM = 2, HLU_K_RKT32 = 3, HLU_K_RKT64 = 4 };
@@ -129,7 +132,7 @@ int hlu_getrf_batched_f64(const hlu_ctx *ctx, const hlu_getrf_desc *d, int count
 int hlu_trsm_batched_f64(const hlu_ctx *ctx, const hlu_trsm_desc *d, int count, int max_n, void *stream);
 int hlu_gemm_batched_f64(const hlu_ctx *ctx, const hlu_gemm_desc *d, const hlu_term *terms, int count,
                          void *stream);
-int hlu_rk_update_batched_f64(const hlu_ctx *ctx, const hlu_rkt_desc *d, const hlu_rkpart *parts,
+int hlu_rk_update_batched_f64(const hlu_ctx *ctx, hlu_rkt_desc *d, const hlu_rkpart *parts,
                               int count, int kclass, void *stream);
 
 /* TSQR workspace (doubles) one truncation needs for an m-row factor of width <= K */
@@ -142,7 +145,7 @@ typedef struct hlu_schedule hlu_schedule;
  * outlive the schedule; use_graph: capture the launch sequence into a CUDA graph */
 int hlu_schedule_create(hlu_schedule **out, const hlu_ctx *ctx, const hlu_launch *launches, int64_t nlaunch,
                         const hlu_getrf_desc *getrf, const hlu_trsm_desc *trsm, const hlu_gemm_desc *gemm,
-                        const hlu_term *terms, const hlu_rkt_desc *rkt, const hlu_rkpart *parts,
+                        const hlu_term *terms, hlu_rkt_desc *rkt, const hlu_rkpart *parts,
                         int use_graph, void *stream);
 int hlu_schedule_launch(hlu_schedule *s, void *stream);
 int hlu_schedule_destroy(hlu_schedule *s);

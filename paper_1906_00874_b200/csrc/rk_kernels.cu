@@ -294,7 +294,7 @@ __device__ void jacobi(double *G, double *V, int p, int q) {
 
 template <int KM>
 __global__ void __launch_bounds__(HLU_NT)
-    k_rkt(hlu_ctx c, const hlu_rkt_desc *__restrict__ d, const hlu_rkpart *__restrict__ parts) {
+    k_rkt(hlu_ctx c, hlu_rkt_desc *__restrict__ d, const hlu_rkpart *__restrict__ parts) {
   using Cfg = RkCfg<KM>;
   extern __shared__ double sm[];
   double *S = sm;                 // BUFD
@@ -329,9 +329,19 @@ __global__ void __launch_bounds__(HLU_NT)
   double *outA = c.pool + o.out_a;
   double *outB = c.pool + o.out_b;
 
-  // which kernel variant owns this op: K <= 32 -> KM=32; 32 < K -> KM=64
-  const bool mine = (KM == 32) ? (K <= 32) : (K > 32);
-  if (!mine) return;
+  // Variant hand-off.  Both variants are launched over the same level; the
+  // KM=32 one decides from the INPUT ranks (the KM=64 launch would see ranks
+  // the KM=32 launch already updated) and flags the ops it leaves behind.
+  if (KM == 32) {
+    if (K > 32) {
+      if (tid == 0) d[blockIdx.x].handoff = 64;
+      return;
+    }
+  } else {
+    if (o.handoff != 64) return;
+    __syncthreads();
+    if (tid == 0) d[blockIdx.x].handoff = 0;
+  }
   if (o.mode == HLU_RK_ADD) {
     const int k1 = P[0].k, k2 = P[1].k;
     if (tid == 0 && o.log >= 0) {
@@ -467,7 +477,7 @@ extern "C" int64_t hlu_rkt_ws_doubles(int32_t m, int32_t kbound) {
   return a > b ? a : b;
 }
 
-extern "C" int hlu_rk_update_batched_f64(const hlu_ctx *ctx, const hlu_rkt_desc *d, const hlu_rkpart *parts,
+extern "C" int hlu_rk_update_batched_f64(const hlu_ctx *ctx, hlu_rkt_desc *d, const hlu_rkpart *parts,
                                          int count, int kclass, void *stream) {
   static bool init = false;
   if (!init) {

@@ -17,7 +17,7 @@ struct hlu_schedule {
   const hlu_trsm_desc *trsm;
   const hlu_gemm_desc *gemm;
   const hlu_term *terms;
-  const hlu_rkt_desc *rkt;
+  hlu_rkt_desc *rkt;
   const hlu_rkpart *parts;
   cudaGraph_t graph;
   cudaGraphExec_t exec;
@@ -53,7 +53,7 @@ static int run_launches(hlu_schedule *s, cudaStream_t st) {
 
 extern "C" int hlu_schedule_create(hlu_schedule **out, const hlu_ctx *ctx, const hlu_launch *launches,
                                    int64_t nlaunch, const hlu_getrf_desc *getrf, const hlu_trsm_desc *trsm,
-                                   const hlu_gemm_desc *gemm, const hlu_term *terms, const hlu_rkt_desc *rkt,
+                                   const hlu_gemm_desc *gemm, const hlu_term *terms, hlu_rkt_desc *rkt,
                                    const hlu_rkpart *parts, int use_graph, void *stream) {
   hlu_schedule *s = new hlu_schedule();
   s->ctx = *ctx;

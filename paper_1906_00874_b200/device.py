@@ -63,6 +63,9 @@ class DeviceCall:
         fill_pool(layout, host_pool, host_ranks, extras)
         self.h2d_bytes = host_pool.nbytes + host_ranks.nbytes
         with torch.cuda.device(self.device):
+            # a dedicated stream: the legacy default stream cannot be graph-captured
+            self.stream = torch.cuda.Stream(self.device)
+        with torch.cuda.device(self.device), torch.cuda.stream(self.stream):
             self.pool = torch.empty(self.total, dtype=torch.float64, device=self.device)
             self.host_pool = torch.from_numpy(host_pool).pin_memory()
             self.host_ranks = torch.from_numpy(host_ranks).pin_memory()
@@ -81,7 +84,6 @@ class DeviceCall:
                 self.pool.data_ptr(), self.ranks.data_ptr(), self.log.data_ptr(), self.err.data_ptr(),
                 self.dlog.data_ptr(), float(ctl.eps), -1 if ctl.kmax is None else int(ctl.kmax), 0,
             )
-            self.stream = torch.cuda.current_stream(self.device)
             handle = ctypes.c_void_p()
             launches = np.ascontiguousarray(p.launches)
             rc = lib.hlu_schedule_create(
@@ -98,28 +100,37 @@ class DeviceCall:
     def upload(self):
         """Host (pinned) -> device copy of payloads and ranks; resets error words."""
         n = self.L.payload_doubles
-        self.pool[:n].copy_(self.host_pool, non_blocking=True)
-        self.ranks.copy_(self.host_ranks, non_blocking=True)
-        self.err.copy_(self.torch.tensor([0, INT32_MAX, 0, 0], dtype=self.torch.int32), non_blocking=True)
+        with self.torch.cuda.stream(self.stream):
+            self.pool[:n].copy_(self.host_pool, non_blocking=True)
+            self.ranks.copy_(self.host_ranks, non_blocking=True)
+            self.err[0] = 0
+            self.err[1] = INT32_MAX
+            self.err[2] = 0
 
     def snapshot(self):
         """Device-resident pristine copy, for repeated timed runs."""
         n = self.L.payload_doubles
-        self._pristine = (self.pool[:n].clone(), self.ranks.clone())
+        with self.torch.cuda.stream(self.stream):
+            self._pristine = (self.pool[:n].clone(), self.ranks.clone())
 
     def restore(self):
         n = self.L.payload_doubles
-        self.pool[:n].copy_(self._pristine[0])
-        self.ranks.copy_(self._pristine[1])
-        self.err[0] = 0
-        self.err[1] = INT32_MAX
-        self.err[2] = 0
+        with self.torch.cuda.stream(self.stream):
+            self.pool[:n].copy_(self._pristine[0])
+            self.ranks.copy_(self._pristine[1])
+            self.err[0] = 0
+            self.err[1] = INT32_MAX
+            self.err[2] = 0
 
     def launch(self):
         rc = self.lib.hlu_schedule_launch(self.handle, ctypes.c_void_p(self.stream.cuda_stream))
         _native.check(rc, "hlu_schedule_launch")
 
+    def sync(self):
+        self.stream.synchronize()
+
     def check_errors(self):
+        self.sync()
         err = self.err.cpu().numpy()
         if err[1] != INT32_MAX:
             op_id = int(err[1])
@@ -137,6 +148,7 @@ class DeviceCall:
     def download(self):
         """Device -> host: install results into the H-matrix; returns d2h bytes."""
         n = self.L.payload_doubles
+        self.sync()
         pool = self.pool[:n].cpu().numpy()
         ranks = self.ranks.cpu().numpy()
         read_pool(self.L, pool, ranks)
@@ -147,6 +159,7 @@ class DeviceCall:
         return read_extra(self.L, self._last_pool, name)
 
     def flops(self):
+        self.sync()
         return effective_flops(self.packed, self.log.cpu().numpy())
 
     def close(self):

@@ -97,7 +97,7 @@ def _truncate_parts(parts_pairs, m, n, ctl, mode, signs=None):
     parts = np.zeros(len(recs), dtype=ir.RKPART)
     parts[:] = recs
     d = np.zeros(1, dtype=ir.RKT)
-    d[0] = (mode, 0, len(recs), m, n, cap, slot, 0, out_a, out_b, wso)
+    d[0] = (mode, 0, len(recs), m, n, cap, slot, 0, out_a, out_b, wso, 0, 0)
     t = None
 
     def fn(lib, ctx, stream):

@@ -22,13 +22,13 @@ GEMM = np.dtype([("term_begin", "<i4"), ("term_count", "<i4"), ("log", "<i4"), (
 RKPART = np.dtype([("a", VIEW), ("b", VIEW), ("sign", "<f8"), ("roff", "<i4"), ("coff", "<i4")])
 RKT = np.dtype([("mode", "<i4"), ("part_begin", "<i4"), ("part_count", "<i4"), ("m", "<i4"),
                 ("n", "<i4"), ("cap", "<i4"), ("out_slot", "<i4"), ("log", "<i4"),
-                ("out_a", "<i8"), ("out_b", "<i8"), ("ws", "<i8")])
+                ("out_a", "<i8"), ("out_b", "<i8"), ("ws", "<i8"), ("handoff", "<i4"), ("pad", "<i4")])
 LAUNCH = np.dtype([("kind", "<i4"), ("count", "<i4"), ("first", "<i8"), ("smem_dim", "<i4"),
                    ("pad", "<i4")])
 
 assert VIEW.itemsize == 32 and GETRF.itemsize == 40 and TRSM.itemsize == 72
 assert TERM.itemsize == 144 and GEMM.itemsize == 16 and RKPART.itemsize == 80
-assert RKT.itemsize == 56 and LAUNCH.itemsize == 24
+assert RKT.itemsize == 64 and LAUNCH.itemsize == 24
 
 # kinds (hlu_b200.h)
 K_GETRF, K_TRSM, K_GEMM, K_RKT32, K_RKT64 = 0, 1, 2, 3, 4

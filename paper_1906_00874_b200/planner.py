@@ -39,6 +39,8 @@ from .ir import (
 
 TEMP_SHIFT = 40  # virtual address of temp t: (t + 1) << TEMP_SHIFT
 DEFAULT_CAP = 32
+IDENT = 64     # identity block edge kept in the pool
+KMAX_STACK = 64  # largest stacked rank the truncation kernel handles
 
 
 def _label(kind, rows, cols):
@@ -155,6 +157,9 @@ class Layout:
                 off += (x.rows + x.cols) * self.cap
                 nrk += 1
         self.nslots = len(self.leaves)
+        # identity block, for truncating explicit dense products as (I, D^T)
+        self.ident_off = off
+        off += IDENT * IDENT
         self.extra = {}
         for name, rows, cols in extra:  # additional dense objects (e.g. a solve vector)
             self.extra[name] = (off, rows, cols, self.nslots)
@@ -335,7 +340,24 @@ class Planner:
             return Pair(T, fb), reads, [t]
         if not _part(a) and not _part(b):
             av, bv = self.dense_view(a), self.dense_view(b)
-            p = self.rkt(RK_RECOMPRESS, [Pair(av, bv.T)], av.rows, bv.cols, reads=reads, defer=True)
+            m, kin, n = av.rows, av.cols, bv.cols
+            if kin <= KMAX_STACK:  # compress_dense(A @ B) as the factor pair (A, B^T)
+                p = self.rkt(RK_RECOMPRESS, [Pair(av, bv.T)], m, n, reads=reads, defer=True)
+                return p, reads, [self._pair_temp(p)]
+            # wide inner dimension: form D = A @ B, then truncate (I, D^T) or (D, I)
+            if min(m, n) > IDENT:
+                raise StructureError(f"dense product {m}x{kin}x{n} exceeds the truncation kernel")
+            t, base = self._temp(m * n)
+            D = View(base, m, n, 1, m)
+            terms = [(TERM_ZERO, D, NULL_VIEW, NULL_VIEW, NULL_VIEW, 0.0, 0),
+                     (TERM_GEMM, D, av, NULL_VIEW, bv, 1.0, 0)]
+            self.gemm_op(terms, reads, [self._temp_res(t)], defer=True, temps_out=[t])
+            I = self.L.ident_off
+            if m <= n:
+                part = Pair(View(I, m, m, 1, IDENT), D.T)
+            else:
+                part = Pair(D, View(I, n, n, 1, IDENT))
+            p = self.rkt(RK_RECOMPRESS, [part], m, n, reads=reads, temps_in=[t], defer=True)
             return p, reads, [self._pair_temp(p)]
         rows = _row_cuts(a) if _part(a) else [_rr(a)]
         cols = _col_cuts(b) if _part(b) else [_cc(b)]

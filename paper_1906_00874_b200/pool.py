@@ -35,6 +35,9 @@ def fill_pool(layout, pool, ranks, extras=None):
             pool[a_off : a_off + m * k] = lf.data.a.ravel(order="F")
             pool[b_off : b_off + n * k] = lf.data.b.ravel(order="F")
             ranks[slot] = k
+    from .planner import IDENT
+
+    pool[layout.ident_off : layout.ident_off + IDENT * IDENT] = np.eye(IDENT).ravel()
     for name, arr in (extras or {}).items():
         off, rows, cols, _ = layout.extra[name]
         pool[off : off + rows * cols] = np.asarray(arr, dtype=float).reshape(rows, cols).ravel(order="F")

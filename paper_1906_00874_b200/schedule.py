@@ -190,7 +190,7 @@ def pack(pl: Planner, arena_base: int):
             pb = len(parts)
             for a, b, sign, roff, coff in pts:
                 parts.append((fv(a), fv(b), sign, roff, coff))
-            rkt.append((mode, pb, len(pts), m, n, cap, slot, log, fix(out_a), fix(out_b), fix(ws) if ws else 0))
+            rkt.append((mode, pb, len(pts), m, n, cap, slot, log, fix(out_a), fix(out_b), fix(ws) if ws else 0, 0, 0))
             kind, idx, dim = ir.K_RKT32, len(rkt) - 1, kb
         key = (lv, kind)
         if cur is not None and cur[0] == key:
