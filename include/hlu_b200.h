@@ -153,6 +153,7 @@ int hlu_schedule_destroy(hlu_schedule *s);
 /* library identity / sanity */
 const char *hlu_version(void);
 int hlu_device_check(void); /* 0 when a sm_100 device is present */
+int64_t hlu_debug_sweeps(int reset); /* total Jacobi sweeps run so far (diagnostics) */
 
 #ifdef __cplusplus
 }

@@ -24,6 +24,7 @@ SYMBOLS = (
     "hlu_schedule_destroy",
     "hlu_version",
     "hlu_device_check",
+    "hlu_debug_sweeps",
 )
 
 

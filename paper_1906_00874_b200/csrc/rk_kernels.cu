@@ -234,6 +234,8 @@ __device__ void apply_q(int m, int K, int kk, const double *W, double *T, const 
   __syncthreads();
 }
 
+__device__ unsigned long long g_sweeps = 0;  // total Jacobi sweeps (diagnostics)
+
 __device__ __forceinline__ int rr_player(int pos, int r, int qq) {
   return pos == 0 ? 0 : 1 + (pos - 1 + r) % (qq - 1);
 }
@@ -286,7 +288,10 @@ __device__ void jacobi(double *G, double *V, int p, int q) {
       }
       __syncthreads();
     }
-    if (s_rot == 0) break;
+    if (s_rot == 0) {
+      if (tid == 0) atomicAdd(&g_sweeps, sweep + 1);
+      break;
+    }
     __syncthreads();
   }
   __syncthreads();
@@ -467,6 +472,16 @@ static size_t rkt_smem() {
 }  // namespace hlu
 
 using namespace hlu;
+
+extern "C" int64_t hlu_debug_sweeps(int reset) {
+  unsigned long long v = 0;
+  cudaMemcpyFromSymbol(&v, g_sweeps, sizeof(v));
+  if (reset) {
+    unsigned long long z = 0;
+    cudaMemcpyToSymbol(g_sweeps, &z, sizeof(z));
+  }
+  return (int64_t)v;
+}
 
 extern "C" int64_t hlu_rkt_ws_doubles(int32_t m, int32_t kbound) {
   // the variant that runs an op depends on its runtime K; take the larger need
