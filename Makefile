@@ -18,3 +18,8 @@ ptxas:
 clean:
 	rm -f $(LIB)
 .PHONY: all clean ptxas
+
+PLAN := paper_1906_00874_b200/libhlu_plan.so
+all: $(PLAN)
+$(PLAN): paper_1906_00874_b200/csrc/planner.cpp include/hlu_plan.h include/hlu_b200.h
+	g++ -O2 -std=c++17 -fPIC -shared -Iinclude paper_1906_00874_b200/csrc/planner.cpp -o $@

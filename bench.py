@@ -166,9 +166,8 @@ def run_ours(args):
     import torch.distributed as dist
 
     from paper_1906_00874_b200 import TruncationControl
-    from paper_1906_00874_b200.hlu import _auto_capacity
+    from paper_1906_00874_b200.hlu import _auto_capacity, plan_call
     from paper_1906_00874_b200.device import DeviceCall
-    from paper_1906_00874_b200.planner import Layout, Planner
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -185,10 +184,8 @@ def run_ours(args):
     template = h.copy()
     t0 = time.perf_counter()
     cap = _auto_capacity([h], ctl)
-    layout = Layout(h, cap=cap)
-    pl = Planner(layout)
-    pl.factor(h)
-    call = DeviceCall(layout, pl, ctl, device=f"cuda:{local}", use_graph=True)
+    layout, packed = plan_call([h], [("factor", h)], cap)
+    call = DeviceCall(layout, packed, ctl, device=f"cuda:{local}", use_graph=True)
     t_plan = time.perf_counter() - t0
     call.launch()
     call.check_errors()  # RankOverflow here would need a larger capacity
@@ -270,7 +267,7 @@ def run_ours(args):
                    "n": CONFIGS[cfg][1], "factor_time_s": t_step, "effective_flops": flops,
                    "l2": "flushed (256 MiB write) before every timed step",
                    "parallelism": "replicas only" if world > 1 else "single GPU",
-                   "levels": call.packed.nlevels, "ops": len(pl.ops),
+                   "levels": call.packed.nlevels, "ops": len(packed.flop_formula),
                    "assembly_s": t_asm, "plan_s": t_plan, "rank_capacity": cap},
         "e2e": {"value": world * flops / t_e2e / 1e9, "unit": "GFLOP/s", "time_s": t_e2e,
                 "h2d_bytes_per_step": int(call.h2d_bytes),

@@ -1,0 +1,65 @@
+/*
+ * hlu_plan.h — C ABI of the native planner / level scheduler (host code).
+ *
+ * Replaces the reference's executor seam (hlu.py:315-354, ex.leaf/ex.parent)
+ * and its task runtime (runtime.py:380-556) for the GPU: the recursion of
+ * hlu.py:400-658 is replayed into typed device ops (hlu_b200.h descriptors),
+ * levelled by skeleton-slot hazards and packed per (level, kernel) launch.
+ */
+#ifndef HLU_PLAN_H
+#define HLU_PLAN_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* One H-matrix node (flattened tree).  Children of a partitioned node are
+ * nodes child0 .. child0 + nr*nc - 1 in row-major grid order. */
+typedef struct {
+  int32_t kind;            /* 0 dense leaf, 1 Rk leaf, 2 partitioned */
+  int32_t r0, r1, c0, c1;  /* global row / column ranges */
+  int32_t nr, nc;          /* grid (partitioned) */
+  int32_t child0;          /* first child, -1 for leaves */
+  int32_t lo, hi;          /* skeleton slot interval */
+  int32_t slot;            /* rank slot (Rk leaves), -1 otherwise */
+  int32_t pad;
+  int64_t off_a;           /* dense payload / Rk left factor offset in the pool */
+  int64_t off_b;           /* Rk right factor offset */
+} hlu_plan_node;           /* 64 bytes */
+
+enum {
+  HLU_CMD_FACTOR = 0,      /* a = root */
+  HLU_CMD_SOLVE_LOWER = 1, /* a = l, b = b   : b := l^-1 b */
+  HLU_CMD_SOLVE_UPPER = 2, /* a = b, b = u   : b := b u^-1 */
+  HLU_CMD_UPDATE = 3,      /* a = c, b = a, c = b : c := c - a b */
+  HLU_CMD_FWD_VEC = 4,     /* a = factored root, vector at vec_off (resource vec_res) */
+  HLU_CMD_BWD_VEC = 5
+};
+
+typedef struct {
+  int32_t kind, a, b, c;
+  int64_t vec_off;
+  int32_t vec_cols, pad;
+  int64_t vec_res;
+} hlu_plan_cmd; /* 40 bytes */
+
+typedef struct hlu_plan hlu_plan;
+
+int hlu_plan_build(hlu_plan **out, const hlu_plan_node *nodes, int64_t nnodes, const hlu_plan_cmd *cmds,
+                   int64_t ncmds, int32_t cap, int64_t ident_off, int64_t nslots, int32_t nrk, int64_t arena_base);
+const char *hlu_plan_error(const hlu_plan *p);
+/* sizes[14]: getrf, trsm, gemm, terms, rkt, parts, launches, ops, levels, arena doubles,
+ *            log entries, rank slots, LU count, temps */
+int hlu_plan_sizes(const hlu_plan *p, int64_t *sizes);
+int hlu_plan_copy(const hlu_plan *p, void *getrf, void *trsm, void *gemm, void *terms, void *rkt, void *parts,
+                  void *launches, int32_t *flop_formula, double *flop_coef, int64_t *flop_log, int64_t *lu_op_ids,
+                  int64_t *lu_nodes, int64_t *op_levels);
+void hlu_plan_free(hlu_plan *p);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* HLU_PLAN_H */

@@ -1,0 +1,1138 @@
+// Native planner + level scheduler (host C++).
+//
+// A line-by-line port of planner.py / schedule.py (which stay as the readable,
+// tested specification): it replays the reference H-LU recursion
+// (hlu.py:400-658) into typed device ops, levels them by skeleton-slot and
+// temp hazards, allocates the temp arena and packs the descriptor arrays.
+// tests/test_native_planner.py checks that both produce byte-identical packed
+// arrays.  The Python planner takes ~75 s per 5.6M reference tasks (cfg3);
+// this one takes a few seconds.
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <limits>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "hlu_b200.h"
+#include "hlu_plan.h"
+
+namespace {
+
+constexpr int64_t TEMP_SHIFT = 40;
+constexpr int KMAX_STACK = 64;
+constexpr int IDENT = 64;
+constexpr int F_STATIC = 0, F_LIN = 1, F_RKUPD = 2, F_QUAD = 3;
+
+struct View {
+  int64_t off;
+  int32_t rows, cols, rs, cs, rdyn, cdyn;
+  View T() const { return View{off, cols, rows, cs, rs, cdyn, rdyn}; }
+  View rows_slice(int i0, int i1) const {
+    if (rdyn >= 0 || i0 < 0 || i1 > rows || i0 > i1) throw std::runtime_error("bad rows_slice");
+    return View{off + (int64_t)i0 * rs, i1 - i0, cols, rs, cs, rdyn, cdyn};
+  }
+  View cols_slice(int j0, int j1) const {
+    if (cdyn >= 0 || j0 < 0 || j1 > cols || j0 > j1) throw std::runtime_error("bad cols_slice");
+    return View{off + (int64_t)j0 * cs, rows, j1 - j0, rs, cs, rdyn, cdyn};
+  }
+};
+const View NULLV{0, 0, 0, 0, 0, -1, -1};
+
+inline hlu_view hv(const View &v) {
+  hlu_view o;
+  o.off = v.off;
+  o.rows = v.rows;
+  o.cols = v.cols;
+  o.rs = v.rs;
+  o.cs = v.cs;
+  o.rdyn = v.rdyn;
+  o.cdyn = v.cdyn;
+  return o;
+}
+
+struct Pair {
+  View a, b;
+  double sign = 1.0;
+  int roff = 0, coff = 0;
+};
+
+struct Opnd {  // an H-node or a window of a leaf, in global coordinates
+  int node;
+  int r0, r1, c0, c1;
+  bool win;
+};
+
+struct Iv {
+  int64_t lo, hi;
+};
+
+struct Term {
+  int kind;
+  View c, a, m, b;
+  double alpha;
+  int assoc;
+};
+
+struct Op {
+  int kind;  // 0 getrf, 1 trsm, 2 gemm, 3 rkt
+  bool defer;
+  int64_t payload;  // index into the kind's payload store
+  int64_t r_begin, r_end, w_begin, w_end;  // into ivs
+  int64_t ti_begin, ti_end, to_begin, to_end;  // into tids
+  int flop_f;
+  double flop_c;
+  int64_t flop_log;
+};
+
+struct GetrfP {
+  View a;
+  int op_id, lu_index;
+};
+struct TrsmP {
+  View t, x;
+  int mode, log;
+};
+struct GemmP {
+  int64_t tb, tn;
+  int log, log_slot;
+};
+struct RktP {
+  int mode;
+  int64_t pb, pn;
+  int m, n, cap, slot, log;
+  int64_t out_a, out_b, ws;
+  int kb;
+};
+
+int64_t ws_one(int m, int k, int ch) {
+  if (m <= 0 || k <= 0) return 0;
+  const int64_t nch = (m + ch - 1) / ch;
+  return nch * ((int64_t)(k + ch) * k + k);
+}
+int chunk_rows(int km) { return (km == 32 ? 4608 : 9216) / km - km; }
+int64_t rkt_ws(int m, int kb) {
+  const int64_t a = ws_one(m, std::min(kb, 32), chunk_rows(32));
+  const int64_t b = ws_one(m, std::min(kb, 64), chunk_rows(64));
+  return std::max(a, b);
+}
+
+struct Planner {
+  const hlu_plan_node *N;
+  int64_t nnodes;
+  int cap;
+  int64_t ident_off;
+  int64_t nslots;
+  int nrank;
+
+  std::vector<Op> ops;
+  std::vector<Iv> ivs;
+  std::vector<int64_t> tids;
+  std::vector<int64_t> temp_size;
+  int64_t nlog = 0;
+  std::vector<GetrfP> getrf;
+  std::vector<TrsmP> trsm;
+  std::vector<GemmP> gemm;
+  std::vector<Term> terms;
+  std::vector<RktP> rkt;
+  std::vector<Pair> parts;
+  std::vector<int64_t> lu_ops, lu_nodes;
+
+  const hlu_plan_node &nd(int i) const { return N[i]; }
+  bool part(const Opnd &o) const { return !o.win && nd(o.node).kind == 2; }
+  bool rk(const Opnd &o) const { return nd(o.node).kind == 1; }
+  Opnd whole(int i) const { const auto &x = nd(i); return Opnd{i, x.r0, x.r1, x.c0, x.c1, false}; }
+  int child(int i, int r, int c) const { const auto &x = nd(i); return x.child0 + r * x.nc + c; }
+  Opnd window(const Opnd &o, int r0, int r1, int c0, int c1) const {
+    if (part(o)) throw std::runtime_error("cannot window a partitioned block");
+    const auto &x = nd(o.node);
+    if (!o.win && r0 == x.r0 && r1 == x.r1 && c0 == x.c0 && c1 == x.c1) return o;
+    return Opnd{o.node, r0, r1, c0, c1, true};
+  }
+  Iv res(const Opnd &o) const { const auto &x = nd(o.node); return Iv{x.lo, x.hi}; }
+  std::vector<std::pair<int, int>> row_cuts(int i) const {
+    const auto &x = nd(i);
+    std::vector<std::pair<int, int>> v;
+    for (int r = 0; r < x.nr; ++r) { const auto &c = nd(child(i, r, 0)); v.push_back({c.r0, c.r1}); }
+    return v;
+  }
+  std::vector<std::pair<int, int>> col_cuts(int i) const {
+    const auto &x = nd(i);
+    std::vector<std::pair<int, int>> v;
+    for (int c = 0; c < x.nc; ++c) { const auto &y = nd(child(i, 0, c)); v.push_back({y.c0, y.c1}); }
+    return v;
+  }
+
+  int64_t temp(int64_t doubles, int64_t *base) {
+    const int64_t t = (int64_t)temp_size.size();
+    temp_size.push_back(doubles);
+    *base = (t + 1) << TEMP_SHIFT;
+    return t;
+  }
+  Iv temp_res(int64_t t) const { return Iv{nslots + t, nslots + t + 1}; }
+  int rank_slot() { return nrank++; }
+  int64_t log(int n = 1) { const int64_t i = nlog; nlog += n; return i; }
+  static int64_t pair_temp(const Pair &p) { return (p.a.off >> TEMP_SHIFT) - 1; }
+
+  View dense_view(const Opnd &o) const {
+    const auto &x = nd(o.node);
+    const int rows = x.r1 - x.r0;
+    return View{x.off_a + (o.r0 - x.r0) + (int64_t)(o.c0 - x.c0) * rows, o.r1 - o.r0, o.c1 - o.c0, 1, rows, -1, -1};
+  }
+  void factor_views(const Opnd &o, View *a, View *b) const {
+    const auto &x = nd(o.node);
+    const int rows = x.r1 - x.r0, cols = x.c1 - x.c0;
+    *a = View{x.off_a + (o.r0 - x.r0), o.r1 - o.r0, cap, 1, rows, -1, x.slot};
+    *b = View{x.off_b + (o.c0 - x.c0), o.c1 - o.c0, cap, 1, cols, -1, x.slot};
+  }
+
+  int64_t emit(int kind, bool defer, int64_t payload, const std::vector<Iv> &reads, const std::vector<Iv> &writes,
+               const std::vector<int64_t> &tin, const std::vector<int64_t> &tout, int ff, double fc, int64_t fl) {
+    Op o;
+    o.kind = kind;
+    o.defer = defer;
+    o.payload = payload;
+    o.r_begin = (int64_t)ivs.size();
+    ivs.insert(ivs.end(), reads.begin(), reads.end());
+    o.r_end = o.w_begin = (int64_t)ivs.size();
+    ivs.insert(ivs.end(), writes.begin(), writes.end());
+    o.w_end = (int64_t)ivs.size();
+    o.ti_begin = (int64_t)tids.size();
+    tids.insert(tids.end(), tin.begin(), tin.end());
+    o.ti_end = o.to_begin = (int64_t)tids.size();
+    tids.insert(tids.end(), tout.begin(), tout.end());
+    o.to_end = (int64_t)tids.size();
+    o.flop_f = ff;
+    o.flop_c = fc;
+    o.flop_log = fl;
+    ops.push_back(o);
+    return (int64_t)ops.size() - 1;
+  }
+
+  // ---------------------------------------------------------- term emitters
+  void terms_matmat(std::vector<Term> &ts, const View &dst, const Opnd &op, const View &x, double alpha) {
+    if (part(op)) {
+      const auto &p = nd(op.node);
+      for (int r = 0; r < p.nr; ++r)
+        for (int c = 0; c < p.nc; ++c) {
+          const int ch = child(op.node, r, c);
+          const auto &q = nd(ch);
+          terms_matmat(ts, dst.rows_slice(q.r0 - p.r0, q.r1 - p.r0), whole(ch), x.rows_slice(q.c0 - p.c0, q.c1 - p.c0), alpha);
+        }
+    } else if (rk(op)) {
+      View fa, fb;
+      factor_views(op, &fa, &fb);
+      ts.push_back(Term{2, dst, fa, fb.T(), x, alpha, 0});
+    } else {
+      ts.push_back(Term{1, dst, dense_view(op), NULLV, x, alpha, 0});
+    }
+  }
+  void terms_tmatmat(std::vector<Term> &ts, const View &dst, const Opnd &op, const View &x, double alpha) {
+    if (part(op)) {
+      const auto &p = nd(op.node);
+      for (int r = 0; r < p.nr; ++r)
+        for (int c = 0; c < p.nc; ++c) {
+          const int ch = child(op.node, r, c);
+          const auto &q = nd(ch);
+          terms_tmatmat(ts, dst.rows_slice(q.c0 - p.c0, q.c1 - p.c0), whole(ch), x.rows_slice(q.r0 - p.r0, q.r1 - p.r0), alpha);
+        }
+    } else if (rk(op)) {
+      View fa, fb;
+      factor_views(op, &fa, &fb);
+      ts.push_back(Term{2, dst, fb, fa.T(), x, alpha, 0});
+    } else {
+      ts.push_back(Term{1, dst, dense_view(op).T(), NULLV, x, alpha, 0});
+    }
+  }
+  void terms_rmatmat(std::vector<Term> &ts, const View &dst, const View &x, const Opnd &op, double alpha) {
+    if (part(op)) {
+      const auto &p = nd(op.node);
+      for (int r = 0; r < p.nr; ++r)
+        for (int c = 0; c < p.nc; ++c) {
+          const int ch = child(op.node, r, c);
+          const auto &q = nd(ch);
+          terms_rmatmat(ts, dst.cols_slice(q.c0 - p.c0, q.c1 - p.c0), x.cols_slice(q.r0 - p.r0, q.r1 - p.r0), whole(ch), alpha);
+        }
+    } else if (rk(op)) {
+      View fa, fb;
+      factor_views(op, &fa, &fb);
+      ts.push_back(Term{2, dst, x, fa, fb.T(), alpha, 1});
+    } else {
+      ts.push_back(Term{1, dst, x, NULLV, dense_view(op), alpha, 0});
+    }
+  }
+
+  int64_t gemm_op(const std::vector<Term> &ts, const std::vector<Iv> &reads, const std::vector<Iv> &writes, int ff,
+                  double fc, int log_slot, bool defer, const std::vector<int64_t> &tout,
+                  const std::vector<int64_t> &tin) {
+    int64_t lg = -1;
+    if (ff == F_LIN || ff == F_QUAD) lg = log();
+    GemmP g{(int64_t)terms.size(), (int64_t)ts.size(), (int)lg, log_slot};
+    terms.insert(terms.end(), ts.begin(), ts.end());
+    gemm.push_back(g);
+    return emit(2, defer, (int64_t)gemm.size() - 1, reads, writes, tin, tout, ff, fc, lg);
+  }
+
+  // ---------------------------------------------------------- truncation
+  bool rkt_op(int mode, const std::vector<Pair> &ps, int m, int n, int out_node, const std::vector<Iv> &reads,
+              const std::vector<int64_t> &tin, bool defer, bool has_flop, double flop_mn, Pair *res) {
+    int kb = 0;
+    for (const auto &p : ps) kb += p.a.cols;
+    std::vector<int64_t> tout;
+    std::vector<Iv> writes;
+    int64_t out_a, out_b;
+    int slot;
+    if (out_node < 0) {
+      int64_t base;
+      const int64_t t = temp((int64_t)(m + n) * cap, &base);
+      slot = rank_slot();
+      out_a = base;
+      out_b = base + (int64_t)m * cap;
+      tout.push_back(t);
+      writes.push_back(temp_res(t));
+      res->a = View{out_a, m, cap, 1, m, -1, slot};
+      res->b = View{out_b, n, cap, 1, n, -1, slot};
+      res->sign = 1.0;
+      res->roff = res->coff = 0;
+    } else {
+      const auto &x = nd(out_node);
+      out_a = x.off_a;
+      out_b = x.off_b;
+      slot = x.slot;
+      writes.push_back(Iv{x.lo, x.hi});
+    }
+    const int64_t wsn = rkt_ws(m, kb) + rkt_ws(n, kb);
+    int64_t ws = 0;
+    if (wsn) {
+      const int64_t tw = temp(wsn, &ws);
+      tout.push_back(tw);
+    }
+    const int64_t lg = log(3);
+    RktP r;
+    r.mode = mode;
+    r.pb = (int64_t)parts.size();
+    r.pn = (int64_t)ps.size();
+    parts.insert(parts.end(), ps.begin(), ps.end());
+    r.m = m;
+    r.n = n;
+    r.cap = cap;
+    r.slot = slot;
+    r.log = (int)lg;
+    r.out_a = out_a;
+    r.out_b = out_b;
+    r.ws = ws;
+    r.kb = kb;
+    rkt.push_back(r);
+    emit(3, defer, (int64_t)rkt.size() - 1, reads, writes, tin, tout, has_flop ? F_RKUPD : F_STATIC,
+         has_flop ? flop_mn : 0.0, has_flop ? lg : -1);
+    return out_node < 0;
+  }
+
+  // ---------------------------------------------------------- products
+  Pair product(const Opnd &a, const Opnd &b, const std::vector<Iv> *ctx, std::vector<Iv> *reads_out,
+               std::vector<int64_t> *tps) {
+    std::vector<Iv> reads = ctx ? *ctx : std::vector<Iv>{res(a), res(b)};
+    *reads_out = reads;
+    tps->clear();
+    if (!part(a) && rk(a)) {
+      View fa, fb;
+      factor_views(a, &fa, &fb);
+      const int n = b.c1 - b.c0;
+      int64_t base;
+      const int64_t t = temp((int64_t)n * cap, &base);
+      const View T{base, n, cap, 1, n, -1, fa.cdyn};
+      std::vector<Term> ts{Term{0, T, NULLV, NULLV, NULLV, 0.0, 0}};
+      terms_tmatmat(ts, T, b, fb, 1.0);
+      gemm_op(ts, reads, {temp_res(t)}, F_STATIC, 0.0, -1, true, {t}, {});
+      tps->push_back(t);
+      return Pair{fa, T, 1.0, 0, 0};
+    }
+    if (!part(b) && rk(b)) {
+      View fa, fb;
+      factor_views(b, &fa, &fb);
+      const int m = a.r1 - a.r0;
+      int64_t base;
+      const int64_t t = temp((int64_t)m * cap, &base);
+      const View T{base, m, cap, 1, m, -1, fa.cdyn};
+      std::vector<Term> ts{Term{0, T, NULLV, NULLV, NULLV, 0.0, 0}};
+      terms_matmat(ts, T, a, fa, 1.0);
+      gemm_op(ts, reads, {temp_res(t)}, F_STATIC, 0.0, -1, true, {t}, {});
+      tps->push_back(t);
+      return Pair{T, fb, 1.0, 0, 0};
+    }
+    if (!part(a) && !part(b)) {
+      const View av = dense_view(a), bv = dense_view(b);
+      const int m = av.rows, kin = av.cols, n = bv.cols;
+      Pair p;
+      if (kin <= KMAX_STACK) {
+        rkt_op(1, {Pair{av, bv.T(), 1.0, 0, 0}}, m, n, -1, reads, {}, true, false, 0.0, &p);
+        tps->push_back(pair_temp(p));
+        return p;
+      }
+      if (std::min(m, n) > IDENT) throw std::runtime_error("dense product exceeds the truncation kernel");
+      int64_t base;
+      const int64_t t = temp((int64_t)m * n, &base);
+      const View D{base, m, n, 1, m, -1, -1};
+      std::vector<Term> ts{Term{0, D, NULLV, NULLV, NULLV, 0.0, 0}, Term{1, D, av, NULLV, bv, 1.0, 0}};
+      gemm_op(ts, reads, {temp_res(t)}, F_STATIC, 0.0, -1, true, {t}, {});
+      Pair part_;
+      if (m <= n) part_ = Pair{View{ident_off, m, m, 1, IDENT, -1, -1}, D.T(), 1.0, 0, 0};
+      else part_ = Pair{D, View{ident_off, n, n, 1, IDENT, -1, -1}, 1.0, 0, 0};
+      rkt_op(1, {part_}, m, n, -1, reads, {t}, true, false, 0.0, &p);
+      tps->push_back(pair_temp(p));
+      return p;
+    }
+    std::vector<std::pair<int, int>> rows = part(a) ? row_cuts(a.node) : std::vector<std::pair<int, int>>{{a.r0, a.r1}};
+    std::vector<std::pair<int, int>> cols = part(b) ? col_cuts(b.node) : std::vector<std::pair<int, int>>{{b.c0, b.c1}};
+    if (part(a) && part(b) && col_cuts(a.node) != row_cuts(b.node))
+      throw std::runtime_error("inner partitions of a product do not match");
+    std::vector<std::pair<int, int>> mids = part(a) ? col_cuts(a.node) : row_cuts(b.node);
+    std::vector<Pair> grid;
+    std::vector<std::vector<int64_t>> gtemps;
+    for (size_t i = 0; i < rows.size(); ++i) {
+      for (size_t j = 0; j < cols.size(); ++j) {
+        bool have = false;
+        Pair acc;
+        std::vector<int64_t> acc_t;
+        for (size_t p = 0; p < mids.size(); ++p) {
+          const Opnd ap = part(a) ? whole(child(a.node, (int)i, (int)p))
+                                  : window(a, rows[i].first, rows[i].second, mids[p].first, mids[p].second);
+          const Opnd bp = part(b) ? whole(child(b.node, (int)p, (int)j))
+                                  : window(b, mids[p].first, mids[p].second, cols[j].first, cols[j].second);
+          std::vector<Iv> rd;
+          std::vector<int64_t> tp;
+          const Pair pp = product(ap, bp, &reads, &rd, &tp);
+          if (!have) {
+            acc = pp;
+            acc_t = tp;
+            have = true;
+            continue;
+          }
+          std::vector<int64_t> tin = acc_t;
+          tin.insert(tin.end(), tp.begin(), tp.end());
+          Pair out;
+          rkt_op(0, {acc, pp}, rows[i].second - rows[i].first, cols[j].second - cols[j].first, -1, reads, tin, false,
+                 false, 0.0, &out);
+          acc = out;
+          acc_t = {pair_temp(out)};
+        }
+        grid.push_back(acc);
+        gtemps.push_back(acc_t);
+      }
+    }
+    if (rows.size() == 1 && cols.size() == 1) {
+      *tps = gtemps[0];
+      return grid[0];
+    }
+    const int m = rows.back().second - rows.front().first;
+    const int n = cols.back().second - cols.front().first;
+    std::vector<Pair> ps;
+    std::vector<int64_t> tin;
+    for (size_t i = 0; i < rows.size(); ++i)
+      for (size_t j = 0; j < cols.size(); ++j) {
+        const Pair &acc = grid[i * cols.size() + j];
+        ps.push_back(Pair{acc.a, acc.b, acc.sign, rows[i].first - rows[0].first, cols[j].first - cols[0].first});
+        const auto &tt = gtemps[i * cols.size() + j];
+        tin.insert(tin.end(), tt.begin(), tt.end());
+      }
+    Pair merged;
+    rkt_op(1, ps, m, n, -1, reads, tin, false, false, 0.0, &merged);
+    tps->assign(1, pair_temp(merged));
+    return merged;
+  }
+
+  // ---------------------------------------------------------- update
+  void update(const Opnd &c, const Opnd &a, const Opnd &b) {
+    if (!c.win && nd(c.node).kind == 1) {
+      std::vector<Iv> reads;
+      std::vector<int64_t> tps;
+      const Pair p = product(a, b, nullptr, &reads, &tps);
+      const auto &x = nd(c.node);
+      const int m = x.r1 - x.r0, n = x.c1 - x.c0;
+      View ca, cb;
+      factor_views(c, &ca, &cb);
+      reads.push_back(res(c));
+      Pair dummy;
+      rkt_op(0, {Pair{ca, cb, 1.0, 0, 0}, Pair{p.a, p.b, -p.sign, 0, 0}}, m, n, c.node, reads, tps, false, true,
+             (double)(m + n), &dummy);
+      return;
+    }
+    const bool cp = part(c), ap = part(a), bp = part(b);
+    if (!(cp || ap || bp)) {
+      update_dense(c, a, b);
+      return;
+    }
+    std::vector<std::pair<int, int>> rows, cols, mids;
+    if (cp) rows = row_cuts(c.node);
+    else if (ap) rows = row_cuts(a.node);
+    else rows = {{c.r0, c.r1}};
+    if (cp) cols = col_cuts(c.node);
+    else if (bp) cols = col_cuts(b.node);
+    else cols = {{c.c0, c.c1}};
+    if (ap && bp && col_cuts(a.node) != row_cuts(b.node))
+      throw std::runtime_error("inner partitions of an update do not match");
+    if (ap) mids = col_cuts(a.node);
+    else if (bp) mids = row_cuts(b.node);
+    else mids = {{a.c0, a.c1}};
+    for (size_t i = 0; i < rows.size(); ++i)
+      for (size_t j = 0; j < cols.size(); ++j) {
+        const Opnd cij = cp ? whole(child(c.node, (int)i, (int)j))
+                            : window(c, rows[i].first, rows[i].second, cols[j].first, cols[j].second);
+        for (size_t p = 0; p < mids.size(); ++p) {
+          const Opnd aa = ap ? whole(child(a.node, (int)i, (int)p))
+                             : window(a, rows[i].first, rows[i].second, mids[p].first, mids[p].second);
+          const Opnd bb = bp ? whole(child(b.node, (int)p, (int)j))
+                             : window(b, mids[p].first, mids[p].second, cols[j].first, cols[j].second);
+          update(cij, aa, bb);
+        }
+      }
+  }
+
+  void update_dense(const Opnd &c, const Opnd &a, const Opnd &b) {
+    const View dst = dense_view(c);
+    const int m = dst.rows, n = dst.cols;
+    const std::vector<Iv> reads{res(a), res(b)};
+    const std::vector<Iv> writes{res(c)};
+    if (!rk(a) && !rk(b)) {
+      const View av = dense_view(a), bv = dense_view(b);
+      gemm_op({Term{1, dst, av, NULLV, bv, -1.0, 0}}, reads, writes, F_STATIC, 2.0 * m * n * av.cols, -1, false, {}, {});
+    } else if (rk(a)) {
+      View fa, fb;
+      factor_views(a, &fa, &fb);
+      int64_t base;
+      const int64_t t = temp((int64_t)n * cap, &base);
+      const View T{base, n, cap, 1, n, -1, fa.cdyn};
+      std::vector<Term> ts{Term{0, T, NULLV, NULLV, NULLV, 0.0, 0}};
+      terms_tmatmat(ts, T, b, fb, 1.0);
+      ts.push_back(Term{1, dst, fa, NULLV, T.T(), -1.0, 0});
+      gemm_op(ts, reads, writes, F_LIN, 2.0 * (m + n) * n, fa.cdyn, false, {t}, {});
+    } else {
+      View fa, fb;
+      factor_views(b, &fa, &fb);
+      int64_t base;
+      const int64_t t = temp((int64_t)m * cap, &base);
+      const View T{base, m, cap, 1, m, -1, fa.cdyn};
+      std::vector<Term> ts{Term{0, T, NULLV, NULLV, NULLV, 0.0, 0}};
+      terms_matmat(ts, T, a, fa, 1.0);
+      ts.push_back(Term{1, dst, T, NULLV, fb.T(), -1.0, 0});
+      gemm_op(ts, reads, writes, F_LIN, 2.0 * (m + n) * m, fa.cdyn, false, {t}, {});
+    }
+  }
+
+  // ---------------------------------------------------------- trsm
+  void trsm_op(const View &t, const View &x, int mode, const std::vector<Iv> &reads, const std::vector<Iv> &writes,
+               double coef, bool dyn) {
+    const int64_t lg = dyn ? log() : -1;
+    trsm.push_back(TrsmP{t, x, mode, (int)lg});
+    emit(1, false, (int64_t)trsm.size() - 1, reads, writes, {}, {}, dyn ? F_LIN : F_STATIC, coef, dyn ? lg : -1);
+  }
+
+  void solve_lower(int l, int b) {
+    const auto &L = nd(l), &B = nd(b);
+    if (L.kind == 0) {
+      const View lv = dense_view(whole(l));
+      const std::vector<Iv> rd{Iv{L.lo, L.hi}}, wr{Iv{B.lo, B.hi}};
+      const int lr = L.r1 - L.r0;
+      if (B.kind == 0) {
+        trsm_op(lv, dense_view(whole(b)), 0, rd, wr, (double)lr * lr * (B.c1 - B.c0), false);
+      } else if (B.kind == 1) {
+        View fa, fb;
+        factor_views(whole(b), &fa, &fb);
+        trsm_op(lv, fa, 0, rd, wr, (double)lr * lr, true);
+      } else {
+        throw std::runtime_error("dense factor against partitioned right-hand side");
+      }
+      return;
+    }
+    if (B.kind == 2) {
+      const int nr = L.nr, nc = B.nc;
+      for (int i = 0; i < nr; ++i) {
+        for (int p = 0; p < i; ++p)
+          for (int j = 0; j < nc; ++j)
+            update(whole(child(b, i, j)), whole(child(l, i, p)), whole(child(b, p, j)));
+        for (int j = 0; j < nc; ++j) solve_lower(child(l, i, i), child(b, i, j));
+      }
+      return;
+    }
+    lower_panel(l, b, B.r0, B.r1);
+  }
+
+  View panel_view(int bleaf, int part_, int axis, int lo, int hi) const {
+    const auto &B = nd(bleaf);
+    if (part_ == 0) {
+      const View v = dense_view(whole(bleaf));
+      return axis == 0 ? v.rows_slice(lo - B.r0, hi - B.r0) : v.cols_slice(lo - B.c0, hi - B.c0);
+    }
+    View fa, fb;
+    factor_views(whole(bleaf), &fa, &fb);
+    if (part_ == 1) return fa.rows_slice(lo - B.r0, hi - B.r0);
+    return fb.rows_slice(lo - B.c0, hi - B.c0);
+  }
+
+  void lower_panel(int l, int bleaf, int lo, int hi) {
+    const auto &B = nd(bleaf);
+    const int part_ = B.kind == 0 ? 0 : 1;
+    const auto &L = nd(l);
+    const std::vector<Iv> rd{Iv{L.lo, L.hi}}, wr{Iv{B.lo, B.hi}};
+    if (L.kind == 0) {
+      const View x = panel_view(bleaf, part_, 0, lo, hi);
+      const bool dyn = part_ == 1;
+      const int lr = L.r1 - L.r0;
+      trsm_op(dense_view(whole(l)), x, 0, rd, wr, (double)lr * lr * (dyn ? 1 : x.cols), dyn);
+      return;
+    }
+    const auto cuts = row_cuts(l);
+    for (size_t i = 0; i < cuts.size(); ++i) {
+      for (size_t p = 0; p < i; ++p) {
+        const int lip = child(l, (int)i, (int)p);
+        const View dst = panel_view(bleaf, part_, 0, cuts[i].first, cuts[i].second);
+        const View src = panel_view(bleaf, part_, 0, cuts[p].first, cuts[p].second);
+        std::vector<Term> ts;
+        terms_matmat(ts, dst, whole(lip), src, -1.0);
+        const std::vector<Iv> rl{Iv{nd(lip).lo, nd(lip).hi}};
+        if (part_ == 1)
+          gemm_op(ts, rl, wr, F_LIN, 2.0 * dst.rows * src.rows, dst.cdyn, false, {}, {});
+        else
+          gemm_op(ts, rl, wr, F_STATIC, 2.0 * dst.rows * dst.cols * src.rows, -1, false, {}, {});
+      }
+      lower_panel(child(l, (int)i, (int)i), bleaf, cuts[i].first, cuts[i].second);
+    }
+  }
+
+  void solve_upper(int b, int u) {
+    const auto &U = nd(u), &B = nd(b);
+    if (U.kind == 0) {
+      const View uv = dense_view(whole(u));
+      const std::vector<Iv> rd{Iv{U.lo, U.hi}}, wr{Iv{B.lo, B.hi}};
+      const int ur = U.r1 - U.r0;
+      if (B.kind == 0) {
+        trsm_op(uv, dense_view(whole(b)), 1, rd, wr, (double)ur * ur * (B.r1 - B.r0), false);
+      } else if (B.kind == 1) {
+        View fa, fb;
+        factor_views(whole(b), &fa, &fb);
+        trsm_op(uv, fb.T(), 1, rd, wr, (double)ur * ur, true);
+      } else {
+        throw std::runtime_error("dense factor against partitioned right-hand side");
+      }
+      return;
+    }
+    if (B.kind == 2) {
+      const int nc = U.nc, nr = B.nr;
+      for (int j = 0; j < nc; ++j) {
+        for (int p = 0; p < j; ++p)
+          for (int i = 0; i < nr; ++i) update(whole(child(b, i, j)), whole(child(b, i, p)), whole(child(u, p, j)));
+        for (int i = 0; i < nr; ++i) solve_upper(child(b, i, j), child(u, j, j));
+      }
+      return;
+    }
+    upper_panel(b, u, B.c0, B.c1);
+  }
+
+  void upper_panel(int bleaf, int u, int lo, int hi) {
+    const auto &B = nd(bleaf), &U = nd(u);
+    const bool dense = B.kind == 0;
+    const int part_ = dense ? 0 : 2, axis = dense ? 1 : 0;
+    const std::vector<Iv> rd{Iv{U.lo, U.hi}}, wr{Iv{B.lo, B.hi}};
+    if (U.kind == 0) {
+      const View x = panel_view(bleaf, part_, axis, lo, hi);
+      const int ur = U.r1 - U.r0;
+      if (dense) trsm_op(dense_view(whole(u)), x, 1, rd, wr, (double)ur * ur * x.rows, false);
+      else trsm_op(dense_view(whole(u)), x.T(), 1, rd, wr, (double)ur * ur, true);
+      return;
+    }
+    const auto cuts = col_cuts(u);
+    for (size_t j = 0; j < cuts.size(); ++j) {
+      for (size_t p = 0; p < j; ++p) {
+        const int upj = child(u, (int)p, (int)j);
+        const View dst = panel_view(bleaf, part_, axis, cuts[j].first, cuts[j].second);
+        const View src = panel_view(bleaf, part_, axis, cuts[p].first, cuts[p].second);
+        std::vector<Term> ts;
+        const std::vector<Iv> ru{Iv{nd(upj).lo, nd(upj).hi}};
+        if (dense) {
+          terms_rmatmat(ts, dst, src, whole(upj), -1.0);
+          gemm_op(ts, ru, wr, F_STATIC, 2.0 * dst.rows * dst.cols * src.cols, -1, false, {}, {});
+        } else {
+          terms_tmatmat(ts, dst, whole(upj), src, -1.0);
+          gemm_op(ts, ru, wr, F_QUAD, 2.0 * dst.rows, dst.cdyn, false, {}, {});
+        }
+      }
+      upper_panel(bleaf, child(u, (int)j, (int)j), cuts[j].first, cuts[j].second);
+    }
+  }
+
+  void factor(int h) {
+    const auto &H = nd(h);
+    if (H.kind == 0) {
+      if (H.r1 - H.r0 != H.c1 - H.c0) throw std::runtime_error("LU requires a square block");
+      const int idx = (int)lu_ops.size();
+      lu_nodes.push_back(h);
+      getrf.push_back(GetrfP{dense_view(whole(h)), (int)ops.size(), idx});
+      const double n = H.r1 - H.r0;
+      lu_ops.push_back(emit(0, false, (int64_t)getrf.size() - 1, {}, {Iv{H.lo, H.hi}}, {}, {}, F_STATIC,
+                            2.0 / 3.0 * (n * n * n), -1));
+      return;
+    }
+    if (H.kind == 1) throw std::runtime_error("diagonal block is low-rank; expected dense");
+    if (H.nr != H.nc) throw std::runtime_error("LU requires a square grid");
+    const int nb = H.nr;
+    for (int k = 0; k < nb; ++k) {
+      factor(child(h, k, k));
+      for (int j = k + 1; j < nb; ++j) solve_lower(child(h, k, k), child(h, k, j));
+      for (int i = k + 1; i < nb; ++i) solve_upper(child(h, i, k), child(h, k, k));
+      for (int i = k + 1; i < nb; ++i)
+        for (int j = k + 1; j < nb; ++j) update(whole(child(h, i, j)), whole(child(h, i, k)), whole(child(h, k, j)));
+    }
+  }
+
+  // vector solves (forward = reference panel route; backward = restated)
+  void vec_lower(int l, const View &x, int base, const Iv &res_) {
+    const auto &L = nd(l);
+    if (L.kind == 0) {
+      trsm_op(dense_view(whole(l)), x, 0, {Iv{L.lo, L.hi}}, {res_}, 0.0, false);
+      return;
+    }
+    const auto cuts = row_cuts(l);
+    for (size_t i = 0; i < cuts.size(); ++i) {
+      for (size_t p = 0; p < i; ++p) {
+        std::vector<Term> ts;
+        const int lip = child(l, (int)i, (int)p);
+        terms_matmat(ts, x.rows_slice(cuts[i].first - base, cuts[i].second - base), whole(lip),
+                     x.rows_slice(cuts[p].first - base, cuts[p].second - base), -1.0);
+        gemm_op(ts, {Iv{nd(lip).lo, nd(lip).hi}}, {res_}, F_STATIC, 0.0, -1, false, {}, {});
+      }
+      vec_lower(child(l, (int)i, (int)i), x.rows_slice(cuts[i].first - base, cuts[i].second - base), cuts[i].first,
+                res_);
+    }
+  }
+  void vec_upper(int u, const View &x, int base, const Iv &res_) {
+    const auto &U = nd(u);
+    if (U.kind == 0) {
+      trsm_op(dense_view(whole(u)), x, 2, {Iv{U.lo, U.hi}}, {res_}, 0.0, false);
+      return;
+    }
+    const auto cuts = row_cuts(u);
+    const int nb = (int)cuts.size();
+    for (int i = nb - 1; i >= 0; --i) {
+      for (int p = i + 1; p < nb; ++p) {
+        std::vector<Term> ts;
+        const int uip = child(u, i, p);
+        terms_matmat(ts, x.rows_slice(cuts[i].first - base, cuts[i].second - base), whole(uip),
+                     x.rows_slice(cuts[p].first - base, cuts[p].second - base), -1.0);
+        gemm_op(ts, {Iv{nd(uip).lo, nd(uip).hi}}, {res_}, F_STATIC, 0.0, -1, false, {}, {});
+      }
+      vec_upper(child(u, i, i), x.rows_slice(cuts[i].first - base, cuts[i].second - base), cuts[i].first, res_);
+    }
+  }
+
+  // ---------------------------------------------------------- schedule
+  std::vector<int64_t> levels;
+  std::vector<int64_t> toffs;
+  int64_t arena = 0;
+
+  // Hazard state: slots in segment trees (reads can span whole partitioned
+  // operands, writes are single leaves or temps), temps in flat arrays.
+  struct MaxTree {  // point assign, range max
+    int64_t n = 1;
+    std::vector<int64_t> t;
+    void init(int64_t m) { while (n < m) n <<= 1; t.assign(2 * n, -1); }
+    void set(int64_t i, int64_t v) { i += n; t[i] = v; for (i >>= 1; i; i >>= 1) t[i] = std::max(t[2 * i], t[2 * i + 1]); }
+    int64_t query(int64_t lo, int64_t hi) const {
+      int64_t r = -1;
+      for (lo += n, hi += n; lo < hi; lo >>= 1, hi >>= 1) {
+        if (lo & 1) r = std::max(r, t[lo++]);
+        if (hi & 1) r = std::max(r, t[--hi]);
+      }
+      return r;
+    }
+  };
+  struct TagTree {  // range chmax, point query
+    int64_t n = 1;
+    std::vector<int64_t> t;
+    void init(int64_t m) { while (n < m) n <<= 1; t.assign(2 * n, -1); }
+    void chmax(int64_t lo, int64_t hi, int64_t v) {
+      for (lo += n, hi += n; lo < hi; lo >>= 1, hi >>= 1) {
+        if (lo & 1) { t[lo] = std::max(t[lo], v); ++lo; }
+        if (hi & 1) { --hi; t[hi] = std::max(t[hi], v); }
+      }
+    }
+    int64_t get(int64_t i) const {
+      int64_t r = -1;
+      for (i += n; i; i >>= 1) r = std::max(r, t[i]);
+      return r;
+    }
+  };
+
+  void assign_levels() {
+    const int64_t nt = (int64_t)temp_size.size();
+    MaxTree lw;
+    TagTree lr;
+    lw.init(std::max<int64_t>(nslots, 1));
+    lr.init(std::max<int64_t>(nslots, 1));
+    // point values of slots are also kept flat for the single-slot fast path
+    std::vector<int64_t> lw_s(nslots, -1);
+    std::vector<int64_t> lwT(nt, -1), lrT(nt, -1);
+    levels.assign(ops.size(), 0);
+    std::vector<std::pair<int64_t, int64_t>> pending;
+    auto constraint = [&](const Op &o) {
+      int64_t c = 0;
+      for (int64_t i = o.r_begin; i < o.r_end; ++i) {
+        const Iv &v = ivs[i];
+        if (v.lo >= nslots) c = std::max(c, lwT[v.lo - nslots] + 1);
+        else if (v.hi - v.lo == 1) c = std::max(c, lw_s[v.lo] + 1);
+        else c = std::max(c, lw.query(v.lo, v.hi) + 1);
+      }
+      for (int64_t i = o.ti_begin; i < o.ti_end; ++i) c = std::max(c, lwT[tids[i]] + 1);
+      for (int64_t i = o.w_begin; i < o.w_end; ++i) {
+        const Iv &v = ivs[i];
+        if (v.lo >= nslots) {
+          const int64_t t = v.lo - nslots;
+          c = std::max(c, std::max(lwT[t], lrT[t]) + 1);
+        } else {
+          for (int64_t s = v.lo; s < v.hi; ++s) c = std::max(c, std::max(lw_s[s], lr.get(s)) + 1);
+        }
+      }
+      return c;
+    };
+    auto commit = [&](const Op &o, int64_t lv) {
+      for (int64_t i = o.r_begin; i < o.r_end; ++i) {
+        const Iv &v = ivs[i];
+        if (v.lo >= nslots) lrT[v.lo - nslots] = std::max(lrT[v.lo - nslots], lv);
+        else lr.chmax(v.lo, v.hi, lv);
+      }
+      for (int64_t i = o.ti_begin; i < o.ti_end; ++i) lrT[tids[i]] = std::max(lrT[tids[i]], lv);
+      for (int64_t i = o.w_begin; i < o.w_end; ++i) {
+        const Iv &v = ivs[i];
+        if (v.lo >= nslots) {
+          lwT[v.lo - nslots] = lv;
+        } else {
+          for (int64_t s = v.lo; s < v.hi; ++s) {
+            lw_s[s] = lv;
+            lw.set(s, lv);
+          }
+        }
+      }
+    };
+    for (size_t i = 0; i < ops.size(); ++i) {
+      const Op &o = ops[i];
+      int64_t c = constraint(o);
+      if (o.defer) {
+        pending.push_back({(int64_t)i, c});
+        continue;
+      }
+      if (!pending.empty()) {
+        int64_t mx = 0;
+        for (auto &pp : pending) mx = std::max(mx, pp.second);
+        c = std::max(c, mx + 1);
+        for (auto &pp : pending) {
+          levels[pp.first] = c - 1;
+          commit(ops[pp.first], c - 1);
+        }
+        pending.clear();
+        c = std::max(c, constraint(o));
+      }
+      levels[i] = c;
+      commit(o, c);
+    }
+    for (auto &pp : pending) {
+      levels[pp.first] = pp.second;
+      commit(ops[pp.first], pp.second);
+    }
+  }
+
+  void allocate_temps() {
+    const int64_t nt = (int64_t)temp_size.size();
+    const int64_t BIG = std::numeric_limits<int64_t>::max();
+    std::vector<int64_t> birth(nt, BIG), death(nt, -1);
+    for (size_t i = 0; i < ops.size(); ++i) {
+      const Op &o = ops[i];
+      const int64_t lv = levels[i];
+      for (int64_t k = o.to_begin; k < o.to_end; ++k) {
+        birth[tids[k]] = std::min(birth[tids[k]], lv);
+        death[tids[k]] = std::max(death[tids[k]], lv);
+      }
+      for (int64_t k = o.ti_begin; k < o.ti_end; ++k) death[tids[k]] = std::max(death[tids[k]], lv);
+    }
+    std::vector<int> cls(nt);
+    for (int64_t t = 0; t < nt; ++t) {
+      const int64_t s = std::max<int64_t>(temp_size[t], 1);
+      int b = 0;
+      while ((int64_t(1) << b) < s) ++b;
+      cls[t] = std::max(6, b);
+    }
+    std::vector<int64_t> order(nt), by_death(nt);
+    for (int64_t t = 0; t < nt; ++t) order[t] = by_death[t] = t;
+    std::stable_sort(order.begin(), order.end(), [&](int64_t a, int64_t b) { return birth[a] < birth[b]; });
+    std::stable_sort(by_death.begin(), by_death.end(), [&](int64_t a, int64_t b) { return death[a] < death[b]; });
+    std::vector<std::vector<int64_t>> freel(64);
+    toffs.assign(nt, 0);
+    int64_t top = 0;
+    int64_t di = 0;
+    for (int64_t t : order) {
+      if (temp_size[t] == 0) continue;
+      const int64_t b = birth[t];
+      while (di < nt && death[by_death[di]] < b) {
+        const int64_t u = by_death[di++];
+        if (temp_size[u] && birth[u] <= death[u]) freel[cls[u]].push_back(toffs[u]);
+      }
+      auto &fl = freel[cls[t]];
+      if (!fl.empty()) {
+        toffs[t] = fl.back();
+        fl.pop_back();
+      } else {
+        toffs[t] = top;
+        top += int64_t(1) << cls[t];
+      }
+    }
+    arena = top;
+  }
+
+  // packed outputs
+  std::vector<hlu_getrf_desc> o_getrf;
+  std::vector<hlu_trsm_desc> o_trsm;
+  std::vector<hlu_gemm_desc> o_gemm;
+  std::vector<hlu_term> o_terms;
+  std::vector<hlu_rkt_desc> o_rkt;
+  std::vector<hlu_rkpart> o_parts;
+  std::vector<hlu_launch> o_launch;
+  int64_t nlevels = 0;
+
+  int64_t fix(int64_t off, int64_t arena_base) const {
+    if (off >= (int64_t(1) << TEMP_SHIFT)) {
+      const int64_t t = (off >> TEMP_SHIFT) - 1;
+      return arena_base + toffs[t] + (off & ((int64_t(1) << TEMP_SHIFT) - 1));
+    }
+    return off;
+  }
+  hlu_view fv(const View &v, int64_t ab) const {
+    hlu_view o = hv(v);
+    o.off = fix(v.off, ab);
+    return o;
+  }
+
+  void pack(int64_t arena_base) {
+    assign_levels();
+    allocate_temps();
+    const size_t n = ops.size();
+    std::vector<int64_t> order(n);
+    for (size_t i = 0; i < n; ++i) order[i] = (int64_t)i;
+    std::stable_sort(order.begin(), order.end(), [&](int64_t a, int64_t b) {
+      if (levels[a] != levels[b]) return levels[a] < levels[b];
+      return ops[a].kind < ops[b].kind;
+    });
+    struct Rec {
+      int kind;
+      int64_t count, first;
+      int dim;
+    };
+    std::vector<Rec> recs;
+    int64_t cur_lv = -1;
+    int cur_kind = -1;
+    for (int64_t i : order) {
+      const Op &o = ops[i];
+      const int64_t lv = levels[i];
+      int kind = 0, dim = 0;
+      int64_t idx = 0;
+      if (o.kind == 0) {
+        const GetrfP &g = getrf[o.payload];
+        hlu_getrf_desc d;
+        d.a = fv(g.a, arena_base);
+        d.op_id = g.op_id;
+        d.lu_index = g.lu_index;
+        o_getrf.push_back(d);
+        kind = HLU_K_GETRF;
+        idx = (int64_t)o_getrf.size() - 1;
+        dim = g.a.rows;
+      } else if (o.kind == 1) {
+        const TrsmP &t = trsm[o.payload];
+        hlu_trsm_desc d;
+        d.t = fv(t.t, arena_base);
+        d.x = fv(t.x, arena_base);
+        d.mode = t.mode;
+        d.log = t.log;
+        o_trsm.push_back(d);
+        kind = HLU_K_TRSM;
+        idx = (int64_t)o_trsm.size() - 1;
+        dim = t.t.rows;
+      } else if (o.kind == 2) {
+        const GemmP &g = gemm[o.payload];
+        hlu_gemm_desc d;
+        d.term_begin = (int32_t)o_terms.size();
+        d.term_count = (int32_t)g.tn;
+        d.log = g.log;
+        d.log_slot = g.log_slot;
+        for (int64_t k = g.tb; k < g.tb + g.tn; ++k) {
+          const Term &t = terms[k];
+          hlu_term h;
+          h.c = fv(t.c, arena_base);
+          h.a = fv(t.a, arena_base);
+          h.m = fv(t.m, arena_base);
+          h.b = fv(t.b, arena_base);
+          h.alpha = t.alpha;
+          h.kind = t.kind;
+          h.assoc = t.assoc;
+          o_terms.push_back(h);
+        }
+        o_gemm.push_back(d);
+        kind = HLU_K_GEMM;
+        idx = (int64_t)o_gemm.size() - 1;
+        dim = 0;
+      } else {
+        const RktP &r = rkt[o.payload];
+        hlu_rkt_desc d;
+        d.mode = r.mode;
+        d.part_begin = (int32_t)o_parts.size();
+        d.part_count = (int32_t)r.pn;
+        d.m = r.m;
+        d.n = r.n;
+        d.cap = r.cap;
+        d.out_slot = r.slot;
+        d.log = r.log;
+        d.out_a = fix(r.out_a, arena_base);
+        d.out_b = fix(r.out_b, arena_base);
+        d.ws = r.ws ? fix(r.ws, arena_base) : 0;
+        d.handoff = 0;
+        d.pad = 0;
+        for (int64_t k = r.pb; k < r.pb + r.pn; ++k) {
+          const Pair &p = parts[k];
+          hlu_rkpart q;
+          q.a = fv(p.a, arena_base);
+          q.b = fv(p.b, arena_base);
+          q.sign = p.sign;
+          q.roff = p.roff;
+          q.coff = p.coff;
+          o_parts.push_back(q);
+        }
+        o_rkt.push_back(d);
+        kind = HLU_K_RKT32;
+        idx = (int64_t)o_rkt.size() - 1;
+        dim = r.kb;
+      }
+      if (!recs.empty() && cur_lv == lv && cur_kind == kind) {
+        recs.back().count += 1;
+        recs.back().dim = std::max(recs.back().dim, dim);
+      } else {
+        recs.push_back(Rec{kind, 1, idx, dim});
+        cur_lv = lv;
+        cur_kind = kind;
+      }
+    }
+    for (const Rec &r : recs) {
+      hlu_launch L;
+      L.kind = r.kind;
+      L.count = (int32_t)r.count;
+      L.first = r.first;
+      L.pad = 0;
+      if (r.kind == HLU_K_RKT32) {
+        L.smem_dim = 0;
+        o_launch.push_back(L);
+        if (r.dim > 32) {
+          L.kind = HLU_K_RKT64;
+          o_launch.push_back(L);
+        }
+      } else {
+        L.smem_dim = r.dim;
+        o_launch.push_back(L);
+      }
+    }
+    nlevels = n ? (*std::max_element(levels.begin(), levels.end()) + 1) : 0;
+  }
+};
+
+}  // namespace
+
+struct hlu_plan {
+  Planner P;
+  std::string error;
+};
+
+extern "C" int hlu_plan_build(hlu_plan **out, const hlu_plan_node *nodes, int64_t nnodes, const hlu_plan_cmd *cmds,
+                              int64_t ncmds, int32_t cap, int64_t ident_off, int64_t nslots, int32_t nrk,
+                              int64_t arena_base) {
+  hlu_plan *p = new hlu_plan();
+  *out = p;
+  Planner &P = p->P;
+  P.N = nodes;
+  P.nnodes = nnodes;
+  P.cap = cap;
+  P.ident_off = ident_off;
+  P.nslots = nslots;
+  P.nrank = nrk;
+  try {
+    for (int64_t i = 0; i < ncmds; ++i) {
+      const hlu_plan_cmd &c = cmds[i];
+      switch (c.kind) {
+        case HLU_CMD_FACTOR: P.factor(c.a); break;
+        case HLU_CMD_SOLVE_LOWER: P.solve_lower(c.a, c.b); break;
+        case HLU_CMD_SOLVE_UPPER: P.solve_upper(c.a, c.b); break;
+        case HLU_CMD_UPDATE: P.update(P.whole(c.a), P.whole(c.b), P.whole(c.c)); break;
+        case HLU_CMD_FWD_VEC:
+        case HLU_CMD_BWD_VEC: {
+          const auto &x = nodes[c.a];
+          const View v{c.vec_off, x.r1 - x.r0, c.vec_cols, 1, x.r1 - x.r0, -1, -1};
+          const Iv r{c.vec_res, c.vec_res + 1};
+          if (c.kind == HLU_CMD_FWD_VEC) P.vec_lower(c.a, v, x.r0, r);
+          else P.vec_upper(c.a, v, x.r0, r);
+          break;
+        }
+        default: throw std::runtime_error("unknown plan command");
+      }
+    }
+    P.pack(arena_base);
+  } catch (const std::exception &e) {
+    p->error = e.what();
+    return -1;
+  }
+  return 0;
+}
+
+extern "C" const char *hlu_plan_error(const hlu_plan *p) { return p->error.c_str(); }
+
+extern "C" int hlu_plan_sizes(const hlu_plan *p, int64_t *s) {
+  const Planner &P = p->P;
+  s[0] = (int64_t)P.o_getrf.size();
+  s[1] = (int64_t)P.o_trsm.size();
+  s[2] = (int64_t)P.o_gemm.size();
+  s[3] = (int64_t)P.o_terms.size();
+  s[4] = (int64_t)P.o_rkt.size();
+  s[5] = (int64_t)P.o_parts.size();
+  s[6] = (int64_t)P.o_launch.size();
+  s[7] = (int64_t)P.ops.size();
+  s[8] = P.nlevels;
+  s[9] = P.arena;
+  s[10] = P.nlog;
+  s[11] = P.nrank;
+  s[12] = (int64_t)P.lu_ops.size();
+  s[13] = (int64_t)P.temp_size.size();
+  return 0;
+}
+
+template <class T>
+static void cp(void *dst, const std::vector<T> &v) {
+  if (dst && !v.empty()) std::memcpy(dst, v.data(), v.size() * sizeof(T));
+}
+
+extern "C" int hlu_plan_copy(const hlu_plan *p, void *getrf, void *trsm, void *gemm, void *terms, void *rkt,
+                             void *parts, void *launches, int32_t *flop_formula, double *flop_coef,
+                             int64_t *flop_log, int64_t *lu_op_ids, int64_t *lu_nodes, int64_t *op_levels) {
+  const Planner &P = p->P;
+  cp(getrf, P.o_getrf);
+  cp(trsm, P.o_trsm);
+  cp(gemm, P.o_gemm);
+  cp(terms, P.o_terms);
+  cp(rkt, P.o_rkt);
+  cp(parts, P.o_parts);
+  cp(launches, P.o_launch);
+  for (size_t i = 0; i < P.ops.size(); ++i) {
+    if (flop_formula) flop_formula[i] = P.ops[i].flop_f;
+    if (flop_coef) flop_coef[i] = P.ops[i].flop_c;
+    if (flop_log) flop_log[i] = P.ops[i].flop_log;
+    if (op_levels) op_levels[i] = P.levels[i];
+  }
+  cp(lu_op_ids, P.lu_ops);
+  cp(lu_nodes, P.lu_nodes);
+  return 0;
+}
+
+extern "C" void hlu_plan_free(hlu_plan *p) { delete p; }

@@ -46,16 +46,17 @@ def _dev_bytes(torch, arr, device):
 class DeviceCall:
     """One planned H-arithmetic call resident on the GPU."""
 
-    def __init__(self, layout, planner, ctl, device=None, use_graph=True, extras=None):
+    def __init__(self, layout, packed, ctl, device=None, use_graph=True, extras=None):
         torch = _torch()
         self.torch = torch
         self.device = torch.device(device if device is not None else "cuda")
         self.L = layout
-        self.pl = planner
         self.ctl = ctl
         lib = _native.lib()
         self.lib = lib
-        self.packed: Packed = pack(planner, layout.payload_doubles)
+        if not isinstance(packed, Packed):  # a Python Planner: pack it here
+            packed = pack(packed, layout.payload_doubles)
+        self.packed: Packed = packed
         p = self.packed
         self.total = layout.payload_doubles + p.arena_doubles
         host_pool = np.zeros(layout.payload_doubles, dtype=np.float64)

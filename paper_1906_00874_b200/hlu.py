@@ -88,17 +88,34 @@ def _auto_capacity(roots, ctl):
     return int(cap)
 
 
-def _run(roots, emit, ctl, capacity, device=None, use_graph=True, extras=None, keep=False):
+def plan_call(roots, commands, capacity, extras=None, planner="native"):
+    """Layout + packed schedule for a list of planner commands, e.g.
+    ``[("factor", h)]``; ``planner`` = "native" (C++) or "python" (the
+    reference-order specification the native planner is tested against)."""
+    layout = Layout(roots, cap=capacity, extra=[(k, v.shape[0], v.shape[1]) for k, v in (extras or {}).items()])
+    if planner == "native":
+        from . import native_plan
+
+        packed, _ = native_plan.plan(layout, commands)
+        return layout, packed
+    pl = Planner(layout)
+    for cmd in commands:
+        name = {"fwd": "forward_vector", "bwd": "backward_vector"}.get(cmd[0], cmd[0])
+        getattr(pl, name)(*cmd[1:])
+    from .schedule import pack
+
+    return layout, pack(pl, layout.payload_doubles)
+
+
+def _run(roots, commands, ctl, capacity, device=None, use_graph=True, extras=None, keep=False):
     """Plan + run one H-arithmetic call on the GPU, re-planning with a doubled
     capacity if any Rk result overflows.  Returns the DeviceCall."""
     from .device import DeviceCall, RankOverflow
 
     cap = capacity
     while True:
-        layout = Layout(roots, cap=cap, extra=[(k, v.shape[0], v.shape[1]) for k, v in (extras or {}).items()])
-        pl = Planner(layout)
-        emit(pl)
-        call = DeviceCall(layout, pl, ctl, device=device, use_graph=use_graph, extras=extras)
+        layout, packed = plan_call(roots, commands, cap, extras)
+        call = DeviceCall(layout, packed, ctl, device=device, use_graph=use_graph, extras=extras)
         call.launch()
         try:
             call.check_errors()
@@ -120,7 +137,7 @@ def hlu_factorize(plan: HluPlan):
     h = plan.matrix
     if h.rows != h.cols:
         raise StructureError("H-LU requires a square matrix")
-    call = _run([h], lambda pl: pl.factor(h), plan.truncation, plan.capacity, plan.device, plan.use_graph)
+    call = _run([h], [("factor", h)], plan.truncation, plan.capacity, plan.device, plan.use_graph)
     plan.flops.add(call.flops())
     plan.last_call = call
     return None
@@ -130,19 +147,19 @@ def solve_lower_hmatrix(l, b, ctl=None, runtime=None, skeleton=None):
     """b := l^-1 b (l holds a factored unit-lower part); ``runtime`` /
     ``skeleton`` are accepted for API compatibility."""
     ctl = ctl if ctl is not None else TruncationControl()
-    _run([l, b], lambda pl: pl.solve_lower(l, b), ctl, _auto_capacity([l, b], ctl))
+    _run([l, b], [("solve_lower", l, b)], ctl, _auto_capacity([l, b], ctl))
 
 
 def solve_upper_hmatrix(b, u, ctl=None, runtime=None, skeleton=None):
     """b := b u^-1."""
     ctl = ctl if ctl is not None else TruncationControl()
-    _run([b, u], lambda pl: pl.solve_upper(b, u), ctl, _auto_capacity([b, u], ctl))
+    _run([b, u], [("solve_upper", b, u)], ctl, _auto_capacity([b, u], ctl))
 
 
 def update_hmatrix(c, a, b, ctl=None, runtime=None, skeleton=None):
     """c := c - a @ b in H-arithmetic."""
     ctl = ctl if ctl is not None else TruncationControl()
-    _run([c, a, b], lambda pl: pl.update(c, a, b), ctl, _auto_capacity([c, a, b], ctl))
+    _run([c, a, b], [("update", c, a, b)], ctl, _auto_capacity([c, a, b], ctl))
 
 
 def hlu_solve(h: HMatrix, rhs, device=None):
@@ -151,12 +168,8 @@ def hlu_solve(h: HMatrix, rhs, device=None):
     rhs = np.asarray(rhs, dtype=float)
     vec = rhs.reshape(h.rows, -1)
 
-    def emit(pl):
-        pl.forward_vector(h, "x")
-        pl.backward_vector(h, "x")
-
-    call = _run([h], emit, TruncationControl(), _auto_capacity([h], None), device,
-                extras={"x": vec}, keep=True)
+    call = _run([h], [("fwd", h, "x"), ("bwd", h, "x")], TruncationControl(), _auto_capacity([h], None),
+                device, extras={"x": vec}, keep=True)
     x = call.extra("x")
     call.close()
     return x.reshape(rhs.shape)
@@ -166,7 +179,7 @@ def forward_solve(h: HMatrix, rhs, device=None):
     """y = L^-1 rhs (the reference's route: ``solve_lower_hmatrix`` with an
     n x 1 dense-leaf right-hand side)."""
     rhs = np.asarray(rhs, dtype=float)
-    call = _run([h], lambda pl: pl.forward_vector(h, "x"), TruncationControl(),
+    call = _run([h], [("fwd", h, "x")], TruncationControl(),
                 _auto_capacity([h], None), device, extras={"x": rhs.reshape(h.rows, -1)}, keep=True)
     y = call.extra("x")
     call.close()

@@ -1,0 +1,162 @@
+"""Binding of the native planner (``include/hlu_plan.h``, ``libhlu_plan.so``).
+
+Flattens the H-matrix trees of a call into ``hlu_plan_node`` records (pool
+offsets from the same ``Layout`` the Python planner uses) and returns the same
+``schedule.Packed`` record as ``schedule.pack(Planner)``.  The two planners
+are checked to produce byte-identical packed arrays
+(``tests/test_native_planner.py``).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+from . import ir
+from .blocks import PARTITIONED
+from .hmatrix import DENSE
+from .schedule import Packed
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+PLAN_LIB = os.path.join(_HERE, "libhlu_plan.so")
+
+NODE = np.dtype([("kind", "<i4"), ("r0", "<i4"), ("r1", "<i4"), ("c0", "<i4"), ("c1", "<i4"),
+                 ("nr", "<i4"), ("nc", "<i4"), ("child0", "<i4"), ("lo", "<i4"), ("hi", "<i4"),
+                 ("slot", "<i4"), ("pad", "<i4"), ("off_a", "<i8"), ("off_b", "<i8")])
+CMD = np.dtype([("kind", "<i4"), ("a", "<i4"), ("b", "<i4"), ("c", "<i4"), ("vec_off", "<i8"),
+                ("vec_cols", "<i4"), ("pad", "<i4"), ("vec_res", "<i8")])
+assert NODE.itemsize == 64 and CMD.itemsize == 40
+
+CMD_FACTOR, CMD_SOLVE_LOWER, CMD_SOLVE_UPPER, CMD_UPDATE, CMD_FWD_VEC, CMD_BWD_VEC = range(6)
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(PLAN_LIB):
+            raise RuntimeError(f"planner library {PLAN_LIB} missing: run `make`")
+        L = ctypes.CDLL(PLAN_LIB)
+        vp, i64, i32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32
+        L.hlu_plan_build.argtypes = [ctypes.POINTER(vp), vp, i64, vp, i64, i32, i64, i64, i32, i64]
+        L.hlu_plan_build.restype = ctypes.c_int
+        L.hlu_plan_error.argtypes = [vp]
+        L.hlu_plan_error.restype = ctypes.c_char_p
+        L.hlu_plan_sizes.argtypes = [vp, vp]
+        L.hlu_plan_copy.argtypes = [vp] * 14
+        L.hlu_plan_free.argtypes = [vp]
+        _lib = L
+    return _lib
+
+
+def flatten_nodes(layout):
+    """Node table over every root of the layout; returns (nodes, index of id(node))."""
+    recs = []
+    index = {}
+
+    def add(x):
+        index[id(x)] = len(recs)
+        recs.append(x)
+
+    for root in layout.roots:
+        if id(root) in index:
+            continue
+        add(root)
+        q = [root]
+        while q:
+            x = q.pop(0)
+            if x.kind == PARTITIONED:
+                for line in x.data:
+                    for ch in line:
+                        add(ch)
+                for line in x.data:
+                    for ch in line:
+                        if ch.kind == PARTITIONED:
+                            q.append(ch)
+    nodes = np.zeros(len(recs), dtype=NODE)
+    for i, x in enumerate(recs):
+        (r0, r1), (c0, c1) = x.row_range, x.col_range
+        lo, hi = layout.interval[id(x)]
+        rec = nodes[i]
+        rec["r0"], rec["r1"], rec["c0"], rec["c1"] = r0, r1, c0, c1
+        rec["lo"], rec["hi"] = lo, hi
+        rec["slot"] = -1
+        rec["child0"] = -1
+        if x.kind == PARTITIONED:
+            rec["kind"] = 2
+            rec["nr"], rec["nc"] = len(x.data), len(x.data[0])
+            rec["child0"] = index[id(x.data[0][0])]
+        elif x.kind == DENSE:
+            rec["kind"] = 0
+            rec["off_a"] = layout.dense_off[id(x)]
+        else:
+            rec["kind"] = 1
+            a_off, b_off, slot = layout.rk[id(x)]
+            rec["off_a"], rec["off_b"], rec["slot"] = a_off, b_off, slot
+    return nodes, index
+
+
+def plan(layout, commands):
+    """commands: list of (kind, nodes..., extras) in the planner's terms:
+    ("factor", h) | ("solve_lower", l, b) | ("solve_upper", b, u) |
+    ("update", c, a, b) | ("fwd", h, name) | ("bwd", h, name)."""
+    nodes, index = flatten_nodes(layout)
+    cmds = np.zeros(len(commands), dtype=CMD)
+    for i, c in enumerate(commands):
+        kind = c[0]
+        if kind == "factor":
+            cmds[i] = (CMD_FACTOR, index[id(c[1])], 0, 0, 0, 0, 0, 0)
+        elif kind == "solve_lower":
+            cmds[i] = (CMD_SOLVE_LOWER, index[id(c[1])], index[id(c[2])], 0, 0, 0, 0, 0)
+        elif kind == "solve_upper":
+            cmds[i] = (CMD_SOLVE_UPPER, index[id(c[1])], index[id(c[2])], 0, 0, 0, 0, 0)
+        elif kind == "update":
+            cmds[i] = (CMD_UPDATE, index[id(c[1])], index[id(c[2])], index[id(c[3])], 0, 0, 0, 0)
+        elif kind in ("fwd", "bwd"):
+            off, rows, cols, res = layout.extra[c[2]]
+            cmds[i] = (CMD_FWD_VEC if kind == "fwd" else CMD_BWD_VEC, index[id(c[1])], 0, 0, off, cols, 0, res)
+        else:
+            raise ValueError(kind)
+    L = lib()
+    h = ctypes.c_void_p()
+    rc = L.hlu_plan_build(ctypes.byref(h), nodes.ctypes.data, len(nodes), cmds.ctypes.data, len(cmds),
+                          layout.cap, layout.ident_off, layout.nslots, layout.nrk, layout.payload_doubles)
+    try:
+        if rc != 0:
+            from .hmatrix import StructureError
+
+            raise StructureError(L.hlu_plan_error(h).decode())
+        sz = np.zeros(14, dtype=np.int64)
+        L.hlu_plan_sizes(h, sz.ctypes.data)
+        ng, nt, nm, nterm, nr, npart, nl, nops, nlev, arena, nlog, nrank, nlu, ntemp = (int(x) for x in sz)
+
+        def arr(n, dt):
+            return np.zeros(max(n, 1), dtype=dt)
+
+        getrf, trsm, gemm = arr(ng, ir.GETRF), arr(nt, ir.TRSM), arr(nm, ir.GEMM)
+        terms, rkt, parts = arr(nterm, ir.TERM), arr(nr, ir.RKT), arr(npart, ir.RKPART)
+        launches = arr(nl, ir.LAUNCH)
+        ff = np.zeros(nops, dtype=np.int32)
+        fc = np.zeros(nops, dtype=np.float64)
+        fl = np.zeros(nops, dtype=np.int64)
+        lu_ops = np.zeros(max(nlu, 1), dtype=np.int64)
+        lu_nodes = np.zeros(max(nlu, 1), dtype=np.int64)
+        lv = np.zeros(nops, dtype=np.int64)
+        L.hlu_plan_copy(h, getrf.ctypes.data, trsm.ctypes.data, gemm.ctypes.data, terms.ctypes.data,
+                        rkt.ctypes.data, parts.ctypes.data, launches.ctypes.data, ff.ctypes.data,
+                        fc.ctypes.data, fl.ctypes.data, lu_ops.ctypes.data, lu_nodes.ctypes.data, lv.ctypes.data)
+    finally:
+        L.hlu_plan_free(h)
+    labels = []
+    for k in lu_nodes[:nlu]:
+        r = nodes[int(k)]
+        labels.append(f"lu[{r['r0']}:{r['r1']})x[{r['c0']}:{r['c1']})")
+    return Packed(
+        getrf=getrf, trsm=trsm, gemm=gemm, terms=terms, rkt=rkt, parts=parts,
+        launches=launches, nlevels=nlev, arena_doubles=arena,
+        flop_formula=ff.astype(np.int64), flop_coef=fc, flop_log=fl, nlog=max(nlog, 1),
+        nranks=max(nrank, 1), lu_op_ids=lu_ops[:nlu], lu_labels=labels, op_levels=lv,
+    ), nops

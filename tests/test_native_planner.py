@@ -1,0 +1,59 @@
+"""The native planner (libhlu_plan.so) must reproduce the Python planner
+(the readable specification, validated against the oracle) byte for byte."""
+
+import numpy as np
+import pytest
+
+import cases
+from paper_1906_00874_b200 import native_plan
+from paper_1906_00874_b200.planner import Layout, Planner
+from paper_1906_00874_b200.schedule import pack
+
+
+def _compare(p_py, p_nat):
+    for f in ("getrf", "trsm", "gemm", "terms", "rkt", "parts", "launches"):
+        a, b = getattr(p_py, f), getattr(p_nat, f)
+        assert a.shape == b.shape, f
+        assert a.tobytes() == b.tobytes(), f
+    for f in ("nlevels", "arena_doubles", "nlog", "nranks"):
+        assert getattr(p_py, f) == getattr(p_nat, f), f
+    assert np.array_equal(p_py.flop_formula, p_nat.flop_formula)
+    assert np.array_equal(p_py.flop_coef, p_nat.flop_coef)
+    assert np.array_equal(p_py.flop_log, p_nat.flop_log)
+    assert np.array_equal(p_py.lu_op_ids, p_nat.lu_op_ids)
+    assert p_py.lu_labels == p_nat.lu_labels
+    assert np.array_equal(p_py.op_levels, p_nat.op_levels)
+
+
+@pytest.mark.parametrize("name", ["mixed_192", "mixed_256_kmax", "dense2x2_256_r3", "bem1d_1024",
+                                  "sphere_1024"])
+def test_factor_plans_identical(name):
+    h, _ = cases.CASES[name][0]()
+    L = Layout(h, cap=32)
+    pl = Planner(L)
+    pl.factor(h)
+    p_py = pack(pl, L.payload_doubles)
+    p_nat, nops = native_plan.plan(L, [("factor", h)])
+    assert nops == len(pl.ops)
+    _compare(p_py, p_nat)
+
+
+def test_solve_and_update_plans_identical():
+    h, _ = cases.mixed(128, 16, 0.5, 10)
+    a, _ = cases.mixed(128, 16, 0.5, 11)
+    b, _ = cases.mixed(128, 16, 0.5, 12)
+    for cmd, roots in ((("update", h, a, b), [h, a, b]), (("solve_lower", a, b), [a, b]),
+                       (("solve_upper", b, a), [b, a])):
+        L = Layout(roots, cap=32)
+        pl = Planner(L)
+        getattr(pl, cmd[0])(*cmd[1:])
+        _compare(pack(pl, L.payload_doubles), native_plan.plan(L, [cmd])[0])
+
+
+def test_vector_solve_plans_identical():
+    h, _ = cases.bem(3, 1024, 2.0, 32, 0.0, 8)
+    L = Layout([h], cap=32, extra=[("x", h.rows, 1)])
+    pl = Planner(L)
+    pl.forward_vector(h, "x")
+    pl.backward_vector(h, "x")
+    _compare(pack(pl, L.payload_doubles), native_plan.plan(L, [("fwd", h, "x"), ("bwd", h, "x")])[0])
