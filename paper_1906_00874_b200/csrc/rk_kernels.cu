@@ -61,101 +61,120 @@ __device__ __forceinline__ double stacked(const PartInfo *P, int np, bool left, 
   return (r >= 0 && r < q.b.rows) ? q.b.get(r, jj) : 0.0;
 }
 
-// Householder QR of S (rows x K, ld LDS) in place; tau[K].  dlarfg conventions.
+// A group of warps working on one factor (X or Y) with its own named barrier.
+struct Grp {
+  int id;   // named barrier id (1, 2) or 0 for the whole CTA
+  int nw;   // warps in the group
+  int w;    // warp index inside the group
+  int l;    // lane
+  int t;    // thread index inside the group
+  __device__ __forceinline__ int nt() const { return nw * 32; }
+  __device__ __forceinline__ void sync() const {
+    if (id == 0) __syncthreads();
+    else asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nw * 32) : "memory");
+  }
+};
+
+// Reflector for column j of S (rows x ., ld LDS), dlarfg conventions, one warp.
+template <int LDS>
+__device__ __forceinline__ void make_reflector(double *S, int rows, int j, double *tau, int l) {
+  double ss = 0.0;
+  for (int i = j + 1 + l; i < rows; i += 32) ss = fma(S[i + j * LDS], S[i + j * LDS], ss);
+  ss = warp_sum(ss);
+  const double alpha = S[j + j * LDS];
+  double tj = 0.0, beta = alpha;
+  if (ss != 0.0) {
+    beta = -copysign(sqrt(fma(alpha, alpha, ss)), alpha);
+    tj = (beta - alpha) / beta;
+    const double sc = 1.0 / (alpha - beta);
+    for (int i = j + 1 + l; i < rows; i += 32) S[i + j * LDS] *= sc;
+  }
+  __syncwarp();
+  if (l == 0) {
+    tau[j] = tj;
+    S[j + j * LDS] = beta;
+  }
+}
+
+// Householder QR of S (rows x K, ld LDS) in place, tau[K]; columns owned
+// round-robin by the group's warps; the owner of column j+1 builds reflector
+// j+1 right after applying reflector j to it (look-ahead), so each step costs
+// one group barrier.
 template <int KM>
-__device__ void house_qr(double *S, int rows, int K, double *tau) {
+__device__ void house_qr(double *S, int rows, int K, double *tau, const Grp &g) {
   constexpr int LDS = RkCfg<KM>::LDS;
-  const int tid = threadIdx.x, w = tid >> 5, l = tid & 31;
-  __shared__ double s_tau, s_beta;
   const int t = min(rows, K);
+  if (t <= 0) return;
+  if (g.w == 0) make_reflector<LDS>(S, rows, 0, tau, g.l);
+  g.sync();
   for (int j = 0; j < t; ++j) {
-    if (w == 0) {
-      double ss = 0.0;
-      for (int i = j + 1 + l; i < rows; i += 32) {
-        const double v = S[i + j * LDS];
-        ss += v * v;
-      }
-      ss = warp_sum(ss);
-      const double alpha = S[j + j * LDS];
-      double tj = 0.0, beta = alpha;
-      if (ss != 0.0) {
-        beta = -copysign(sqrt(alpha * alpha + ss), alpha);
-        tj = (beta - alpha) / beta;
-        const double sc = 1.0 / (alpha - beta);
-        for (int i = j + 1 + l; i < rows; i += 32) S[i + j * LDS] *= sc;
-      }
-      if (l == 0) {
-        s_tau = tj;
-        s_beta = beta;
-        tau[j] = tj;
-      }
-    }
-    __syncthreads();
-    const double tj = s_tau;
-    if (tj != 0.0) {
-      for (int col = j + 1 + w; col < K; col += HLU_NWARP) {
+    const double tj = tau[j];
+    int col = j + 1 + ((g.w - (j + 1)) % g.nw + g.nw) % g.nw;
+    for (; col < K; col += g.nw) {
+      if (tj != 0.0) {
         double acc = 0.0;
-        for (int i = j + 1 + l; i < rows; i += 32) acc += S[i + j * LDS] * S[i + col * LDS];
+        for (int i = j + 1 + g.l; i < rows; i += 32) acc = fma(S[i + j * LDS], S[i + col * LDS], acc);
         acc = warp_sum(acc) + S[j + col * LDS];
         const double f = tj * acc;
-        for (int i = j + 1 + l; i < rows; i += 32) S[i + col * LDS] -= f * S[i + j * LDS];
-        if (l == 0) S[j + col * LDS] -= f;
+        for (int i = j + 1 + g.l; i < rows; i += 32) S[i + col * LDS] -= f * S[i + j * LDS];
+        __syncwarp();
+        if (g.l == 0) S[j + col * LDS] -= f;
+        __syncwarp();
       }
+      if (col == j + 1 && col < t) make_reflector<LDS>(S, rows, col, tau, g.l);
     }
-    if (tid == 0) S[j + j * LDS] = s_beta;
-    __syncthreads();
+    g.sync();
   }
 }
 
 // TSQR of one stacked factor.  R (rr x K, ld KM, zero below the diagonal) -> R.
 template <int KM>
 __device__ int tsqr(const PartInfo *P, int np, bool left, int m, int K, double *S, double *R, double *tau,
-                    double *ws) {
+                    double *ws, const Grp &g) {
   constexpr int LDS = RkCfg<KM>::LDS, CH = RkCfg<KM>::CH;
-  const int tid = threadIdx.x;
   int r = 0;  // carried R rows at the top of S
   int64_t off = 0;
   for (int r0 = 0; r0 < m; r0 += CH) {
     const int cnt = min(CH, m - r0);
     const int rows = r + cnt;
-    for (int e = tid; e < cnt * K; e += HLU_NT) {
+    for (int e = g.t; e < cnt * K; e += g.nt()) {
       const int i = e % cnt, j = e / cnt;
       S[r + i + j * LDS] = stacked(P, np, left, r0 + i, j);
     }
-    __syncthreads();
-    house_qr<KM>(S, rows, K, tau);
+    g.sync();
+    house_qr<KM>(S, rows, K, tau, g);
     // save the chunk's compact QR (ld = rows) and tau
     double *dst = ws + off;
-    for (int e = tid; e < rows * K; e += HLU_NT) {
+    for (int e = g.t; e < rows * K; e += g.nt()) {
       const int i = e % rows, j = e / rows;
       dst[i + (int64_t)j * rows] = S[i + j * LDS];
     }
-    for (int j = tid; j < K; j += HLU_NT) dst[(int64_t)rows * K + j] = (j < min(rows, K)) ? tau[j] : 0.0;
+    for (int j = g.t; j < K; j += g.nt()) dst[(int64_t)rows * K + j] = (j < min(rows, K)) ? tau[j] : 0.0;
     off += (int64_t)rows * K + K;
     r = min(rows, K);
-    __syncthreads();
-    // keep R on top, clear the reflector entries below its diagonal
-    for (int e = tid; e < r * K; e += HLU_NT) {
-      const int i = e % r, j = e / r;
-      if (i > j) S[i + j * LDS] = 0.0;
+    g.sync();
+    if (r0 + CH < m) {  // keep R on top for the next chunk
+      for (int e = g.t; e < r * K; e += g.nt()) {
+        const int i = e % r, j = e / r;
+        if (i > j) S[i + j * LDS] = 0.0;
+      }
+      g.sync();
     }
-    __syncthreads();
   }
-  for (int e = tid; e < KM * K; e += HLU_NT) {
+  for (int e = g.t; e < KM * K; e += g.nt()) {
     const int i = e % KM, j = e / KM;
     R[i + j * KM] = (i < r && i <= j) ? S[i + j * LDS] : 0.0;
   }
-  __syncthreads();
+  g.sync();
   return r;
 }
 
 // out (m x kk, ld m) = Q [W (rr x kk, ld KM); 0], Q from the stored chunks.
 template <int KM>
-__device__ void apply_q(int m, int K, int kk, const double *W, double *T, const double *ws, double *out) {
+__device__ void apply_q(int m, int K, int kk, const double *W, double *T, const double *ws, double *out,
+                        const Grp &g) {
   constexpr int LDS = RkCfg<KM>::LDS, CH = RkCfg<KM>::CH;
-  const int tid = threadIdx.x, w = tid >> 5, l = tid & 31;
   const int nch = (m + CH - 1) / CH;
-  // chunk geometry: rows_s = r_{s-1} + cnt_s, r_s = min(rows_s, K); offsets are prefix sums
   int64_t off_last = 0;
   int rprev_last = 0;
   {
@@ -171,8 +190,7 @@ __device__ void apply_q(int m, int K, int kk, const double *W, double *T, const 
       off += (int64_t)rows * K + K;
       r = min(rows, K);
     }
-    // top of T = W (r_last rows)
-    for (int e = tid; e < r * kk; e += HLU_NT) {
+    for (int e = g.t; e < r * kk; e += g.nt()) {
       const int i = e % r, j = e / r;
       T[i + j * LDS] = W[i + j * KM];
     }
@@ -183,36 +201,34 @@ __device__ void apply_q(int m, int K, int kk, const double *W, double *T, const 
     const int cnt = min(CH, m - s * CH);
     const int rows = rprev + cnt;
     const int rs = min(rows, K);
-    __syncthreads();
-    for (int e = tid; e < (rows - rs) * kk; e += HLU_NT) {
+    g.sync();
+    for (int e = g.t; e < (rows - rs) * kk; e += g.nt()) {
       const int i = rs + e % (rows - rs), j = e / (rows - rs);
       T[i + j * LDS] = 0.0;
     }
-    __syncthreads();
+    g.sync();
     const double *V = ws + off;
     const double *tau = V + (int64_t)rows * K;
-    // columns are independent: one warp per column runs all reflectors
-    for (int col = w; col < kk; col += HLU_NWARP) {
+    for (int col = g.w; col < kk; col += g.nw) {
       double *t = T + col * LDS;
       for (int j = rs - 1; j >= 0; --j) {
         const double tj = tau[j];
         if (tj == 0.0) continue;
         double acc = 0.0;
-        for (int i = j + 1 + l; i < rows; i += 32) acc += V[i + (int64_t)j * rows] * t[i];
+        for (int i = j + 1 + g.l; i < rows; i += 32) acc = fma(V[i + (int64_t)j * rows], t[i], acc);
         acc = warp_sum(acc) + t[j];
         const double f = tj * acc;
-        for (int i = j + 1 + l; i < rows; i += 32) t[i] -= f * V[i + (int64_t)j * rows];
+        for (int i = j + 1 + g.l; i < rows; i += 32) t[i] -= f * V[i + (int64_t)j * rows];
         __syncwarp();
-        if (l == 0) t[j] -= f;
+        if (g.l == 0) t[j] -= f;
         __syncwarp();
       }
     }
-    __syncthreads();
-    for (int e = tid; e < cnt * kk; e += HLU_NT) {
+    g.sync();
+    for (int e = g.t; e < cnt * kk; e += g.nt()) {
       const int i = e % cnt, j = e / cnt;
       out[(int64_t)s * CH + i + (int64_t)j * m] = T[rprev + i + j * LDS];
     }
-    // step back: previous chunk's geometry
     if (s > 0) {
       int r = 0;
       int64_t o2 = 0, o_prev = 0;
@@ -231,69 +247,190 @@ __device__ void apply_q(int m, int K, int kk, const double *W, double *T, const 
       rprev = rp_prev;
     }
   }
-  __syncthreads();
+  g.sync();
 }
 
 __device__ unsigned long long g_sweeps = 0;  // total Jacobi sweeps (diagnostics)
 
-__device__ __forceinline__ int rr_player(int pos, int r, int qq) {
-  return pos == 0 ? 0 : 1 + (pos - 1 + r) % (qq - 1);
+// Round-robin pairing table: round r, slot i -> (a, b); computed once per op.
+__device__ __forceinline__ void build_pairs(unsigned char *pa, unsigned char *pb, int qq) {
+  for (int e = threadIdx.x; e < (qq - 1) * (qq / 2); e += HLU_NT) {
+    const int r = e / (qq / 2), i = e % (qq / 2);
+    const int u = i, v = qq - 1 - i;
+    int a = u == 0 ? 0 : 1 + (u - 1 + r) % (qq - 1);
+    int b = v == 0 ? 0 : 1 + (v - 1 + r) % (qq - 1);
+    if (a > b) { const int x = a; a = b; b = x; }
+    pa[e] = (unsigned char)a;
+    pb[e] = (unsigned char)b;
+  }
 }
 
-// One-sided Jacobi on G (p x q, ld KM) accumulating V (q x q, ld KM).
+// QR with column pivoting of G (p x q, p >= q, ld KM), in place, without
+// moving data: cm[j] is the physical column holding logical column j (the
+// pivot order), reflector j lives below row j of column cm[j], tau[j].
 template <int KM>
-__device__ void jacobi(double *G, double *V, int p, int q) {
+__device__ void qrcp(double *G, int p, int q, double *tau, int *cm, double *nrm) {
   const int tid = threadIdx.x, w = tid >> 5, l = tid & 31;
-  __shared__ int s_rot;
-  for (int e = tid; e < KM * KM; e += HLU_NT) V[e] = ((e % KM) == (e / KM)) ? 1.0 : 0.0;
-  const int qq = q + (q & 1);
-  const double tol = 1e-15;
-  if (q < 2) {
-    __syncthreads();
-    return;
+  __shared__ double s_beta;
+  for (int c = tid; c < q; c += HLU_NT) cm[c] = c;
+  for (int c = w; c < q; c += HLU_NWARP) {
+    double ss = 0.0;
+    for (int i = l; i < p; i += 32) ss += G[i + c * KM] * G[i + c * KM];
+    ss = warp_sum(ss);
+    if (l == 0) nrm[c] = ss;
   }
-  for (int sweep = 0; sweep < 60; ++sweep) {
-    if (tid == 0) s_rot = 0;
+  __syncthreads();
+  for (int j = 0; j < q; ++j) {
+    if (w == 0) {
+      // pivot: largest remaining norm (first on ties), then the reflector
+      double best = -1.0;
+      int bi = j;
+      for (int c = j + l; c < q; c += 32) {
+        const double v = nrm[cm[c]];
+        if (v > best) { best = v; bi = c; }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+      }
+      const int cj = cm[bi];
+      __syncwarp();
+      if (l == 0 && bi != j) { cm[bi] = cm[j]; cm[j] = cj; }
+      double ss = 0.0;
+      for (int i = j + 1 + l; i < p; i += 32) ss += G[i + cj * KM] * G[i + cj * KM];
+      ss = warp_sum(ss);
+      const double alpha = G[j + cj * KM];
+      double tj = 0.0, beta = alpha;
+      if (ss != 0.0) {
+        beta = -copysign(sqrt(alpha * alpha + ss), alpha);
+        tj = (beta - alpha) / beta;
+        const double sc = 1.0 / (alpha - beta);
+        for (int i = j + 1 + l; i < p; i += 32) G[i + cj * KM] *= sc;
+      }
+      if (l == 0) { tau[j] = tj; s_beta = beta; }
+    }
     __syncthreads();
+    const double tj = tau[j];
+    const int cj = cm[j];
+    for (int c = j + 1 + w; c < q; c += HLU_NWARP) {
+      const int pc = cm[c];
+      if (tj != 0.0) {
+        double acc = 0.0;
+        for (int i = j + 1 + l; i < p; i += 32) acc += G[i + cj * KM] * G[i + pc * KM];
+        acc = warp_sum(acc) + G[j + pc * KM];
+        const double f = tj * acc;
+        for (int i = j + 1 + l; i < p; i += 32) G[i + pc * KM] -= f * G[i + cj * KM];
+        __syncwarp();
+        if (l == 0) G[j + pc * KM] -= f;
+      }
+      double ss = 0.0;
+      for (int i = j + 1 + l; i < p; i += 32) ss += G[i + pc * KM] * G[i + pc * KM];
+      ss = warp_sum(ss);
+      if (l == 0) nrm[pc] = ss;
+    }
+    if (tid == 0) G[j + cj * KM] = s_beta;
+    __syncthreads();
+  }
+}
+
+// z (p rows, stride 1) <- Q [z(0:q); 0] with the qrcp reflectors; one warp.
+template <int KM>
+__device__ void qrcp_apply(const double *G, int p, int q, const double *tau, const int *cm, double *z) {
+  const int l = threadIdx.x & 31;
+  for (int j = q - 1; j >= 0; --j) {
+    const double tj = tau[j];
+    if (tj == 0.0) continue;
+    const double *v = G + cm[j] * KM;
+    double acc = 0.0;
+    for (int i = j + 1 + l; i < p; i += 32) acc += v[i] * z[i];
+    acc = warp_sum(acc) + z[j];
+    const double f = tj * acc;
+    for (int i = j + 1 + l; i < p; i += 32) z[i] -= f * v[i];
+    __syncwarp();
+    if (l == 0) z[j] -= f;
+    __syncwarp();
+  }
+}
+
+// One-sided (Hestenes) Jacobi on X (n x n, ld KM) accumulating V; round-robin
+// pairs from the table, LP lanes per pair (16 when a round has > 8 pairs), one
+// barrier per round.  Stops after a sweep with no rotation, or after a sweep
+// whose largest relative off-diagonal was < 1e-8 (quadratic convergence puts
+// the next sweep below the 1e-15 rotation threshold).
+template <int LP>
+__device__ __forceinline__ double part_sum(double v) {
+  // lanes of one pair only: half-warps of a warp may take different branches
+  const unsigned mask = LP == 32 ? 0xffffffffu : (0xffffu << (threadIdx.x & 16));
+#pragma unroll
+  for (int o = LP / 2; o > 0; o >>= 1) v += __shfl_xor_sync(mask, v, o);
+  return v;
+}
+
+template <int KM, int LP>
+__device__ void jacobi_lp(double *X, double *V, int n, const unsigned char *pa, const unsigned char *pb,
+                          double *smax) {
+  const int tid = threadIdx.x;
+  const int grp = tid / LP, l = tid % LP, ngrp = HLU_NT / LP;
+  const int qq = n + (n & 1);
+  const int np = qq / 2;
+  const double tol = 1e-15;
+  for (int sweep = 0; sweep < 40; ++sweep) {
+    double mx = 0.0;
     for (int r = 0; r < qq - 1; ++r) {
-      for (int pi = w; pi < qq / 2; pi += HLU_NWARP) {
-        int a = rr_player(pi, r, qq), b = rr_player(qq - 1 - pi, r, qq);
-        if (a >= q || b >= q) continue;
-        if (a > b) { const int x = a; a = b; b = x; }
+      for (int pi = grp; pi < np; pi += ngrp) {
+        const int a = pa[r * np + pi], b = pb[r * np + pi];
+        if (b >= n) continue;
         double al = 0.0, be = 0.0, ga = 0.0;
-        for (int i = l; i < p; i += 32) {
-          const double x = G[i + a * KM], y = G[i + b * KM];
-          al += x * x;
-          be += y * y;
-          ga += x * y;
+        for (int i = l; i < n; i += LP) {
+          const double x = X[i + a * KM], y = X[i + b * KM];
+          al = fma(x, x, al);
+          be = fma(y, y, be);
+          ga = fma(x, y, ga);
         }
-        al = warp_sum(al);
-        be = warp_sum(be);
-        ga = warp_sum(ga);
-        if (ga == 0.0 || !(fabs(ga) > tol * sqrt(al * be))) continue;
+        al = part_sum<LP>(al);
+        be = part_sum<LP>(be);
+        ga = part_sum<LP>(ga);
+        const double den = sqrt(al * be);
+        if (ga == 0.0 || !(fabs(ga) > tol * den)) continue;
+        mx = fmax(mx, fabs(ga) / den);
         const double zeta = (be - al) / (2.0 * ga);
-        const double t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-        const double cs = 1.0 / sqrt(1.0 + t * t), sn = cs * t;
-        for (int i = l; i < p; i += 32) {
-          const double x = G[i + a * KM], y = G[i + b * KM];
-          G[i + a * KM] = cs * x - sn * y;
-          G[i + b * KM] = sn * x + cs * y;
+        const double t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
+        const double cs = rsqrt(fma(t, t, 1.0)), sn = cs * t;
+        for (int i = l; i < n; i += LP) {
+          const double x = X[i + a * KM], y = X[i + b * KM];
+          X[i + a * KM] = cs * x - sn * y;
+          X[i + b * KM] = sn * x + cs * y;
+          const double u = V[i + a * KM], v = V[i + b * KM];
+          V[i + a * KM] = cs * u - sn * v;
+          V[i + b * KM] = sn * u + cs * v;
         }
-        for (int i = l; i < q; i += 32) {
-          const double x = V[i + a * KM], y = V[i + b * KM];
-          V[i + a * KM] = cs * x - sn * y;
-          V[i + b * KM] = sn * x + cs * y;
-        }
-        if (l == 0) s_rot = 1;
       }
       __syncthreads();
     }
-    if (s_rot == 0) {
+    mx = warp_max(mx);
+    if ((tid & 31) == 0) smax[tid >> 5] = mx;
+    __syncthreads();
+    double m2 = 0.0;
+#pragma unroll
+    for (int i = 0; i < HLU_NWARP; ++i) m2 = fmax(m2, smax[i]);
+    __syncthreads();
+    if (m2 < 1e-8) {
       if (tid == 0) atomicAdd(&g_sweeps, sweep + 1);
       break;
     }
-    __syncthreads();
   }
+}
+
+template <int KM>
+__device__ void jacobi(double *X, double *V, int n, const unsigned char *pa, const unsigned char *pb) {
+  __shared__ double smax[HLU_NWARP];
+  for (int e = threadIdx.x; e < KM * KM; e += HLU_NT) V[e] = ((e % KM) == (e / KM)) ? 1.0 : 0.0;
+  __syncthreads();
+  if (n < 2) return;
+  if ((n + 1) / 2 > HLU_NWARP) jacobi_lp<KM, 16>(X, V, n, pa, pb, smax);
+  else jacobi_lp<KM, 32>(X, V, n, pa, pb, smax);
   __syncthreads();
 }
 
@@ -302,13 +439,18 @@ __global__ void __launch_bounds__(HLU_NT)
     k_rkt(hlu_ctx c, hlu_rkt_desc *__restrict__ d, const hlu_rkpart *__restrict__ parts) {
   using Cfg = RkCfg<KM>;
   extern __shared__ double sm[];
-  double *S = sm;                 // BUFD
-  double *RA = S + Cfg::BUFD;     // KM*KM
+  double *S = sm;                 // BUFD   group-0 chunk buffer (X), later G | V
+  double *S1 = S + Cfg::BUFD;     // BUFD   group-1 chunk buffer (Y), later XT
+  double *RA = S1 + Cfg::BUFD;    // KM*KM
   double *RB = RA + KM * KM;      // KM*KM
   double *tau = RB + KM * KM;     // KM
-  double *sig = tau + KM;         // KM
+  double *tau1 = tau + KM;        // KM
+  double *sig = tau1 + KM;        // KM
+  double *XT = S1;                // KM*KM  (R^T, then W = R^T V)
   __shared__ PartInfo P[RK_MAXP];
   __shared__ int perm[KM];
+  __shared__ int cmap[KM];
+  __shared__ unsigned char pairs_a[(KM - 1) * (KM / 2)], pairs_b[(KM - 1) * (KM / 2)];
   __shared__ int s_kk;
   const hlu_rkt_desc o = d[blockIdx.x];
   const int tid = threadIdx.x;
@@ -391,9 +533,19 @@ __global__ void __launch_bounds__(HLU_NT)
   }
   double *wsA = c.pool + o.ws;
   double *wsB = wsA + rk_ws_one(m, K, Cfg::CH);
-  // A/B. TSQR of both stacked factors
-  const int ra = tsqr<KM>(P, np, true, m, K, S, RA, tau, wsA);
-  const int rb = tsqr<KM>(P, np, false, n, K, S, RB, tau, wsB);
+  // A/B. TSQR of both stacked factors, concurrently on two warp groups
+  const int wq = tid >> 5;
+  const Grp grp{1 + (wq >= HLU_NWARP / 2), HLU_NWARP / 2, wq % (HLU_NWARP / 2), tid & 31, tid % (HLU_NT / 2)};
+  __shared__ int s_ra, s_rb;
+  if (wq < HLU_NWARP / 2) {
+    const int r_ = tsqr<KM>(P, np, true, m, K, S, RA, tau, wsA, grp);
+    if (grp.t == 0) s_ra = r_;
+  } else {
+    const int r_ = tsqr<KM>(P, np, false, n, K, S1, RB, tau1, wsB, grp);
+    if (grp.t == 0) s_rb = r_;
+  }
+  __syncthreads();
+  const int ra = s_ra, rb = s_rb;
   // C. core M = R_a R_b^T (ra x rb); G = M or M^T so that G has q <= p columns
   const bool tr = rb > ra;
   const int p = tr ? rb : ra, q = tr ? ra : rb;
@@ -408,12 +560,21 @@ __global__ void __launch_bounds__(HLU_NT)
     else G[i + j * KM] = acc;
   }
   __syncthreads();
-  // D. SVD
-  jacobi<KM>(G, V, p, q);
+  // D. SVD of G via QR with column pivoting + one-sided Jacobi on R^T
+  //    (G P = Q R, R^T V = W = U S  =>  G = (Q V) S (P U)^T)
+  qrcp<KM>(G, p, q, tau, cmap, sig);
+  for (int e = tid; e < KM * KM; e += HLU_NT) {
+    const int i = e % KM, j = e / KM;  // XT[i, j] = R[j, i]
+    XT[e] = (i < q && j < q && j <= i) ? G[j + cmap[i] * KM] : 0.0;
+  }
+  const int qq = q + (q & 1);
+  build_pairs(pairs_a, pairs_b, qq);
+  __syncthreads();
+  jacobi<KM>(XT, V, q, pairs_a, pairs_b);
   // E. singular values, order, rank
   for (int j = tid; j < q; j += HLU_NT) {
     double ss = 0.0;
-    for (int i = 0; i < p; ++i) ss += G[i + j * KM] * G[i + j * KM];
+    for (int i = 0; i < q; ++i) ss = fma(XT[i + j * KM], XT[i + j * KM], ss);
     sig[j] = sqrt(ss);
   }
   __syncthreads();
@@ -440,24 +601,26 @@ __global__ void __launch_bounds__(HLU_NT)
   }
   __syncthreads();
   const int kk = s_kk;
-  // F. W_a (ra x kk) -> RA, W_b (rb x kk) -> RB
+  // F. W_a (ra x kk) -> RA, W_b (rb x kk) -> RB.
+  //   G = M  (!tr): W_a = Q (V S)_sel,  W_b = P W_sel / S
+  //   G = M^T (tr): W_a = P W_sel,      W_b = Q V_sel
+  double *WQ = tr ? RB : RA;  // the side that needs Q applied
+  double *WP = tr ? RA : RB;  // the permuted side
   for (int e = tid; e < KM * kk; e += HLU_NT) {
     const int i = e % KM, cidx = e / KM;
     const int j = perm[cidx];
-    double wa = 0.0, wb = 0.0;
-    if (!tr) {
-      if (i < ra) wa = G[i + j * KM];
-      if (i < rb) wb = V[i + j * KM];
-    } else {
-      if (i < ra) wa = V[i + j * KM] * sig[j];
-      if (i < rb) wb = G[i + j * KM] / sig[j];
-    }
-    RA[i + cidx * KM] = wa;
-    RB[i + cidx * KM] = wb;
+    WQ[i + cidx * KM] = (i < q) ? (tr ? V[i + j * KM] : V[i + j * KM] * sig[j]) : 0.0;
+    if (i < q) WP[cmap[i] + cidx * KM] = tr ? XT[i + j * KM] : XT[i + j * KM] / sig[j];
+  }
+  for (int e = tid; e < (KM - q) * kk; e += HLU_NT) {  // rows >= q of the permuted side
+    const int i = q + e % (KM - q), cidx = e / (KM - q);
+    WP[i + cidx * KM] = 0.0;
   }
   __syncthreads();
-  apply_q<KM>(m, K, kk, RA, S, wsA, outA);
-  apply_q<KM>(n, K, kk, RB, S, wsB, outB);
+  for (int col = tid >> 5; col < kk; col += HLU_NWARP) qrcp_apply<KM>(G, p, q, tau, cmap, WQ + col * KM);
+  __syncthreads();
+  if (wq < HLU_NWARP / 2) apply_q<KM>(m, K, kk, RA, S, wsA, outA, grp);
+  else apply_q<KM>(n, K, kk, RB, S1, wsB, outB, grp);
   if (tid == 0) {
     c.ranks[o.out_slot] = kk;
     if (o.log >= 0) c.log[o.log + 2] = kk;
@@ -466,7 +629,7 @@ __global__ void __launch_bounds__(HLU_NT)
 
 template <int KM>
 static size_t rkt_smem() {
-  return (size_t)(RkCfg<KM>::BUFD + 2 * KM * KM + 2 * KM) * sizeof(double);
+  return (size_t)(2 * RkCfg<KM>::BUFD + 2 * KM * KM + 3 * KM) * sizeof(double);
 }
 
 }  // namespace hlu
