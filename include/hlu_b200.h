@@ -154,6 +154,7 @@ int hlu_schedule_destroy(hlu_schedule *s);
 const char *hlu_version(void);
 int hlu_device_check(void); /* 0 when a sm_100 device is present */
 int64_t hlu_debug_sweeps(int reset); /* total Jacobi sweeps run so far (diagnostics) */
+int hlu_debug_phases(double *sum_out, double *max_out, int reset); /* RKT phase cycles (diagnostics) */
 
 #ifdef __cplusplus
 }

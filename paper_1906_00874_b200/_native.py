@@ -25,6 +25,7 @@ SYMBOLS = (
     "hlu_version",
     "hlu_device_check",
     "hlu_debug_sweeps",
+    "hlu_debug_phases",
 )
 
 

@@ -52,6 +52,31 @@ __device__ __forceinline__ double warp_max(double v) {
   return v;
 }
 
+// Full-precision fp64 reciprocal / reciprocal square root: the MUFU
+// approximation refined by two Newton steps (quadratic convergence from
+// >= 2^-20 relative to below one ulp), without the IEEE slow-path branches of
+// '/' and sqrt() that dominate latency-bound chains.
+__device__ __forceinline__ double fast_rcp(double x) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  double e = fma(-x, y, 1.0);
+  y = fma(y, e, y);
+  e = fma(-x, y, 1.0);
+  return fma(y, e, y);
+}
+
+__device__ __forceinline__ double fast_rsqrt(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  const double h = 0.5 * x;
+  double t = fma(-h * y, y, 0.5);
+  y = fma(y, t, y);
+  t = fma(-h * y, y, 0.5);
+  y = fma(y, t, y);
+  t = fma(-h * y, y, 0.5);
+  return fma(y, t, y);
+}
+
 // block-wide max over HLU_NT threads; red must hold HLU_NWARP doubles
 __device__ __forceinline__ double block_max(double v, double *red) {
   v = warp_max(v);

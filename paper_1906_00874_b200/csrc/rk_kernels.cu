@@ -84,9 +84,14 @@ __device__ __forceinline__ void make_reflector(double *S, int rows, int j, doubl
   const double alpha = S[j + j * LDS];
   double tj = 0.0, beta = alpha;
   if (ss != 0.0) {
-    beta = -copysign(sqrt(fma(alpha, alpha, ss)), alpha);
-    tj = (beta - alpha) / beta;
-    const double sc = 1.0 / (alpha - beta);
+    // beta = -sign(alpha) ||x||, tau = (beta - alpha) / beta = 1 + |alpha| / ||x||,
+    // v = x / (alpha - beta)
+    const double n2 = fma(alpha, alpha, ss);
+    const double rn = fast_rsqrt(n2);
+    const double nrm = n2 * rn;
+    beta = -copysign(nrm, alpha);
+    tj = fma(fabs(alpha), rn, 1.0);
+    const double sc = fast_rcp(alpha - beta);
     for (int i = j + 1 + l; i < rows; i += 32) S[i + j * LDS] *= sc;
   }
   __syncwarp();
@@ -170,9 +175,12 @@ __device__ int tsqr(const PartInfo *P, int np, bool left, int m, int K, double *
 }
 
 // out (m x kk, ld m) = Q [W (rr x kk, ld KM); 0], Q from the stored chunks.
+// T (BUFD) holds the moving block, VS (BUFD) each chunk's reflectors staged
+// from the workspace with one coalesced copy, so the sequential reflector
+// chain runs out of shared memory; one warp per output column.
 template <int KM>
-__device__ void apply_q(int m, int K, int kk, const double *W, double *T, const double *ws, double *out,
-                        const Grp &g) {
+__device__ void apply_q(int m, int K, int kk, const double *W, double *T, double *VS, const double *ws,
+                        double *out, const Grp &g) {
   constexpr int LDS = RkCfg<KM>::LDS, CH = RkCfg<KM>::CH;
   const int nch = (m + CH - 1) / CH;
   int64_t off_last = 0;
@@ -206,19 +214,21 @@ __device__ void apply_q(int m, int K, int kk, const double *W, double *T, const 
       const int i = rs + e % (rows - rs), j = e / (rows - rs);
       T[i + j * LDS] = 0.0;
     }
-    g.sync();
     const double *V = ws + off;
-    const double *tau = V + (int64_t)rows * K;
+    for (int e = g.t; e < rows * K + K; e += g.nt()) VS[e] = V[e];  // reflectors (ld rows) + tau
+    g.sync();
+    const double *tau = VS + rows * K;
     for (int col = g.w; col < kk; col += g.nw) {
       double *t = T + col * LDS;
       for (int j = rs - 1; j >= 0; --j) {
         const double tj = tau[j];
         if (tj == 0.0) continue;
+        const double *v = VS + j * rows;
         double acc = 0.0;
-        for (int i = j + 1 + g.l; i < rows; i += 32) acc = fma(V[i + (int64_t)j * rows], t[i], acc);
+        for (int i = j + 1 + g.l; i < rows; i += 32) acc = fma(v[i], t[i], acc);
         acc = warp_sum(acc) + t[j];
         const double f = tj * acc;
-        for (int i = j + 1 + g.l; i < rows; i += 32) t[i] -= f * V[i + (int64_t)j * rows];
+        for (int i = j + 1 + g.l; i < rows; i += 32) t[i] -= f * v[i];
         __syncwarp();
         if (g.l == 0) t[j] -= f;
         __syncwarp();
@@ -251,6 +261,15 @@ __device__ void apply_q(int m, int K, int kk, const double *W, double *T, const 
 }
 
 __device__ unsigned long long g_sweeps = 0;  // total Jacobi sweeps (diagnostics)
+__device__ unsigned long long g_phase[10];   // summed cycles per phase (diagnostics)
+__device__ unsigned long long g_phase_max[10];
+#define PHASE(k)                                                   \
+  if (threadIdx.x == 0) {                                          \
+    const unsigned long long now = clock64();                      \
+    atomicAdd(&g_phase[k], now - t_last);                          \
+    atomicMax(&g_phase_max[k], now - t_last);                      \
+    t_last = now;                                                  \
+  }
 
 // Round-robin pairing table: round r, slot i -> (a, b); computed once per op.
 __device__ __forceinline__ void build_pairs(unsigned char *pa, unsigned char *pb, int qq) {
@@ -304,9 +323,11 @@ __device__ void qrcp(double *G, int p, int q, double *tau, int *cm, double *nrm)
       const double alpha = G[j + cj * KM];
       double tj = 0.0, beta = alpha;
       if (ss != 0.0) {
-        beta = -copysign(sqrt(alpha * alpha + ss), alpha);
-        tj = (beta - alpha) / beta;
-        const double sc = 1.0 / (alpha - beta);
+        const double n2 = fma(alpha, alpha, ss);
+        const double rn = fast_rsqrt(n2);
+        beta = -copysign(n2 * rn, alpha);
+        tj = fma(fabs(alpha), rn, 1.0);
+        const double sc = fast_rcp(alpha - beta);
         for (int i = j + 1 + l; i < p; i += 32) G[i + cj * KM] *= sc;
       }
       if (l == 0) { tau[j] = tj; s_beta = beta; }
@@ -375,9 +396,8 @@ __device__ void jacobi_lp(double *X, double *V, int n, const unsigned char *pa, 
   const int grp = tid / LP, l = tid % LP, ngrp = HLU_NT / LP;
   const int qq = n + (n & 1);
   const int np = qq / 2;
-  const double tol = 1e-15;
   for (int sweep = 0; sweep < 40; ++sweep) {
-    double mx = 0.0;
+    int big = 0;
     for (int r = 0; r < qq - 1; ++r) {
       for (int pi = grp; pi < np; pi += ngrp) {
         const int a = pa[r * np + pi], b = pb[r * np + pi];
@@ -392,12 +412,15 @@ __device__ void jacobi_lp(double *X, double *V, int n, const unsigned char *pa, 
         al = part_sum<LP>(al);
         be = part_sum<LP>(be);
         ga = part_sum<LP>(ga);
-        const double den = sqrt(al * be);
-        if (ga == 0.0 || !(fabs(ga) > tol * den)) continue;
-        mx = fmax(mx, fabs(ga) / den);
-        const double zeta = (be - al) / (2.0 * ga);
-        const double t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
-        const double cs = rsqrt(fma(t, t, 1.0)), sn = cs * t;
+        const double g2 = ga * ga, ab = al * be;
+        if (ga == 0.0 || !(g2 > 1e-30 * ab)) continue;  // |ga| <= 1e-15 sqrt(al be)
+        if (g2 > 1e-16 * ab) big = 1;                    // not yet in the quadratic regime
+        // t = tan(theta) = 2 ga / (d + sign(d) sqrt(d^2 + 4 ga^2)), d = be - al
+        const double d = be - al;
+        const double q2 = fma(d, d, 4.0 * g2);
+        const double r = q2 * fast_rsqrt(q2);
+        const double t = 2.0 * ga * fast_rcp(d + copysign(r, d));
+        const double cs = fast_rsqrt(fma(t, t, 1.0)), sn = cs * t;
         for (int i = l; i < n; i += LP) {
           const double x = X[i + a * KM], y = X[i + b * KM];
           X[i + a * KM] = cs * x - sn * y;
@@ -409,14 +432,7 @@ __device__ void jacobi_lp(double *X, double *V, int n, const unsigned char *pa, 
       }
       __syncthreads();
     }
-    mx = warp_max(mx);
-    if ((tid & 31) == 0) smax[tid >> 5] = mx;
-    __syncthreads();
-    double m2 = 0.0;
-#pragma unroll
-    for (int i = 0; i < HLU_NWARP; ++i) m2 = fmax(m2, smax[i]);
-    __syncthreads();
-    if (m2 < 1e-8) {
+    if (__syncthreads_or(big) == 0) {
       if (tid == 0) atomicAdd(&g_sweeps, sweep + 1);
       break;
     }
@@ -452,19 +468,23 @@ __global__ void __launch_bounds__(HLU_NT)
   __shared__ int cmap[KM];
   __shared__ unsigned char pairs_a[(KM - 1) * (KM / 2)], pairs_b[(KM - 1) * (KM / 2)];
   __shared__ int s_kk;
+  unsigned long long t_last = clock64();
   const hlu_rkt_desc o = d[blockIdx.x];
   const int tid = threadIdx.x;
   const int np = o.part_count;
+  if (tid < np && tid < RK_MAXP) {  // one thread per part: the descriptor/rank loads overlap
+    const hlu_rkpart q = parts[o.part_begin + tid];
+    P[tid].a = resolve(c, q.a);
+    P[tid].b = resolve(c, q.b);
+    P[tid].sign = q.sign;
+    P[tid].roff = q.roff;
+    P[tid].coff = q.coff;
+    P[tid].k = P[tid].a.cols;
+  }
+  __syncthreads();
   if (tid == 0) {
     int col = 0;
     for (int p = 0; p < np && p < RK_MAXP; ++p) {
-      const hlu_rkpart q = parts[o.part_begin + p];
-      P[p].a = resolve(c, q.a);
-      P[p].b = resolve(c, q.b);
-      P[p].sign = q.sign;
-      P[p].roff = q.roff;
-      P[p].coff = q.coff;
-      P[p].k = P[p].a.cols;
       P[p].col0 = col;
       col += P[p].k;
     }
@@ -531,6 +551,7 @@ __global__ void __launch_bounds__(HLU_NT)
     if (tid == 0) atomicAdd(&c.err[2], 1);
     return;
   }
+  PHASE(0)
   double *wsA = c.pool + o.ws;
   double *wsB = wsA + rk_ws_one(m, K, Cfg::CH);
   // A/B. TSQR of both stacked factors, concurrently on two warp groups
@@ -546,6 +567,7 @@ __global__ void __launch_bounds__(HLU_NT)
   }
   __syncthreads();
   const int ra = s_ra, rb = s_rb;
+  PHASE(1)
   // C. core M = R_a R_b^T (ra x rb); G = M or M^T so that G has q <= p columns
   const bool tr = rb > ra;
   const int p = tr ? rb : ra, q = tr ? ra : rb;
@@ -562,7 +584,9 @@ __global__ void __launch_bounds__(HLU_NT)
   __syncthreads();
   // D. SVD of G via QR with column pivoting + one-sided Jacobi on R^T
   //    (G P = Q R, R^T V = W = U S  =>  G = (Q V) S (P U)^T)
+  PHASE(2)
   qrcp<KM>(G, p, q, tau, cmap, sig);
+  PHASE(3)
   for (int e = tid; e < KM * KM; e += HLU_NT) {
     const int i = e % KM, j = e / KM;  // XT[i, j] = R[j, i]
     XT[e] = (i < q && j < q && j <= i) ? G[j + cmap[i] * KM] : 0.0;
@@ -570,7 +594,9 @@ __global__ void __launch_bounds__(HLU_NT)
   const int qq = q + (q & 1);
   build_pairs(pairs_a, pairs_b, qq);
   __syncthreads();
+  PHASE(4)
   jacobi<KM>(XT, V, q, pairs_a, pairs_b);
+  PHASE(5)
   // E. singular values, order, rank
   for (int j = tid; j < q; j += HLU_NT) {
     double ss = 0.0;
@@ -619,8 +645,11 @@ __global__ void __launch_bounds__(HLU_NT)
   __syncthreads();
   for (int col = tid >> 5; col < kk; col += HLU_NWARP) qrcp_apply<KM>(G, p, q, tau, cmap, WQ + col * KM);
   __syncthreads();
-  if (wq < HLU_NWARP / 2) apply_q<KM>(m, K, kk, RA, S, wsA, outA, grp);
-  else apply_q<KM>(n, K, kk, RB, S1, wsB, outB, grp);
+  PHASE(6)
+  const Grp all{0, HLU_NWARP, wq, tid & 31, tid};
+  apply_q<KM>(m, K, kk, RA, S, S1, wsA, outA, all);
+  apply_q<KM>(n, K, kk, RB, S, S1, wsB, outB, all);
+  PHASE(7)
   if (tid == 0) {
     c.ranks[o.out_slot] = kk;
     if (o.log >= 0) c.log[o.log + 2] = kk;
@@ -635,6 +664,22 @@ static size_t rkt_smem() {
 }  // namespace hlu
 
 using namespace hlu;
+
+extern "C" int hlu_debug_phases(double *sum_out, double *max_out, int reset) {
+  unsigned long long a[10], b[10];
+  cudaMemcpyFromSymbol(a, g_phase, sizeof(a));
+  cudaMemcpyFromSymbol(b, g_phase_max, sizeof(b));
+  for (int i = 0; i < 10; ++i) {
+    sum_out[i] = (double)a[i];
+    max_out[i] = (double)b[i];
+  }
+  if (reset) {
+    unsigned long long z[10] = {0};
+    cudaMemcpyToSymbol(g_phase, z, sizeof(z));
+    cudaMemcpyToSymbol(g_phase_max, z, sizeof(z));
+  }
+  return 0;
+}
 
 extern "C" int64_t hlu_debug_sweeps(int reset) {
   unsigned long long v = 0;

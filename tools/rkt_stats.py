@@ -18,6 +18,10 @@ call.launch(); call.check_errors(); call.snapshot()
 p = call.packed
 st = ctypes.c_void_p(call.stream.cuda_stream); ctx = ctypes.byref(call.ctx)
 call.restore(); call.sync(); lib.hlu_debug_sweeps(1)
+import numpy as _np
+ph_s = _np.zeros(10); ph_m = _np.zeros(10)
+lib.hlu_debug_phases.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int]
+lib.hlu_debug_phases(ph_s.ctypes.data, ph_m.ctypes.data, 1)
 tot = {}
 evs = []
 with torch.cuda.stream(call.stream):
@@ -37,6 +41,10 @@ for kind, count, a, b in evs:
     tt = tot.setdefault(k, [0, 0, 0.0, 0.0]); tt[0] += 1; tt[1] += count; tt[2] += t; tt[3] = max(tt[3], t)
 nrkt = len(p.rkt)
 print("sweeps total", lib.hlu_debug_sweeps(0), "rkt ops", nrkt)
+lib.hlu_debug_phases(ph_s.ctypes.data, ph_m.ctypes.data, 0)
+names = ["parts", "tsqr", "core M", "qrcp", "XT+pairs", "jacobi", "rank+W", "apply_q"]
+for i, nm in enumerate(names):
+    print(f"phase {nm:9s} total Mcyc {ph_s[i]/1e6:10.1f}  avg/op kcyc {ph_s[i]/nrkt/1e3:8.2f}  max kcyc {ph_m[i]/1e3:9.1f}")
 for k, (nl, nops, t, mx) in tot.items():
     print(f"{k:6s} launches {nl:6d} ops {nops:8d} total {t:9.2f} ms  per-launch {t/nl:7.3f} ms  max {mx:7.3f}")
 call.restore(); call.sync()
