@@ -21,7 +21,7 @@
 
 namespace {
 
-constexpr int64_t TEMP_SHIFT = 40;
+constexpr int64_t TEMP_SHIFT = 36;  // temp t at (t+1) << 36: up to 2^27 temps, 2^36-double offsets
 constexpr int KMAX_STACK = 64;
 constexpr int IDENT = 64;
 constexpr int F_STATIC = 0, F_LIN = 1, F_RKUPD = 2, F_QUAD = 3;
@@ -167,6 +167,7 @@ struct Planner {
 
   int64_t temp(int64_t doubles, int64_t *base) {
     const int64_t t = (int64_t)temp_size.size();
+    if (t + 1 >= (int64_t(1) << 27)) throw std::runtime_error("too many temporaries for the 36-bit temp encoding");
     temp_size.push_back(doubles);
     *base = (t + 1) << TEMP_SHIFT;
     return t;

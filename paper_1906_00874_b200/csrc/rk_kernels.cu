@@ -179,8 +179,8 @@ __device__ int tsqr(const PartInfo *P, int np, bool left, int m, int K, double *
 // from the workspace with one coalesced copy, so the sequential reflector
 // chain runs out of shared memory; one warp per output column.
 template <int KM>
-__device__ void apply_q(int m, int K, int kk, const double *W, double *T, double *VS, const double *ws,
-                        double *out, const Grp &g) {
+__device__ void apply_q(int m, int K, int kk, const double *W, double *T, double *VS, double *tq,
+                        const double *ws, double *out, const Grp &g) {
   constexpr int LDS = RkCfg<KM>::LDS, CH = RkCfg<KM>::CH;
   const int nch = (m + CH - 1) / CH;
   int64_t off_last = 0;
@@ -215,9 +215,10 @@ __device__ void apply_q(int m, int K, int kk, const double *W, double *T, double
       T[i + j * LDS] = 0.0;
     }
     const double *V = ws + off;
-    for (int e = g.t; e < rows * K + K; e += g.nt()) VS[e] = V[e];  // reflectors (ld rows) + tau
+    for (int e = g.t; e < rows * K; e += g.nt()) VS[e] = V[e];  // reflectors, ld rows (<= BUFD)
+    for (int e = g.t; e < K; e += g.nt()) tq[e] = V[rows * K + e];
     g.sync();
-    const double *tau = VS + rows * K;
+    const double *tau = tq;
     for (int col = g.w; col < kk; col += g.nw) {
       double *t = T + col * LDS;
       for (int j = rs - 1; j >= 0; --j) {
@@ -647,8 +648,8 @@ __global__ void __launch_bounds__(HLU_NT)
   __syncthreads();
   PHASE(6)
   const Grp all{0, HLU_NWARP, wq, tid & 31, tid};
-  apply_q<KM>(m, K, kk, RA, S, S1, wsA, outA, all);
-  apply_q<KM>(n, K, kk, RB, S, S1, wsB, outB, all);
+  apply_q<KM>(m, K, kk, RA, S, S1, tau, wsA, outA, all);
+  apply_q<KM>(n, K, kk, RB, S, S1, tau, wsB, outB, all);
   PHASE(7)
   if (tid == 0) {
     c.ranks[o.out_slot] = kk;

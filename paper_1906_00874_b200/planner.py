@@ -37,7 +37,7 @@ from .ir import (
     TERM_ZERO, TRSM_LEFT_UPPER, TRSM_LOWER_UNIT, TRSM_RIGHT_UPPER, View, colmajor, rkt_ws_doubles,
 )
 
-TEMP_SHIFT = 40  # virtual address of temp t: (t + 1) << TEMP_SHIFT
+TEMP_SHIFT = 36  # virtual address of temp t: (t + 1) << TEMP_SHIFT (2^27 temps, 2^36-double offsets)
 DEFAULT_CAP = 32
 IDENT = 64     # identity block edge kept in the pool
 KMAX_STACK = 64  # largest stacked rank the truncation kernel handles
