@@ -7,15 +7,23 @@ import cases
 from paper_1906_00874_b200.device import DeviceCall
 from paper_1906_00874_b200.lowrank import TruncationControl
 from paper_1906_00874_b200.planner import Layout, Planner
-name = sys.argv[1]
-reps = int(sys.argv[2]) if len(sys.argv) > 2 else 1
-build, ctl = cases.CASES[name]
-h, _ = build()
-L = Layout(h, cap=32); pl = Planner(L); pl.factor(h)
-call = DeviceCall(L, pl, TruncationControl(*ctl), use_graph=True)
-call.snapshot()
-for r in range(reps):
-    call.restore(); t0 = time.perf_counter(); call.launch(); call.sync()
-    print(f"run {r}: {time.perf_counter()-t0:.4f}s", flush=True)
-call.check_errors()
-print("ok", name, "launches", len(call.packed.launches))
+
+
+def main():
+    name = sys.argv[1]
+    reps = int(sys.argv[2]) if len(sys.argv) > 2 else 1
+    build, ctl = cases.CASES[name]
+    h, _ = build()
+    L = Layout(h, cap=32); pl = Planner(L); pl.factor(h)
+    call = DeviceCall(L, pl, TruncationControl(*ctl), use_graph=True)
+    call.snapshot()
+    for r in range(reps):
+        call.restore(); t0 = time.perf_counter(); call.launch(); call.sync()
+        print(f"run {r}: {time.perf_counter()-t0:.4f}s", flush=True)
+    call.check_errors()
+    print("ok", name, "launches", len(call.packed.launches))
+
+
+
+if __name__ == "__main__":
+    main()
