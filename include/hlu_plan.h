@@ -47,8 +47,11 @@ typedef struct {
 
 typedef struct hlu_plan hlu_plan;
 
+/* split_rows > 0: cut GEMM chains whose terms write disjoint row ranges of one
+ * target into independent sub-chains of >= split_rows rows (0 = never) */
 int hlu_plan_build(hlu_plan **out, const hlu_plan_node *nodes, int64_t nnodes, const hlu_plan_cmd *cmds,
-                   int64_t ncmds, int32_t cap, int64_t ident_off, int64_t nslots, int32_t nrk, int64_t arena_base);
+                   int64_t ncmds, int32_t cap, int64_t ident_off, int64_t nslots, int32_t nrk, int64_t arena_base,
+                   int32_t split_rows);
 const char *hlu_plan_error(const hlu_plan *p);
 /* sizes[14]: getrf, trsm, gemm, terms, rkt, parts, launches, ops, levels, arena doubles,
  *            log entries, rank slots, LU count, temps */

@@ -98,6 +98,7 @@ struct TrsmP {
 struct GemmP {
   int64_t tb, tn;
   int log, log_slot;
+  bool split;  // terms only write row ranges of one target and never read it
 };
 struct RktP {
   int mode;
@@ -267,10 +268,10 @@ struct Planner {
 
   int64_t gemm_op(const std::vector<Term> &ts, const std::vector<Iv> &reads, const std::vector<Iv> &writes, int ff,
                   double fc, int log_slot, bool defer, const std::vector<int64_t> &tout,
-                  const std::vector<int64_t> &tin) {
+                  const std::vector<int64_t> &tin, bool splittable = true) {
     int64_t lg = -1;
     if (ff == F_LIN || ff == F_QUAD) lg = log();
-    GemmP g{(int64_t)terms.size(), (int64_t)ts.size(), (int)lg, log_slot};
+    GemmP g{(int64_t)terms.size(), (int64_t)ts.size(), (int)lg, log_slot, splittable};
     terms.insert(terms.end(), ts.begin(), ts.end());
     gemm.push_back(g);
     return emit(2, defer, (int64_t)gemm.size() - 1, reads, writes, tin, tout, ff, fc, lg);
@@ -498,7 +499,8 @@ struct Planner {
     const std::vector<Iv> writes{res(c)};
     if (!rk(a) && !rk(b)) {
       const View av = dense_view(a), bv = dense_view(b);
-      gemm_op({Term{1, dst, av, NULLV, bv, -1.0, 0}}, reads, writes, F_STATIC, 2.0 * m * n * av.cols, -1, false, {}, {});
+      gemm_op({Term{1, dst, av, NULLV, bv, -1.0, 0}}, reads, writes, F_STATIC, 2.0 * m * n * av.cols, -1, false, {}, {},
+              false);
     } else if (rk(a)) {
       View fa, fb;
       factor_views(a, &fa, &fb);
@@ -508,7 +510,7 @@ struct Planner {
       std::vector<Term> ts{Term{0, T, NULLV, NULLV, NULLV, 0.0, 0}};
       terms_tmatmat(ts, T, b, fb, 1.0);
       ts.push_back(Term{1, dst, fa, NULLV, T.T(), -1.0, 0});
-      gemm_op(ts, reads, writes, F_LIN, 2.0 * (m + n) * n, fa.cdyn, false, {t}, {});
+      gemm_op(ts, reads, writes, F_LIN, 2.0 * (m + n) * n, fa.cdyn, false, {t}, {}, false);
     } else {
       View fa, fb;
       factor_views(b, &fa, &fb);
@@ -518,7 +520,7 @@ struct Planner {
       std::vector<Term> ts{Term{0, T, NULLV, NULLV, NULLV, 0.0, 0}};
       terms_matmat(ts, T, a, fa, 1.0);
       ts.push_back(Term{1, dst, T, NULLV, fb.T(), -1.0, 0});
-      gemm_op(ts, reads, writes, F_LIN, 2.0 * (m + n) * m, fa.cdyn, false, {t}, {});
+      gemm_op(ts, reads, writes, F_LIN, 2.0 * (m + n) * m, fa.cdyn, false, {t}, {}, false);
     }
   }
 
@@ -653,7 +655,7 @@ struct Planner {
         const std::vector<Iv> ru{Iv{nd(upj).lo, nd(upj).hi}};
         if (dense) {
           terms_rmatmat(ts, dst, src, whole(upj), -1.0);
-          gemm_op(ts, ru, wr, F_STATIC, 2.0 * dst.rows * dst.cols * src.cols, -1, false, {}, {});
+          gemm_op(ts, ru, wr, F_STATIC, 2.0 * dst.rows * dst.cols * src.cols, -1, false, {}, {}, false);
         } else {
           terms_tmatmat(ts, dst, whole(upj), src, -1.0);
           gemm_op(ts, ru, wr, F_QUAD, 2.0 * dst.rows, dst.cdyn, false, {}, {});
@@ -912,6 +914,90 @@ struct Planner {
     return o;
   }
 
+  int split_rows = 0;  // 0: never split chains; else minimum rows per sub-chain
+
+  void push_term(const Term &t, int64_t ab) {
+    hlu_term h;
+    h.c = fv(t.c, ab);
+    h.a = fv(t.a, ab);
+    h.m = fv(t.m, ab);
+    h.b = fv(t.b, ab);
+    h.alpha = t.alpha;
+    h.kind = t.kind;
+    h.assoc = t.assoc;
+    o_terms.push_back(h);
+  }
+
+  // A chain whose terms write row ranges of one column-major target is cut
+  // into independent sub-chains over disjoint row groups (>= split_rows rows
+  // each); every sub-chain keeps the original term order on its rows.
+  void emit_gemm(const GemmP &g, int64_t ab) {
+    bool ok = split_rows > 0 && g.split && g.tn > 1;
+    int64_t base = 0, ld = 0, cols = 0;
+    if (ok) {
+      const Term &t0 = terms[g.tb];
+      base = t0.c.off;
+      ld = t0.c.cs;
+      cols = t0.c.cols;
+      for (int64_t k = g.tb; k < g.tb + g.tn && ok; ++k) {
+        const View &c = terms[k].c;
+        if (c.rs != 1 || c.cs != ld || c.cols != cols || c.rdyn >= 0 || c.cdyn != t0.c.cdyn) ok = false;
+        base = std::min(base, c.off);
+      }
+      for (int64_t k = g.tb; k < g.tb + g.tn && ok; ++k) {
+        const int64_t r0 = terms[k].c.off - base;
+        if (r0 < 0 || r0 + terms[k].c.rows > ld) ok = false;  // not row slices of one target
+        if (terms[k].kind != 0 && terms[k].a.rdyn >= 0) ok = false;
+      }
+    }
+    std::vector<int64_t> cuts;
+    if (ok) {
+      for (int64_t k = g.tb; k < g.tb + g.tn; ++k) {
+        const int64_t r0 = terms[k].c.off - base;
+        cuts.push_back(r0);
+        cuts.push_back(r0 + terms[k].c.rows);
+      }
+      std::sort(cuts.begin(), cuts.end());
+      cuts.erase(std::unique(cuts.begin(), cuts.end()), cuts.end());
+      std::vector<int64_t> merged{cuts.front()};
+      for (size_t i = 1; i < cuts.size(); ++i)
+        if (cuts[i] - merged.back() >= split_rows || i + 1 == cuts.size()) merged.push_back(cuts[i]);
+      cuts.swap(merged);
+      if (cuts.size() <= 2) ok = false;
+    }
+    if (!ok) {
+      hlu_gemm_desc d;
+      d.term_begin = (int32_t)o_terms.size();
+      d.term_count = (int32_t)g.tn;
+      d.log = g.log;
+      d.log_slot = g.log_slot;
+      for (int64_t k = g.tb; k < g.tb + g.tn; ++k) push_term(terms[k], ab);
+      o_gemm.push_back(d);
+      return;
+    }
+    for (size_t q = 0; q + 1 < cuts.size(); ++q) {
+      const int64_t g0 = cuts[q], g1 = cuts[q + 1];
+      hlu_gemm_desc d;
+      d.term_begin = (int32_t)o_terms.size();
+      d.log = g.log;
+      d.log_slot = g.log_slot;
+      int cnt = 0;
+      for (int64_t k = g.tb; k < g.tb + g.tn; ++k) {
+        const Term &t = terms[k];
+        const int64_t r0 = t.c.off - base, r1 = r0 + t.c.rows;
+        const int64_t lo = std::max(r0, g0), hi = std::min(r1, g1);
+        if (lo >= hi) continue;
+        Term p = t;
+        p.c = t.c.rows_slice((int)(lo - r0), (int)(hi - r0));
+        if (t.kind != 0) p.a = t.a.rows_slice((int)(lo - r0), (int)(hi - r0));
+        push_term(p, ab);
+        ++cnt;
+      }
+      d.term_count = cnt;
+      o_gemm.push_back(d);
+    }
+  }
+
   void pack(int64_t arena_base) {
     assign_levels();
     allocate_temps();
@@ -934,7 +1020,7 @@ struct Planner {
       const Op &o = ops[i];
       const int64_t lv = levels[i];
       int kind = 0, dim = 0;
-      int64_t idx = 0;
+      int64_t idx = 0, extra = 0;
       if (o.kind == 0) {
         const GetrfP &g = getrf[o.payload];
         hlu_getrf_desc d;
@@ -958,27 +1044,12 @@ struct Planner {
         dim = t.t.rows;
       } else if (o.kind == 2) {
         const GemmP &g = gemm[o.payload];
-        hlu_gemm_desc d;
-        d.term_begin = (int32_t)o_terms.size();
-        d.term_count = (int32_t)g.tn;
-        d.log = g.log;
-        d.log_slot = g.log_slot;
-        for (int64_t k = g.tb; k < g.tb + g.tn; ++k) {
-          const Term &t = terms[k];
-          hlu_term h;
-          h.c = fv(t.c, arena_base);
-          h.a = fv(t.a, arena_base);
-          h.m = fv(t.m, arena_base);
-          h.b = fv(t.b, arena_base);
-          h.alpha = t.alpha;
-          h.kind = t.kind;
-          h.assoc = t.assoc;
-          o_terms.push_back(h);
-        }
-        o_gemm.push_back(d);
+        const int64_t first_desc = (int64_t)o_gemm.size();
+        emit_gemm(g, arena_base);
         kind = HLU_K_GEMM;
-        idx = (int64_t)o_gemm.size() - 1;
+        idx = first_desc;
         dim = 0;
+        extra = (int64_t)o_gemm.size() - first_desc - 1;
       } else {
         const RktP &r = rkt[o.payload];
         hlu_rkt_desc d;
@@ -1011,10 +1082,10 @@ struct Planner {
         dim = r.kb;
       }
       if (!recs.empty() && cur_lv == lv && cur_kind == kind) {
-        recs.back().count += 1;
+        recs.back().count += 1 + extra;
         recs.back().dim = std::max(recs.back().dim, dim);
       } else {
-        recs.push_back(Rec{kind, 1, idx, dim});
+        recs.push_back(Rec{kind, 1 + extra, idx, dim});
         cur_lv = lv;
         cur_kind = kind;
       }
@@ -1050,7 +1121,7 @@ struct hlu_plan {
 
 extern "C" int hlu_plan_build(hlu_plan **out, const hlu_plan_node *nodes, int64_t nnodes, const hlu_plan_cmd *cmds,
                               int64_t ncmds, int32_t cap, int64_t ident_off, int64_t nslots, int32_t nrk,
-                              int64_t arena_base) {
+                              int64_t arena_base, int32_t split_rows) {
   hlu_plan *p = new hlu_plan();
   *out = p;
   Planner &P = p->P;
@@ -1060,6 +1131,7 @@ extern "C" int hlu_plan_build(hlu_plan **out, const hlu_plan_node *nodes, int64_
   P.ident_off = ident_off;
   P.nslots = nslots;
   P.nrank = nrk;
+  P.split_rows = split_rows;
   try {
     for (int64_t i = 0; i < ncmds; ++i) {
       const hlu_plan_cmd &c = cmds[i];

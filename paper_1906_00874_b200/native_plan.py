@@ -41,7 +41,7 @@ def lib():
             raise RuntimeError(f"planner library {PLAN_LIB} missing: run `make`")
         L = ctypes.CDLL(PLAN_LIB)
         vp, i64, i32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32
-        L.hlu_plan_build.argtypes = [ctypes.POINTER(vp), vp, i64, vp, i64, i32, i64, i64, i32, i64]
+        L.hlu_plan_build.argtypes = [ctypes.POINTER(vp), vp, i64, vp, i64, i32, i64, i64, i32, i64, i32]
         L.hlu_plan_build.restype = ctypes.c_int
         L.hlu_plan_error.argtypes = [vp]
         L.hlu_plan_error.restype = ctypes.c_char_p
@@ -99,7 +99,10 @@ def flatten_nodes(layout):
     return nodes, index
 
 
-def plan(layout, commands):
+SPLIT_ROWS = 64
+
+
+def plan(layout, commands, split_rows=SPLIT_ROWS):
     """commands: list of (kind, nodes..., extras) in the planner's terms:
     ("factor", h) | ("solve_lower", l, b) | ("solve_upper", b, u) |
     ("update", c, a, b) | ("fwd", h, name) | ("bwd", h, name)."""
@@ -123,7 +126,8 @@ def plan(layout, commands):
     L = lib()
     h = ctypes.c_void_p()
     rc = L.hlu_plan_build(ctypes.byref(h), nodes.ctypes.data, len(nodes), cmds.ctypes.data, len(cmds),
-                          layout.cap, layout.ident_off, layout.nslots, layout.nrk, layout.payload_doubles)
+                          layout.cap, layout.ident_off, layout.nslots, layout.nrk, layout.payload_doubles,
+                          int(split_rows))
     try:
         if rc != 0:
             from .hmatrix import StructureError

@@ -33,7 +33,7 @@ def test_factor_plans_identical(name):
     pl = Planner(L)
     pl.factor(h)
     p_py = pack(pl, L.payload_doubles)
-    p_nat, nops = native_plan.plan(L, [("factor", h)])
+    p_nat, nops = native_plan.plan(L, [("factor", h)], split_rows=0)
     assert nops == len(pl.ops)
     _compare(p_py, p_nat)
 
@@ -47,7 +47,7 @@ def test_solve_and_update_plans_identical():
         L = Layout(roots, cap=32)
         pl = Planner(L)
         getattr(pl, cmd[0])(*cmd[1:])
-        _compare(pack(pl, L.payload_doubles), native_plan.plan(L, [cmd])[0])
+        _compare(pack(pl, L.payload_doubles), native_plan.plan(L, [cmd], split_rows=0)[0])
 
 
 def test_vector_solve_plans_identical():
@@ -56,4 +56,29 @@ def test_vector_solve_plans_identical():
     pl = Planner(L)
     pl.forward_vector(h, "x")
     pl.backward_vector(h, "x")
-    _compare(pack(pl, L.payload_doubles), native_plan.plan(L, [("fwd", h, "x"), ("bwd", h, "x")])[0])
+    _compare(pack(pl, L.payload_doubles), native_plan.plan(L, [("fwd", h, "x"), ("bwd", h, "x")], split_rows=0)[0])
+
+
+@pytest.mark.parametrize("name", ["mixed_192", "bem1d_1024", "sphere_1024"])
+def test_split_chains_reproduce_reference(name):
+    """The production plan (GEMM chains cut into row-group sub-chains) executed
+    by the CPU IR machine still reproduces the reference ranks and flops."""
+    from ir_exec import CpuMachine
+    from paper_1906_00874_b200.pool import fill_pool, read_pool
+    from paper_1906_00874_b200.schedule import effective_flops
+
+    g = cases.golden(name)
+    build, ctl = cases.CASES[name]
+    h, _ = build()
+    L = Layout(h, cap=32)
+    p, _ = native_plan.plan(L, [("factor", h)], split_rows=16)
+    p0, _ = native_plan.plan(L, [("factor", h)], split_rows=0)
+    assert len(p.gemm) >= len(p0.gemm)
+    pool = np.zeros(L.payload_doubles + p.arena_doubles)
+    ranks = np.zeros(p.nranks, np.int32)
+    fill_pool(L, pool, ranks)
+    M = CpuMachine(pool, ranks, p.nlog, ctl[0], ctl[1])
+    M.run(p)
+    read_pool(L, pool, ranks)
+    assert np.array_equal(cases.ranks(h), g["ranks_out"])
+    assert abs(effective_flops(p, M.log) - float(g["flops"])) <= 1e-12 * float(g["flops"])
