@@ -142,6 +142,9 @@ def time_rkt_launches(call, torch):
             elif kind == ir.K_GEMM:
                 lib.hlu_gemm_batched_f64(ctx, call.d_gemm.data_ptr() + first * ir.GEMM.itemsize,
                                          call.d_terms.data_ptr(), count, st)
+            elif kind == ir.K_GEMM_SMALL:
+                lib.hlu_gemm_small_batched_f64(ctx, call.d_gemm.data_ptr() + first * ir.GEMM.itemsize,
+                                               call.d_terms.data_ptr(), count, st)
             else:  # RKT (+ its KM=64 companion) timed as one launch group
                 e0 = torch.cuda.Event(enable_timing=True)
                 e1 = torch.cuda.Event(enable_timing=True)

@@ -117,7 +117,7 @@ typedef struct {
 } hlu_rkt_desc; /* 64 bytes */
 
 /* launch kinds of a schedule entry */
-enum { HLU_K_GETRF = 0, HLU_K_TRSM = 1, HLU_K_GEMM = 2, HLU_K_RKT32 = 3, HLU_K_RKT64 = 4 };
+enum { HLU_K_GETRF = 0, HLU_K_TRSM = 1, HLU_K_GEMM = 2, HLU_K_RKT32 = 3, HLU_K_RKT64 = 4, HLU_K_GEMM_SMALL = 5 };
 
 typedef struct {
   int32_t kind;
@@ -132,6 +132,10 @@ int hlu_getrf_batched_f64(const hlu_ctx *ctx, const hlu_getrf_desc *d, int count
 int hlu_trsm_batched_f64(const hlu_ctx *ctx, const hlu_trsm_desc *d, int count, int max_n, void *stream);
 int hlu_gemm_batched_f64(const hlu_ctx *ctx, const hlu_gemm_desc *d, const hlu_term *terms, int count,
                          void *stream);
+/* small chains (planner-classified: every triple's M.rows x C.cols <= 1024,
+ * assoc-1 triples with M.cols <= 64): one warp per chain */
+int hlu_gemm_small_batched_f64(const hlu_ctx *ctx, const hlu_gemm_desc *d, const hlu_term *terms, int count,
+                               void *stream);
 int hlu_rk_update_batched_f64(const hlu_ctx *ctx, hlu_rkt_desc *d, const hlu_rkpart *parts,
                               int count, int kclass, void *stream);
 

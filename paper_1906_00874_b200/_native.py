@@ -17,6 +17,7 @@ SYMBOLS = (
     "hlu_getrf_batched_f64",
     "hlu_trsm_batched_f64",
     "hlu_gemm_batched_f64",
+    "hlu_gemm_small_batched_f64",
     "hlu_rk_update_batched_f64",
     "hlu_rkt_ws_doubles",
     "hlu_schedule_create",
@@ -60,6 +61,7 @@ def lib():
     L.hlu_getrf_batched_f64.argtypes = [ctypes.POINTER(HluCtx), vp, i32, i32, vp]
     L.hlu_trsm_batched_f64.argtypes = [ctypes.POINTER(HluCtx), vp, i32, i32, vp]
     L.hlu_gemm_batched_f64.argtypes = [ctypes.POINTER(HluCtx), vp, vp, i32, vp]
+    L.hlu_gemm_small_batched_f64.argtypes = [ctypes.POINTER(HluCtx), vp, vp, i32, vp]
     L.hlu_rk_update_batched_f64.argtypes = [ctypes.POINTER(HluCtx), vp, vp, i32, i32, vp]
     L.hlu_rkt_ws_doubles.argtypes = [i32, i32]
     L.hlu_rkt_ws_doubles.restype = i64
@@ -68,7 +70,7 @@ def lib():
     L.hlu_schedule_launch.argtypes = [vp, vp]
     L.hlu_schedule_destroy.argtypes = [vp]
     L.hlu_version.restype = ctypes.c_char_p
-    for name in ("hlu_getrf_batched_f64", "hlu_trsm_batched_f64", "hlu_gemm_batched_f64",
+    for name in ("hlu_getrf_batched_f64", "hlu_trsm_batched_f64", "hlu_gemm_batched_f64", "hlu_gemm_small_batched_f64",
                  "hlu_rk_update_batched_f64", "hlu_schedule_create", "hlu_schedule_launch",
                  "hlu_schedule_destroy", "hlu_device_check"):
         getattr(L, name).restype = ctypes.c_int

@@ -262,6 +262,95 @@ __global__ void __launch_bounds__(HLU_NT)
   }
 }
 
+// ---------------------------------------------------------------------------
+// Warp-per-chain GEMM for small chains (classified statically by the planner):
+// lane = output column, 16-row register blocks, broadcast loads of A; a triple
+// term stages W = M B (<= WSMALL doubles) or a row block of A M in per-warp
+// shared memory.  Terms run in order with __syncwarp between them.
+// ---------------------------------------------------------------------------
+#define WSMALL 1024
+#define RB 16
+
+// C (m x n) += alpha * A (m x k) * B (k x n); one warp.
+__device__ __forceinline__ void warp_gemm(const Mat &C, const Mat &A, const Mat &B, double alpha) {
+  const int l = threadIdx.x & 31;
+  const int m = C.rows, n = C.cols, k = A.cols;
+  for (int c = l; c - l < n; c += 32) {
+    const bool on = c < n;
+    for (int r0 = 0; r0 < m; r0 += RB) {
+      double acc[RB];
+#pragma unroll
+      for (int i = 0; i < RB; ++i) acc[i] = 0.0;
+      const int rr = min(RB, m - r0);
+      for (int t = 0; t < k; ++t) {
+        const double b = on ? B.get(t, c) : 0.0;
+#pragma unroll
+        for (int i = 0; i < RB; ++i)
+          if (i < rr) acc[i] = fma(A.get(r0 + i, t), b, acc[i]);
+      }
+      if (on) {
+#pragma unroll
+        for (int i = 0; i < RB; ++i)
+          if (i < rr) C.at(r0 + i, c) += alpha * acc[i];
+      }
+    }
+  }
+  __syncwarp();
+}
+
+__global__ void __launch_bounds__(HLU_NT)
+    k_gemm_warp(hlu_ctx c, const hlu_gemm_desc *__restrict__ d, const hlu_term *__restrict__ terms, int count) {
+  extern __shared__ double wbuf[];
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  const int di = blockIdx.x * HLU_NWARP + w;
+  if (di >= count) return;
+  const hlu_gemm_desc o = d[di];
+  if (o.log >= 0 && l == 0) c.log[o.log] = c.ranks[o.log_slot];
+  double *W = wbuf + w * WSMALL;
+  for (int t = 0; t < o.term_count; ++t) {
+    const hlu_term tm = terms[o.term_begin + t];
+    const Mat C = resolve(c, tm.c);
+    if (tm.kind == HLU_TERM_ZERO) {
+      for (int e = l; e < C.rows * C.cols; e += 32) C.at(e % C.rows, e / C.rows) = 0.0;
+      __syncwarp();
+      continue;
+    }
+    if (C.rows == 0 || C.cols == 0) continue;
+    const Mat A = resolve(c, tm.a);
+    const Mat B = resolve(c, tm.b);
+    if (tm.kind == HLU_TERM_GEMM) {
+      if (A.cols > 0) warp_gemm(C, A, B, tm.alpha);
+      continue;
+    }
+    const Mat M = resolve(c, tm.m);
+    if (M.rows == 0 || M.cols == 0) continue;
+    if (tm.assoc == 0) {
+      // W (k1 x n) = M B, then C += alpha A W
+      const Mat Ws = smat(W, M.rows, C.cols, M.rows);
+      for (int e = l; e < M.rows * C.cols; e += 32) W[e] = 0.0;
+      __syncwarp();
+      warp_gemm(Ws, M, B, 1.0);
+      warp_gemm(C, A, Ws, tm.alpha);
+    } else {
+      // per row block: W (rb x k2) = A[rb,:] M, then C[rb,:] += alpha W B
+      for (int r0 = 0; r0 < C.rows; r0 += RB) {
+        const int rr = min(RB, C.rows - r0);
+        const Mat Ws = smat(W, rr, M.cols, rr);
+        for (int e = l; e < rr * M.cols; e += 32) W[e] = 0.0;
+        __syncwarp();
+        Mat Ar = A;
+        Ar.p = A.p + r0 * A.rs;
+        Ar.rows = rr;
+        Mat Cr = C;
+        Cr.p = C.p + r0 * C.rs;
+        Cr.rows = rr;
+        warp_gemm(Ws, Ar, M, 1.0);
+        warp_gemm(Cr, Ws, B, tm.alpha);
+      }
+    }
+  }
+}
+
 }  // namespace hlu
 
 using namespace hlu;
@@ -299,5 +388,18 @@ extern "C" int hlu_gemm_batched_f64(const hlu_ctx *ctx, const hlu_gemm_desc *d, 
                                     int count, void *stream) {
   if (count <= 0) return 0;
   k_gemm<<<count, HLU_NT, 0, (cudaStream_t)stream>>>(*ctx, d, terms);
+  return cudaGetLastError() == cudaSuccess ? 0 : -1;
+}
+
+extern "C" int hlu_gemm_small_batched_f64(const hlu_ctx *ctx, const hlu_gemm_desc *d, const hlu_term *terms,
+                                          int count, void *stream) {
+  const size_t smem = (size_t)HLU_NWARP * WSMALL * sizeof(double);
+  static bool init = false;
+  if (!init) {
+    cudaFuncSetAttribute(k_gemm_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    init = true;
+  }
+  if (count <= 0) return 0;
+  k_gemm_warp<<<(count + HLU_NWARP - 1) / HLU_NWARP, HLU_NT, smem, (cudaStream_t)stream>>>(*ctx, d, terms, count);
   return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }

@@ -916,7 +916,7 @@ struct Planner {
 
   int split_rows = 0;  // 0: never split chains; else minimum rows per sub-chain
 
-  void push_term(const Term &t, int64_t ab) {
+  void push_term(std::vector<hlu_term> &out, const Term &t, int64_t ab) {
     hlu_term h;
     h.c = fv(t.c, ab);
     h.a = fv(t.a, ab);
@@ -925,13 +925,32 @@ struct Planner {
     h.alpha = t.alpha;
     h.kind = t.kind;
     h.assoc = t.assoc;
-    o_terms.push_back(h);
+    out.push_back(h);
+  }
+
+  // small enough for the warp-per-chain kernel (hlu_gemm_small_batched_f64)
+  static bool small_chain(const hlu_term *t, int n) {
+    for (int i = 0; i < n; ++i) {
+      if (t[i].kind == 0) continue;
+      const double crc = (double)t[i].c.rows * t[i].c.cols;
+      if (t[i].kind == 1) {
+        if (crc * t[i].a.cols > 131072.0) return false;
+      } else if (t[i].assoc == 0) {
+        if ((double)t[i].m.rows * t[i].c.cols > 1024.0) return false;
+        if ((double)t[i].m.rows * t[i].c.cols * t[i].m.cols + crc * t[i].a.cols > 262144.0) return false;
+      } else {
+        if (t[i].m.cols > 64) return false;
+        if (crc * t[i].a.cols + crc * t[i].m.cols > 262144.0) return false;
+      }
+    }
+    return true;
   }
 
   // A chain whose terms write row ranges of one column-major target is cut
   // into independent sub-chains over disjoint row groups (>= split_rows rows
   // each); every sub-chain keeps the original term order on its rows.
-  void emit_gemm(const GemmP &g, int64_t ab) {
+  // appends the op's chain(s) to (large, small) staging lists
+  void emit_gemm(const GemmP &g, int64_t ab, std::vector<std::vector<hlu_term>> &chains) {
     bool ok = split_rows > 0 && g.split && g.tn > 1;
     int64_t base = 0, ld = 0, cols = 0;
     if (ok) {
@@ -966,22 +985,13 @@ struct Planner {
       if (cuts.size() <= 2) ok = false;
     }
     if (!ok) {
-      hlu_gemm_desc d;
-      d.term_begin = (int32_t)o_terms.size();
-      d.term_count = (int32_t)g.tn;
-      d.log = g.log;
-      d.log_slot = g.log_slot;
-      for (int64_t k = g.tb; k < g.tb + g.tn; ++k) push_term(terms[k], ab);
-      o_gemm.push_back(d);
+      chains.emplace_back();
+      for (int64_t k = g.tb; k < g.tb + g.tn; ++k) push_term(chains.back(), terms[k], ab);
       return;
     }
     for (size_t q = 0; q + 1 < cuts.size(); ++q) {
       const int64_t g0 = cuts[q], g1 = cuts[q + 1];
-      hlu_gemm_desc d;
-      d.term_begin = (int32_t)o_terms.size();
-      d.log = g.log;
-      d.log_slot = g.log_slot;
-      int cnt = 0;
+      chains.emplace_back();
       for (int64_t k = g.tb; k < g.tb + g.tn; ++k) {
         const Term &t = terms[k];
         const int64_t r0 = t.c.off - base, r1 = r0 + t.c.rows;
@@ -990,13 +1000,16 @@ struct Planner {
         Term p = t;
         p.c = t.c.rows_slice((int)(lo - r0), (int)(hi - r0));
         if (t.kind != 0) p.a = t.a.rows_slice((int)(lo - r0), (int)(hi - r0));
-        push_term(p, ab);
-        ++cnt;
+        push_term(chains.back(), p, ab);
       }
-      d.term_count = cnt;
-      o_gemm.push_back(d);
     }
   }
+
+  struct StagedChain {
+    int log, log_slot;
+    std::vector<hlu_term> terms;
+  };
+  std::vector<StagedChain> stage_large, stage_small;
 
   void pack(int64_t arena_base) {
     assign_levels();
@@ -1016,9 +1029,33 @@ struct Planner {
     std::vector<Rec> recs;
     int64_t cur_lv = -1;
     int cur_kind = -1;
+    int64_t pending_lv = -1;
+    auto flush_gemm = [&]() {
+      for (int pass = 0; pass < 2; ++pass) {
+        auto &st = pass == 0 ? stage_large : stage_small;
+        if (st.empty()) continue;
+        const int64_t first = (int64_t)o_gemm.size();
+        for (auto &c : st) {
+          hlu_gemm_desc d;
+          d.term_begin = (int32_t)o_terms.size();
+          d.term_count = (int32_t)c.terms.size();
+          d.log = c.log;
+          d.log_slot = c.log_slot;
+          o_terms.insert(o_terms.end(), c.terms.begin(), c.terms.end());
+          o_gemm.push_back(d);
+        }
+        recs.push_back(Rec{pass == 0 ? HLU_K_GEMM : HLU_K_GEMM_SMALL, (int64_t)st.size(), first, 0});
+        st.clear();
+      }
+      cur_kind = -1;
+    };
     for (int64_t i : order) {
       const Op &o = ops[i];
       const int64_t lv = levels[i];
+      if (pending_lv >= 0 && (o.kind != 2 || lv != pending_lv)) {
+        flush_gemm();
+        pending_lv = -1;
+      }
       int kind = 0, dim = 0;
       int64_t idx = 0, extra = 0;
       if (o.kind == 0) {
@@ -1044,12 +1081,15 @@ struct Planner {
         dim = t.t.rows;
       } else if (o.kind == 2) {
         const GemmP &g = gemm[o.payload];
-        const int64_t first_desc = (int64_t)o_gemm.size();
-        emit_gemm(g, arena_base);
-        kind = HLU_K_GEMM;
-        idx = first_desc;
-        dim = 0;
-        extra = (int64_t)o_gemm.size() - first_desc - 1;
+        std::vector<std::vector<hlu_term>> chains;
+        emit_gemm(g, arena_base, chains);
+        for (auto &ch : chains) {
+          const bool sm = split_rows > 0 && small_chain(ch.data(), (int)ch.size());
+          auto &dst = sm ? stage_small : stage_large;
+          dst.push_back({g.log, g.log_slot, std::move(ch)});
+        }
+        pending_lv = lv;
+        continue;
       } else {
         const RktP &r = rkt[o.payload];
         hlu_rkt_desc d;
@@ -1090,6 +1130,7 @@ struct Planner {
         cur_kind = kind;
       }
     }
+    if (pending_lv >= 0) flush_gemm();
     for (const Rec &r : recs) {
       hlu_launch L;
       L.kind = r.kind;

@@ -37,6 +37,9 @@ static int run_launches(hlu_schedule *s, cudaStream_t st) {
       case HLU_K_GEMM:
         rc = hlu_gemm_batched_f64(&s->ctx, s->gemm + L.first, s->terms, L.count, st);
         break;
+      case HLU_K_GEMM_SMALL:
+        rc = hlu_gemm_small_batched_f64(&s->ctx, s->gemm + L.first, s->terms, L.count, st);
+        break;
       case HLU_K_RKT32:
         rc = hlu_rk_update_batched_f64(&s->ctx, s->rkt + L.first, s->parts, L.count, 32, st);
         break;
@@ -73,6 +76,7 @@ extern "C" int hlu_schedule_create(hlu_schedule **out, const hlu_ctx *ctx, const
     hlu_getrf_batched_f64(&s->ctx, s->getrf, 0, 0, st);
     hlu_trsm_batched_f64(&s->ctx, s->trsm, 0, 0, st);
     hlu_rk_update_batched_f64(&s->ctx, s->rkt, s->parts, 0, 32, st);
+    hlu_gemm_small_batched_f64(&s->ctx, s->gemm, s->terms, 0, st);
     if (cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
       delete s;
       return -10;

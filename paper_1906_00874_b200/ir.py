@@ -31,7 +31,7 @@ assert TERM.itemsize == 144 and GEMM.itemsize == 16 and RKPART.itemsize == 80
 assert RKT.itemsize == 64 and LAUNCH.itemsize == 24
 
 # kinds (hlu_b200.h)
-K_GETRF, K_TRSM, K_GEMM, K_RKT32, K_RKT64 = 0, 1, 2, 3, 4
+K_GETRF, K_TRSM, K_GEMM, K_RKT32, K_RKT64, K_GEMM_SMALL = 0, 1, 2, 3, 4, 5
 TRSM_LOWER_UNIT, TRSM_RIGHT_UPPER, TRSM_LEFT_UPPER = 0, 1, 2
 TERM_ZERO, TERM_GEMM, TERM_TRIPLE = 0, 1, 2
 RK_ADD, RK_RECOMPRESS = 0, 1

@@ -154,7 +154,7 @@ class CpuMachine:
             elif kind == ir.K_TRSM:
                 for i in rng:
                     self.trsm(packed.trsm[i])
-            elif kind == ir.K_GEMM:
+            elif kind in (ir.K_GEMM, ir.K_GEMM_SMALL):
                 for i in rng:
                     self.gemm(packed.gemm[i], packed.terms)
             elif kind == ir.K_RKT32:  # RKT64 launches cover the same ops

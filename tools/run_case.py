@@ -14,7 +14,8 @@ def main():
     reps = int(sys.argv[2]) if len(sys.argv) > 2 else 1
     build, ctl = cases.CASES[name]
     h, _ = build()
-    L = Layout(h, cap=32); pl = Planner(L); pl.factor(h)
+    from paper_1906_00874_b200.hlu import plan_call
+    L, pl = plan_call([h], [("factor", h)], 32)
     call = DeviceCall(L, pl, TruncationControl(*ctl), use_graph=True)
     call.snapshot()
     for r in range(reps):
