@@ -146,8 +146,12 @@ __global__ void __launch_bounds__(HLU_NT) k_trsm(hlu_ctx c, const hlu_trsm_desc 
 // each thread a 4x4 register tile (rows ty+16q, cols tx+16q).
 // ---------------------------------------------------------------------------
 #define GB 64
-#define GK 16
+#define GK 32
+#define GPF (GB * GK / HLU_NT)  // tile elements each thread stages per operand (8)
 
+// C += alpha * A B.  64x64 output tiles, 32-deep k-steps; the next k-tile is
+// prefetched into registers while the current one is consumed from shared
+// memory, so each k-step costs max(load latency, compute) instead of the sum.
 __device__ void tile_gemm(const Mat &C, const Mat &A, const Mat &B, double alpha, double *sA,
                           double *sB) {
   const int m = C.rows, n = C.cols, k = A.cols;
@@ -159,19 +163,32 @@ __device__ void tile_gemm(const Mat &C, const Mat &A, const Mat &B, double alpha
       for (int a = 0; a < 4; ++a)
 #pragma unroll
         for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
-      for (int k0 = 0; k0 < k; k0 += GK) {
-        __syncthreads();
-        for (int e = tid; e < GB * GK; e += HLU_NT) {
+      double pa[GPF], pb[GPF];
+      auto fetch = [&](int k0) {
+#pragma unroll
+        for (int u = 0; u < GPF; ++u) {
+          const int e = tid + u * HLU_NT;
           const int r = e % GB, q = e / GB;  // A tile: row r, k q
           const int gi = i0 + r, gk = k0 + q;
-          sA[q * GB + r] = (gi < m && gk < k) ? A.get(gi, gk) : 0.0;
+          pa[u] = (gi < m && gk < k) ? A.get(gi, gk) : 0.0;
           const int cc = e % GB, qq = e / GB;  // B tile: k qq, col cc
           const int bj = j0 + cc, bk = k0 + qq;
-          sB[qq * GB + cc] = (bk < k && bj < n) ? B.get(bk, bj) : 0.0;
+          pb[u] = (bk < k && bj < n) ? B.get(bk, bj) : 0.0;
         }
+      };
+      fetch(0);
+      for (int k0 = 0; k0 < k; k0 += GK) {
         __syncthreads();
 #pragma unroll
-        for (int q = 0; q < GK; ++q) {
+        for (int u = 0; u < GPF; ++u) {
+          const int e = tid + u * HLU_NT;
+          sA[(e / GB) * GB + e % GB] = pa[u];
+          sB[(e / GB) * GB + e % GB] = pb[u];
+        }
+        __syncthreads();
+        if (k0 + GK < k) fetch(k0 + GK);  // in flight during the FMAs below
+        const int kk = min(GK, k - k0);
+        for (int q = 0; q < kk; ++q) {
           double av[4], bv[4];
 #pragma unroll
           for (int a = 0; a < 4; ++a) av[a] = sA[q * GB + ty + 16 * a];
@@ -213,9 +230,10 @@ __device__ void zero_mat(const Mat &C) {
 
 __global__ void __launch_bounds__(HLU_NT)
     k_gemm(hlu_ctx c, const hlu_gemm_desc *__restrict__ d, const hlu_term *__restrict__ terms) {
-  __shared__ double sA[GB * GK];
-  __shared__ double sB[GB * GK];
-  __shared__ double sW[GB * GB];
+  extern __shared__ double gsm[];
+  double *sA = gsm;
+  double *sB = sA + GB * GK;
+  double *sW = sB + GB * GK;
   const hlu_gemm_desc o = d[blockIdx.x];
   if (o.log >= 0 && threadIdx.x == 0) c.log[o.log] = c.ranks[o.log_slot];
   for (int t = 0; t < o.term_count; ++t) {
@@ -386,8 +404,14 @@ extern "C" int hlu_trsm_batched_f64(const hlu_ctx *ctx, const hlu_trsm_desc *d, 
 
 extern "C" int hlu_gemm_batched_f64(const hlu_ctx *ctx, const hlu_gemm_desc *d, const hlu_term *terms,
                                     int count, void *stream) {
+  const size_t smem = (size_t)(2 * GB * GK + GB * GB) * sizeof(double);
+  static bool init = false;
+  if (!init) {
+    cudaFuncSetAttribute(k_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    init = true;
+  }
   if (count <= 0) return 0;
-  k_gemm<<<count, HLU_NT, 0, (cudaStream_t)stream>>>(*ctx, d, terms);
+  k_gemm<<<count, HLU_NT, smem, (cudaStream_t)stream>>>(*ctx, d, terms);
   return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }
 

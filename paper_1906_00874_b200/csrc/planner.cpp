@@ -915,6 +915,7 @@ struct Planner {
   }
 
   int split_rows = 0;  // 0: never split chains; else minimum rows per sub-chain
+  bool small_gemm = false;  // route small chains to the warp-per-chain kernel
 
   void push_term(std::vector<hlu_term> &out, const Term &t, int64_t ab) {
     hlu_term h;
@@ -1084,7 +1085,7 @@ struct Planner {
         std::vector<std::vector<hlu_term>> chains;
         emit_gemm(g, arena_base, chains);
         for (auto &ch : chains) {
-          const bool sm = split_rows > 0 && small_chain(ch.data(), (int)ch.size());
+          const bool sm = small_gemm && small_chain(ch.data(), (int)ch.size());
           auto &dst = sm ? stage_small : stage_large;
           dst.push_back({g.log, g.log_slot, std::move(ch)});
         }

@@ -77,6 +77,7 @@ extern "C" int hlu_schedule_create(hlu_schedule **out, const hlu_ctx *ctx, const
     hlu_trsm_batched_f64(&s->ctx, s->trsm, 0, 0, st);
     hlu_rk_update_batched_f64(&s->ctx, s->rkt, s->parts, 0, 32, st);
     hlu_gemm_small_batched_f64(&s->ctx, s->gemm, s->terms, 0, st);
+    hlu_gemm_batched_f64(&s->ctx, s->gemm, s->terms, 0, st);
     if (cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
       delete s;
       return -10;

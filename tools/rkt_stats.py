@@ -63,7 +63,7 @@ def main():
             ts = p.terms[int(g["term_begin"]): int(g["term_begin"]) + int(g["term_count"])]
             big = [(int(t["kind"]), int(t["c"]["rows"]), int(t["c"]["cols"]), int(t["a"]["cols"]), int(t["m"]["rows"]), int(t["m"]["cols"]), int(t["b"]["rows"]), int(t["assoc"])) for t in ts]
             work = sum(c_r * c_c * max(a_c, 1) + mr * mc * c_c for (_, c_r, c_c, a_c, mr, mc, b_r, _) in big)
-            if work > 5e7 or len(ts) > 100:
+            if gi < first + 3 or work > 5e7 or len(ts) > 100:
                 print("  desc", gi, "terms", len(ts), "work", f"{work:.3g}", big[:4])
     call.restore(); call.sync()
     t0 = time.perf_counter(); e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
