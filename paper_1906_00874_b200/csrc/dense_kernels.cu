@@ -164,14 +164,16 @@ __device__ void tile_gemm(const Mat &C, const Mat &A, const Mat &B, double alpha
 #pragma unroll
         for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
       double pa[GPF], pb[GPF];
+      // coalescing: walk the operand's unit-stride dimension fastest
+      const bool a_rows_fast = A.rs == 1, b_rows_fast = B.rs == 1;
       auto fetch = [&](int k0) {
 #pragma unroll
         for (int u = 0; u < GPF; ++u) {
           const int e = tid + u * HLU_NT;
-          const int r = e % GB, q = e / GB;  // A tile: row r, k q
+          const int r = a_rows_fast ? e % GB : e / GK, q = a_rows_fast ? e / GB : e % GK;
           const int gi = i0 + r, gk = k0 + q;
           pa[u] = (gi < m && gk < k) ? A.get(gi, gk) : 0.0;
-          const int cc = e % GB, qq = e / GB;  // B tile: k qq, col cc
+          const int qq = b_rows_fast ? e % GK : e / GB, cc = b_rows_fast ? e / GK : e % GB;
           const int bj = j0 + cc, bk = k0 + qq;
           pb[u] = (bk < k && bj < n) ? B.get(bk, bj) : 0.0;
         }
@@ -182,8 +184,10 @@ __device__ void tile_gemm(const Mat &C, const Mat &A, const Mat &B, double alpha
 #pragma unroll
         for (int u = 0; u < GPF; ++u) {
           const int e = tid + u * HLU_NT;
-          sA[(e / GB) * GB + e % GB] = pa[u];
-          sB[(e / GB) * GB + e % GB] = pb[u];
+          const int r = a_rows_fast ? e % GB : e / GK, q = a_rows_fast ? e / GB : e % GK;
+          sA[q * GB + r] = pa[u];
+          const int qq = b_rows_fast ? e % GK : e / GB, cc = b_rows_fast ? e / GK : e % GB;
+          sB[qq * GB + cc] = pb[u];
         }
         __syncthreads();
         if (k0 + GK < k) fetch(k0 + GK);  // in flight during the FMAs below
