@@ -148,12 +148,13 @@ __global__ void __launch_bounds__(HLU_NT) k_trsm(hlu_ctx c, const hlu_trsm_desc 
 #define GB 64
 #define GK 32
 #define GPF (GB * GK / HLU_NT)  // tile elements each thread stages per operand (8)
+#define GLD (GB + 1)            // padded tile row: transposed stores stay conflict-free
 
 // C += alpha * A B.  64x64 output tiles, 32-deep k-steps; the next k-tile is
 // prefetched into registers while the current one is consumed from shared
 // memory, so each k-step costs max(load latency, compute) instead of the sum.
-__device__ void tile_gemm(const Mat &C, const Mat &A, const Mat &B, double alpha, double *sA,
-                          double *sB) {
+__device__ __noinline__ void tile_gemm(const Mat &C, const Mat &A, const Mat &B, double alpha, double *sA,
+                                       double *sB) {
   const int m = C.rows, n = C.cols, k = A.cols;
   const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
   for (int i0 = 0; i0 < m; i0 += GB) {
@@ -185,9 +186,9 @@ __device__ void tile_gemm(const Mat &C, const Mat &A, const Mat &B, double alpha
         for (int u = 0; u < GPF; ++u) {
           const int e = tid + u * HLU_NT;
           const int r = a_rows_fast ? e % GB : e / GK, q = a_rows_fast ? e / GB : e % GK;
-          sA[q * GB + r] = pa[u];
+          sA[q * GLD + r] = pa[u];
           const int qq = b_rows_fast ? e % GK : e / GB, cc = b_rows_fast ? e / GK : e % GB;
-          sB[qq * GB + cc] = pb[u];
+          sB[qq * GLD + cc] = pb[u];
         }
         __syncthreads();
         if (k0 + GK < k) fetch(k0 + GK);  // in flight during the FMAs below
@@ -195,9 +196,9 @@ __device__ void tile_gemm(const Mat &C, const Mat &A, const Mat &B, double alpha
         for (int q = 0; q < kk; ++q) {
           double av[4], bv[4];
 #pragma unroll
-          for (int a = 0; a < 4; ++a) av[a] = sA[q * GB + ty + 16 * a];
+          for (int a = 0; a < 4; ++a) av[a] = sA[q * GLD + ty + 16 * a];
 #pragma unroll
-          for (int b = 0; b < 4; ++b) bv[b] = sB[q * GB + tx + 16 * b];
+          for (int b = 0; b < 4; ++b) bv[b] = sB[q * GLD + tx + 16 * b];
 #pragma unroll
           for (int a = 0; a < 4; ++a)
 #pragma unroll
@@ -232,12 +233,12 @@ __device__ void zero_mat(const Mat &C) {
   __syncthreads();
 }
 
-__global__ void __launch_bounds__(HLU_NT)
+__global__ void __launch_bounds__(HLU_NT, 2)
     k_gemm(hlu_ctx c, const hlu_gemm_desc *__restrict__ d, const hlu_term *__restrict__ terms) {
   extern __shared__ double gsm[];
   double *sA = gsm;
-  double *sB = sA + GB * GK;
-  double *sW = sB + GB * GK;
+  double *sB = sA + GLD * GK;
+  double *sW = sB + GLD * GK;
   const hlu_gemm_desc o = d[blockIdx.x];
   if (o.log >= 0 && threadIdx.x == 0) c.log[o.log] = c.ranks[o.log_slot];
   for (int t = 0; t < o.term_count; ++t) {
@@ -408,7 +409,7 @@ extern "C" int hlu_trsm_batched_f64(const hlu_ctx *ctx, const hlu_trsm_desc *d, 
 
 extern "C" int hlu_gemm_batched_f64(const hlu_ctx *ctx, const hlu_gemm_desc *d, const hlu_term *terms,
                                     int count, void *stream) {
-  const size_t smem = (size_t)(2 * GB * GK + GB * GB) * sizeof(double);
+  const size_t smem = (size_t)(2 * GLD * GK + GB * GB) * sizeof(double);
   static bool init = false;
   if (!init) {
     cudaFuncSetAttribute(k_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

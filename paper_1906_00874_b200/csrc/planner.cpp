@@ -332,9 +332,32 @@ struct Planner {
     return out_node < 0;
   }
 
+  // hoisted inner product W = fa_b[mid]^T fb_a[mid] shared by all leaves of a
+  // partitioned destination (see planner.py: hoist_inner)
+  struct Hoist {
+    bool on = false;
+    View W;
+    int64_t t = -1;
+  };
+
+  Hoist hoist_inner(const Opnd &a, const Opnd &b) {
+    View fa_a, fb_a, fa_b, fb_b;
+    factor_views(a, &fa_a, &fb_a);
+    factor_views(b, &fa_b, &fb_b);
+    int64_t base;
+    const int64_t t = temp((int64_t)cap * cap, &base);
+    Hoist h;
+    h.on = true;
+    h.t = t;
+    h.W = View{base, cap, cap, 1, cap, fa_b.cdyn, fa_a.cdyn};
+    std::vector<Term> ts{Term{0, h.W, NULLV, NULLV, NULLV, 0.0, 0}, Term{1, h.W, fa_b.T(), NULLV, fb_a, 1.0, 0}};
+    gemm_op(ts, {res(a), res(b)}, {temp_res(t)}, F_STATIC, 0.0, -1, false, {t}, {});
+    return h;
+  }
+
   // ---------------------------------------------------------- products
   Pair product(const Opnd &a, const Opnd &b, const std::vector<Iv> *ctx, std::vector<Iv> *reads_out,
-               std::vector<int64_t> *tps) {
+               std::vector<int64_t> *tps, const Hoist *hw = nullptr) {
     std::vector<Iv> reads = ctx ? *ctx : std::vector<Iv>{res(a), res(b)};
     *reads_out = reads;
     tps->clear();
@@ -346,8 +369,16 @@ struct Planner {
       const int64_t t = temp((int64_t)n * cap, &base);
       const View T{base, n, cap, 1, n, -1, fa.cdyn};
       std::vector<Term> ts{Term{0, T, NULLV, NULLV, NULLV, 0.0, 0}};
-      terms_tmatmat(ts, T, b, fb, 1.0);
-      gemm_op(ts, reads, {temp_res(t)}, F_STATIC, 0.0, -1, true, {t}, {});
+      std::vector<int64_t> tin;
+      if (hw && hw->on) {
+        View fab, fbb;
+        factor_views(b, &fab, &fbb);
+        ts.push_back(Term{1, T, fbb, NULLV, hw->W, 1.0, 0});
+        tin.push_back(hw->t);
+      } else {
+        terms_tmatmat(ts, T, b, fb, 1.0);
+      }
+      gemm_op(ts, reads, {temp_res(t)}, F_STATIC, 0.0, -1, true, {t}, tin);
       tps->push_back(t);
       return Pair{fa, T, 1.0, 0, 0};
     }
@@ -446,11 +477,11 @@ struct Planner {
   }
 
   // ---------------------------------------------------------- update
-  void update(const Opnd &c, const Opnd &a, const Opnd &b) {
+  void update(const Opnd &c, const Opnd &a, const Opnd &b, const Hoist *hw = nullptr) {
     if (!c.win && nd(c.node).kind == 1) {
       std::vector<Iv> reads;
       std::vector<int64_t> tps;
-      const Pair p = product(a, b, nullptr, &reads, &tps);
+      const Pair p = product(a, b, nullptr, &reads, &tps, hw);
       const auto &x = nd(c.node);
       const int m = x.r1 - x.r0, n = x.c1 - x.c0;
       View ca, cb;
@@ -463,8 +494,13 @@ struct Planner {
     }
     const bool cp = part(c), ap = part(a), bp = part(b);
     if (!(cp || ap || bp)) {
-      update_dense(c, a, b);
+      update_dense(c, a, b, hw);
       return;
+    }
+    Hoist local;
+    if (!hw && cp && !ap && !bp && rk(a) && rk(b)) {
+      local = hoist_inner(a, b);
+      hw = &local;
     }
     std::vector<std::pair<int, int>> rows, cols, mids;
     if (cp) rows = row_cuts(c.node);
@@ -487,12 +523,12 @@ struct Planner {
                              : window(a, rows[i].first, rows[i].second, mids[p].first, mids[p].second);
           const Opnd bb = bp ? whole(child(b.node, (int)p, (int)j))
                              : window(b, mids[p].first, mids[p].second, cols[j].first, cols[j].second);
-          update(cij, aa, bb);
+          update(cij, aa, bb, hw);
         }
       }
   }
 
-  void update_dense(const Opnd &c, const Opnd &a, const Opnd &b) {
+  void update_dense(const Opnd &c, const Opnd &a, const Opnd &b, const Hoist *hw = nullptr) {
     const View dst = dense_view(c);
     const int m = dst.rows, n = dst.cols;
     const std::vector<Iv> reads{res(a), res(b)};
@@ -508,9 +544,17 @@ struct Planner {
       const int64_t t = temp((int64_t)n * cap, &base);
       const View T{base, n, cap, 1, n, -1, fa.cdyn};
       std::vector<Term> ts{Term{0, T, NULLV, NULLV, NULLV, 0.0, 0}};
-      terms_tmatmat(ts, T, b, fb, 1.0);
+      std::vector<int64_t> tin;
+      if (hw && hw->on) {
+        View fab, fbb;
+        factor_views(b, &fab, &fbb);
+        ts.push_back(Term{1, T, fbb, NULLV, hw->W, 1.0, 0});
+        tin.push_back(hw->t);
+      } else {
+        terms_tmatmat(ts, T, b, fb, 1.0);
+      }
       ts.push_back(Term{1, dst, fa, NULLV, T.T(), -1.0, 0});
-      gemm_op(ts, reads, writes, F_LIN, 2.0 * (m + n) * n, fa.cdyn, false, {t}, {}, false);
+      gemm_op(ts, reads, writes, F_LIN, 2.0 * (m + n) * n, fa.cdyn, false, {t}, tin, false);
     } else {
       View fa, fb;
       factor_views(b, &fa, &fb);

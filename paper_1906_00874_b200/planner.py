@@ -313,7 +313,23 @@ class Planner:
         return res
 
     # ------------------------------------------------------------ products
-    def product(self, a, b, ctx_reads=None):
+    def hoist_inner(self, a, b):
+        """W = fa_b[mid]^T fb_a[mid] (k_b x k_a) for a leaf-operand update
+        c -= a @ b with both a and b low-rank: every leaf of a partitioned c
+        needs this same inner product (``_op_t_matmat`` of the b window
+        against a's right factor, hlu.py:178-193); computed once here with the
+        same kernel and shapes, so the values are identical."""
+        cap = self.L.cap
+        fa_a, fb_a = self.factor_views(a)
+        fa_b, fb_b = self.factor_views(b)
+        t, base = self._temp(cap * cap)
+        W = View(base, cap, cap, 1, cap, fa_b.cdyn, fa_a.cdyn)
+        terms = [(TERM_ZERO, W, NULL_VIEW, NULL_VIEW, NULL_VIEW, 0.0, 0),
+                 (TERM_GEMM, W, fa_b.T, NULL_VIEW, fb_a, 1.0, 0)]
+        self.gemm_op(terms, [self.L.res(a), self.L.res(b)], [self._temp_res(t)], temps_out=[t])
+        return (W, t)
+
+    def product(self, a, b, ctx_reads=None, hw=None):
         """Low-rank product a @ b (``_multiply_lowrank``, hlu.py:261-291).
         Returns (Pair, read intervals, temps the pair lives in).  Operands are
         read-only for the whole product, so every op inside a compound product
@@ -326,8 +342,14 @@ class Planner:
             t, base = self._temp(n * cap)
             T = View(base, n, cap, 1, n, -1, fa.cdyn)
             terms = [(TERM_ZERO, T, NULL_VIEW, NULL_VIEW, NULL_VIEW, 0.0, 0)]
-            self.terms_tmatmat(terms, T, b, fb, 1.0)
-            self.gemm_op(terms, reads, [self._temp_res(t)], defer=True, temps_out=[t])
+            tin = []
+            if hw is not None:  # T = fb_b[cols] W  (W hoisted by the caller)
+                _, fbb = self.factor_views(b)
+                terms.append((TERM_GEMM, T, fbb, NULL_VIEW, hw[0], 1.0, 0))
+                tin = [hw[1]]
+            else:
+                self.terms_tmatmat(terms, T, b, fb, 1.0)
+            self.gemm_op(terms, reads, [self._temp_res(t)], defer=True, temps_out=[t], temps_in=tin)
             return Pair(fa, T), reads, [t]
         if not _part(b) and _rk(b):
             fa, fb = self.factor_views(b)
@@ -399,10 +421,10 @@ class Planner:
         return (pair.a.off >> TEMP_SHIFT) - 1
 
     # ------------------------------------------------------------- update
-    def update(self, c, a, b):
+    def update(self, c, a, b, hw=None):
         """c := c - a @ b (hlu.py:568-623)."""
         if isinstance(c, HMatrix) and c.kind == LOWRANK:
-            p, reads, tps = self.product(a, b)
+            p, reads, tps = self.product(a, b, hw=hw)
             m, n = c.rows, c.cols
             ca, cb = self.factor_views(c)
             self.rkt(RK_ADD, [Pair(ca, cb), Pair(p.a, p.b, -p.sign)], m, n, out=c,
@@ -410,8 +432,10 @@ class Planner:
             return
         cp, ap, bp = _part(c), _part(a), _part(b)
         if not (cp or ap or bp):
-            self._update_dense(c, a, b)
+            self._update_dense(c, a, b, hw)
             return
+        if hw is None and cp and not ap and not bp and _rk(a) and _rk(b):
+            hw = self.hoist_inner(a, b)
         rows = _row_cuts(c) if cp else (_row_cuts(a) if ap else [_rr(c)])
         cols = _col_cuts(c) if cp else (_col_cuts(b) if bp else [_cc(c)])
         if ap and bp and _col_cuts(a) != _row_cuts(b):
@@ -422,9 +446,9 @@ class Planner:
                 cij = c.child(i, j) if cp else _window(c, rr, cc)
                 for p, mm in enumerate(mids):
                     self.update(cij, a.child(i, p) if ap else _window(a, rr, mm),
-                                b.child(p, j) if bp else _window(b, mm, cc))
+                                b.child(p, j) if bp else _window(b, mm, cc), hw)
 
-    def _update_dense(self, c, a, b):
+    def _update_dense(self, c, a, b, hw=None):
         dst = self.dense_view(c)
         m, n = dst.rows, dst.cols
         reads = [self.L.res(a), self.L.res(b)]
@@ -439,10 +463,16 @@ class Planner:
             t, base = self._temp(n * cap)
             T = View(base, n, cap, 1, n, -1, fa.cdyn)
             terms = [(TERM_ZERO, T, NULL_VIEW, NULL_VIEW, NULL_VIEW, 0.0, 0)]
-            self.terms_tmatmat(terms, T, b, fb, 1.0)
+            tin = []
+            if hw is not None:  # T = fb_b[cols] W  (W hoisted by the caller)
+                _, fbb = self.factor_views(b)
+                terms.append((TERM_GEMM, T, fbb, NULL_VIEW, hw[0], 1.0, 0))
+                tin = [hw[1]]
+            else:
+                self.terms_tmatmat(terms, T, b, fb, 1.0)
             terms.append((TERM_GEMM, dst, fa, NULL_VIEW, T.T, -1.0, 0))
             self.gemm_op(terms, reads, writes, (F_LIN, 2.0 * (m + n) * n, -1), log_slot=fa.cdyn,
-                         temps_out=[t])
+                         temps_out=[t], temps_in=tin)
         else:
             fa, fb = self.factor_views(b)
             t, base = self._temp(m * cap)
