@@ -127,6 +127,8 @@ def time_rkt_launches(call, torch):
     st = ctypes.c_void_p(call.stream.cuda_stream)
     ctx = ctypes.byref(call.ctx)
     call.restore()
+    lib.hlu_epoch_bump.argtypes = [ctypes.c_void_p]
+    lib.hlu_epoch_bump(st)
     durations = []
     with torch.cuda.stream(call.stream):
         pend = []

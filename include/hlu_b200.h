@@ -111,8 +111,8 @@ typedef struct {
   int32_t out_slot, log;
   int64_t out_a, out_b;  /* column-major outputs, ld = m / n, capacity cap columns */
   int64_t ws;            /* workspace offset in the pool (TSQR reflectors) */
-  int32_t handoff;       /* scratch: set by the KM=32 kernel when the op's runtime stacked rank
-                            exceeds 32, consumed (and reset to 0) by the KM=64 kernel */
+  int32_t handoff;       /* scratch: replay epoch stamped by the KM=32 kernel when it claims
+                            the op (runtime stacked rank <= 32); initialise to 0 */
   int32_t pad;
 } hlu_rkt_desc; /* 64 bytes */
 
@@ -157,6 +157,7 @@ int hlu_schedule_destroy(hlu_schedule *s);
 /* library identity / sanity */
 const char *hlu_version(void);
 int hlu_device_check(void); /* 0 when a sm_100 device is present */
+int hlu_epoch_bump(void *stream);  /* new replay epoch for the truncation-variant claim protocol */
 int64_t hlu_debug_sweeps(int reset); /* total Jacobi sweeps run so far (diagnostics) */
 int hlu_debug_phases(double *sum_out, double *max_out, int reset); /* RKT phase cycles (diagnostics) */
 

@@ -25,6 +25,7 @@ SYMBOLS = (
     "hlu_schedule_destroy",
     "hlu_version",
     "hlu_device_check",
+    "hlu_epoch_bump",
     "hlu_debug_sweeps",
     "hlu_debug_phases",
 )

@@ -262,6 +262,7 @@ __device__ void apply_q(int m, int K, int kk, const double *W, double *T, double
 }
 
 __device__ unsigned long long g_sweeps = 0;  // total Jacobi sweeps (diagnostics)
+__device__ unsigned g_epoch = 1;            // bumped once per schedule replay
 __device__ unsigned long long g_phase[10];   // summed cycles per phase (diagnostics)
 __device__ unsigned long long g_phase_max[10];
 #define PHASE(k)                                                   \
@@ -497,18 +498,28 @@ __global__ void __launch_bounds__(HLU_NT)
   double *outA = c.pool + o.out_a;
   double *outB = c.pool + o.out_b;
 
-  // Variant hand-off.  Both variants are launched over the same level; the
-  // KM=32 one decides from the INPUT ranks (the KM=64 launch would see ranks
-  // the KM=32 launch already updated) and flags the ops it leaves behind.
+  // Variant ownership.  Both variants run over the same level, possibly
+  // concurrently.  The KM=32 kernel claims the ops it takes (K <= 32) by
+  // stamping the replay epoch into the descriptor BEFORE it changes any rank;
+  // the KM=64 kernel takes an op only if its K > 32 and the op is unclaimed.
+  // If the KM=64 kernel observed a rank already updated by the KM=32 kernel it
+  // also observes the claim (fence on both sides), so no op runs twice.
+  const unsigned epoch = *(volatile unsigned *)&g_epoch;
+  __shared__ int s_take;
   if (KM == 32) {
-    if (K > 32) {
-      if (tid == 0) d[blockIdx.x].handoff = 64;
-      return;
+    if (K > 32) return;
+    if (tid == 0) {
+      *(volatile int *)&d[blockIdx.x].handoff = (int)epoch;
+      __threadfence();
     }
   } else {
-    if (o.handoff != 64) return;
+    if (tid == 0) {
+      __threadfence();
+      const int claimed = *(volatile int *)&d[blockIdx.x].handoff == (int)epoch;
+      s_take = (K > 32) && !claimed;
+    }
     __syncthreads();
-    if (tid == 0) d[blockIdx.x].handoff = 0;
+    if (!s_take) return;
   }
   if (o.mode == HLU_RK_ADD) {
     const int k1 = P[0].k, k2 = P[1].k;
@@ -665,6 +676,13 @@ static size_t rkt_smem() {
 }  // namespace hlu
 
 using namespace hlu;
+
+__global__ void k_epoch_bump() { g_epoch += 1; }
+
+extern "C" int hlu_epoch_bump(void *stream) {
+  k_epoch_bump<<<1, 1, 0, (cudaStream_t)stream>>>();
+  return cudaGetLastError() == cudaSuccess ? 0 : -1;
+}
 
 extern "C" int hlu_debug_phases(double *sum_out, double *max_out, int reset) {
   unsigned long long a[10], b[10];

@@ -10,8 +10,12 @@
 
 #include "common.cuh"
 
+extern "C" int hlu_epoch_bump(void *stream);
+
 struct hlu_schedule {
   hlu_ctx ctx;
+  cudaStream_t side;
+  cudaEvent_t ev_fork, ev_join;
   std::vector<hlu_launch> launches;
   const hlu_getrf_desc *getrf;
   const hlu_trsm_desc *trsm;
@@ -25,8 +29,24 @@ struct hlu_schedule {
 };
 
 static int run_launches(hlu_schedule *s, cudaStream_t st) {
-  for (const hlu_launch &L : s->launches) {
+  int rc0 = hlu_epoch_bump(st);
+  if (rc0 != 0) return rc0;
+  const size_t nl = s->launches.size();
+  for (size_t i = 0; i < nl; ++i) {
+    const hlu_launch &L = s->launches[i];
     int rc = 0;
+    // the KM=64 companion of a truncation launch runs as a concurrent branch
+    if (L.kind == HLU_K_RKT32 && i + 1 < nl && s->launches[i + 1].kind == HLU_K_RKT64) {
+      cudaEventRecord(s->ev_fork, st);
+      cudaStreamWaitEvent(s->side, s->ev_fork, 0);
+      rc = hlu_rk_update_batched_f64(&s->ctx, s->rkt + L.first, s->parts, L.count, 64, s->side);
+      if (rc == 0) rc = hlu_rk_update_batched_f64(&s->ctx, s->rkt + L.first, s->parts, L.count, 32, st);
+      cudaEventRecord(s->ev_join, s->side);
+      cudaStreamWaitEvent(st, s->ev_join, 0);
+      ++i;
+      if (rc != 0) return rc;
+      continue;
+    }
     switch (L.kind) {
       case HLU_K_GETRF:
         rc = hlu_getrf_batched_f64(&s->ctx, s->getrf + L.first, L.count, L.smem_dim, st);
@@ -71,6 +91,9 @@ extern "C" int hlu_schedule_create(hlu_schedule **out, const hlu_ctx *ctx, const
   s->exec = nullptr;
   s->use_graph = use_graph != 0;
   cudaStream_t st = (cudaStream_t)stream;
+  cudaStreamCreateWithFlags(&s->side, cudaStreamNonBlocking);
+  cudaEventCreateWithFlags(&s->ev_fork, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&s->ev_join, cudaEventDisableTiming);
   if (s->use_graph) {
     // make sure kernel attributes are set outside capture
     hlu_getrf_batched_f64(&s->ctx, s->getrf, 0, 0, st);
@@ -111,6 +134,9 @@ extern "C" int hlu_schedule_destroy(hlu_schedule *s) {
   if (!s) return 0;
   if (s->exec) cudaGraphExecDestroy(s->exec);
   if (s->graph) cudaGraphDestroy(s->graph);
+  cudaEventDestroy(s->ev_fork);
+  cudaEventDestroy(s->ev_join);
+  cudaStreamDestroy(s->side);
   delete s;
   return 0;
 }

@@ -68,6 +68,8 @@ def rel(g, c):
     return np.linalg.norm(g - c) / den if den > 0 else np.linalg.norm(g)
 
 
+lib.hlu_epoch_bump.argtypes = [ctypes.c_void_p]
+lib.hlu_epoch_bump(st)
 li = 0
 nl = len(p.launches)
 while li < nl:

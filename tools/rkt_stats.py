@@ -28,6 +28,8 @@ def main():
     lib.hlu_debug_phases(ph_s.ctypes.data, ph_m.ctypes.data, 1)
     tot = {}
     evs = []
+    lib.hlu_epoch_bump.argtypes = [ctypes.c_void_p]
+    lib.hlu_epoch_bump(st)
     with torch.cuda.stream(call.stream):
         for L_ in p.launches:
             kind, count, first, dim = int(L_["kind"]), int(L_["count"]), int(L_["first"]), int(L_["smem_dim"])
@@ -52,6 +54,20 @@ def main():
         print(f"phase {nm:9s} total Mcyc {ph_s[i]/1e6:10.1f}  avg/op kcyc {ph_s[i]/nrkt/1e3:8.2f}  max kcyc {ph_m[i]/1e3:9.1f}")
     for k, (nl, nops, t, mx) in tot.items():
         print(f"{k:6s} launches {nl:6d} ops {nops:8d} total {t:9.2f} ms  per-launch {t/nl:7.3f} ms  max {mx:7.3f}")
+    # RKT launch time vs the largest factor height in the launch
+    import collections as _c
+    byb = _c.defaultdict(lambda: [0, 0.0])
+    for li, (kind, count, a, b) in enumerate(evs):
+        if kind not in (ir.K_RKT32, ir.K_RKT64):
+            continue
+        L_ = p.launches[li]
+        d_ = p.rkt[int(L_["first"]): int(L_["first"]) + int(L_["count"])]
+        mm = int(max(d_["m"].max(), d_["n"].max()))
+        bucket = 1 << max(0, (mm - 1).bit_length())
+        byb[(kind, bucket)][0] += 1
+        byb[(kind, bucket)][1] += a.elapsed_time(b)
+    for (kind, bucket), (cnt, t) in sorted(byb.items()):
+        print(f"rkt kind {kind} max(m,n) <= {bucket:6d}: launches {cnt:6d} total {t:9.1f} ms")
     # the slowest GEMM launch: what is in it
     worst = max(((a.elapsed_time(b), i) for i, (kind, count, a, b) in enumerate(evs) if kind == ir.K_GEMM), default=None)
     if worst:
