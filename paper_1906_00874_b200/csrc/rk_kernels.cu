@@ -499,28 +499,27 @@ __global__ void __launch_bounds__(HLU_NT)
   double *outB = c.pool + o.out_b;
 
   // Variant ownership.  Both variants run over the same level, possibly
-  // concurrently.  The KM=32 kernel claims the ops it takes (K <= 32) by
-  // stamping the replay epoch into the descriptor BEFORE it changes any rank;
-  // the KM=64 kernel takes an op only if its K > 32 and the op is unclaimed.
-  // If the KM=64 kernel observed a rank already updated by the KM=32 kernel it
-  // also observes the claim (fence on both sides), so no op runs twice.
-  const unsigned epoch = *(volatile unsigned *)&g_epoch;
+  // concurrently.  An op is taken by the variant whose range contains its
+  // stacked rank K, and only after that variant wins an atomicCAS that stamps
+  // the replay epoch into the descriptor; ranks change only after a claim.
+  // The first claim therefore always sees the level-start ranks (so the right
+  // variant wins), and a variant that reads ranks already updated by the other
+  // one loses the CAS (fences on both sides), so no op runs twice.
+  const int epoch = (int)*(volatile unsigned *)&g_epoch;
   __shared__ int s_take;
-  if (KM == 32) {
-    if (K > 32) return;
-    if (tid == 0) {
-      *(volatile int *)&d[blockIdx.x].handoff = (int)epoch;
+  if (tid == 0) {
+    const bool mine = (KM == 32) ? (K <= 32) : (K > 32);
+    int take = 0;
+    if (mine) {
+      __threadfence();
+      const int h = *(volatile int *)&d[blockIdx.x].handoff;
+      take = h != epoch && atomicCAS(&d[blockIdx.x].handoff, h, epoch) == h;
       __threadfence();
     }
-  } else {
-    if (tid == 0) {
-      __threadfence();
-      const int claimed = *(volatile int *)&d[blockIdx.x].handoff == (int)epoch;
-      s_take = (K > 32) && !claimed;
-    }
-    __syncthreads();
-    if (!s_take) return;
+    s_take = take;
   }
+  __syncthreads();
+  if (!s_take) return;
   if (o.mode == HLU_RK_ADD) {
     const int k1 = P[0].k, k2 = P[1].k;
     if (tid == 0 && o.log >= 0) {
