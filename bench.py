@@ -39,7 +39,7 @@ CONFIGS = {
     "cfg2": (3, 32768, 2.0, 64, 1e-6, 32, 1e-6, 32),
     "cfg3": (3, 131072, 2.0, 64, 1e-4, None, 1e-4, None),
 }
-DEFAULT_CONFIG = os.environ.get("HLU_BENCH_CONFIG", "cfg2")
+DEFAULT_CONFIG = os.environ.get("HLU_BENCH_CONFIG", "cfg3")  # BASELINE metric config (n=131072)
 
 
 def _peaks():
@@ -388,7 +388,7 @@ def run_reference(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default=DEFAULT_CONFIG, choices=sorted(CONFIGS))

@@ -1,0 +1,174 @@
+"""Owner-computes decomposition of the H-LU op DAG over several GPUs
+(SURVEY.md §8e).
+
+* Every leaf (skeleton slot) gets an owner rank from a 2-D block-cyclic grid
+  over the index space (block size ~ n / (4 * grid side), i.e. about four
+  block rows/columns per rank, the balance point the survey measured).
+* Every op runs on the owner of the slot it writes; a temp producer (product
+  GEMM, accumulated/merged Rk temp, hoisted inner product) runs on every rank
+  that consumes the temp (replicated when consumers live on several ranks),
+  so temps never cross ranks.  The per-destination op order — and therefore
+  every rank decision — is the single-GPU one.
+* After each level, every rank ships the slots it wrote in that level
+  (payload region + rank) to the ranks that will read them: the exchange
+  list is static, computed here from the plan.
+
+``run_level_exchange`` drives any per-rank executor with a
+``torch.distributed`` process group (gloo on CPU in the tests; NCCL on GPUs).
+"""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+
+from .hmatrix import DENSE
+
+
+def grid_shape(nranks):
+    pr = int(math.isqrt(nranks))
+    while nranks % pr:
+        pr -= 1
+    return pr, nranks // pr
+
+
+def owner_map(layout, nranks, n=None, blocks_per_rank=4):
+    """Owner rank of every skeleton slot (leaves, then extra objects -> rank 0)."""
+    pr, pc = grid_shape(nranks)
+    if n is None:
+        n = max(lf.row_range[1] for lf in layout.leaves)
+    bs_r = max(1, n // (blocks_per_rank * pr))
+    bs_c = max(1, n // (blocks_per_rank * pc))
+    own = np.zeros(layout.nslots, dtype=np.int64)
+    for s, lf in enumerate(layout.leaves):
+        r = (lf.row_range[0] // bs_r) % pr
+        c = (lf.col_range[0] // bs_c) % pc
+        own[s] = r * pc + c
+    return own
+
+
+def op_owners(planner, slot_owner):
+    """Ranks executing every op (a frozenset per op): the owner of the slot it
+    writes, or the union of its temps' consumers for temp-only producers."""
+    ops = planner.ops
+    nslots = planner.L.nslots
+    owners = [None] * len(ops)
+    consumers = {}
+    for i in range(len(ops) - 1, -1, -1):
+        op = ops[i]
+        slot_writes = [lo for lo, hi in op.writes if lo < nslots]
+        if slot_writes:
+            owners[i] = frozenset([int(slot_owner[slot_writes[0]])])
+        else:
+            ranks = set()
+            for t in op.temps_out:
+                ranks |= consumers.get(t, set())
+            owners[i] = frozenset(ranks or {0})
+        for t in op.temps_in:
+            consumers.setdefault(t, set()).update(owners[i])
+    return owners
+
+
+def slot_region(layout, s):
+    """(offset, length) of slot s's payload in the pool (Rk: both factor slabs)."""
+    lf = layout.leaves[s]
+    if lf.kind == DENSE:
+        return layout.dense_off[id(lf)], lf.rows * lf.cols
+    a_off, _, _ = layout.rk[id(lf)]
+    return a_off, (lf.rows + lf.cols) * layout.cap
+
+
+def exchange_plan(planner, packed, owner):
+    """Per level: {rank: sorted slots written by that rank which another rank
+    reads later}.  Returns (plan, bytes per level)."""
+    ops = planner.ops
+    nslots = planner.L.nslots
+    levels = packed.op_levels
+    readers = {}
+    for i, op in enumerate(ops):
+        for lo, hi in op.reads:
+            for s in range(lo, min(hi, nslots)):
+                readers.setdefault(s, set()).update(owner[i])
+    plan = {}
+    vol = {}
+    for i, op in enumerate(ops):
+        lv = int(levels[i])
+        for lo, hi in op.writes:
+            for s in range(lo, min(hi, nslots)):
+                (w,) = owner[i]
+                if readers.get(s, set()) - {w}:
+                    plan.setdefault(lv, {}).setdefault(w, set()).add(s)
+    for lv, per in plan.items():
+        vol[lv] = sum(slot_region(planner.L, s)[1] * 8 for ss in per.values() for s in ss)
+    return plan, vol
+
+
+def run_level_exchange(packed, planner, owner, plan, rank, execute_desc, pool, ranks_arr, dist,
+                       slot_owner=None, gather_to=0):
+    """Level-synchronous owner-computes execution.  ``execute_desc(kind, idx)``
+    runs one descriptor on this rank's device/CPU machine; after every level
+    the slots in ``plan`` are broadcast from their writer (payload + rank)."""
+    L = planner.L
+    kind_name = {0: "getrf", 1: "trsm", 2: "gemm", 3: "rkt", 4: "rkt", 5: "gemm"}
+    levels = packed.op_levels
+    nl = len(packed.launches)
+
+    def level_of(launch):
+        k = kind_name[int(launch["kind"])]
+        return int(levels[packed.desc_op[k][int(launch["first"])]])
+
+    li = 0
+    while li < nl:
+        lv = level_of(packed.launches[li])
+        while li < nl and level_of(packed.launches[li]) == lv:
+            Lr = packed.launches[li]
+            kind = int(Lr["kind"])
+            if kind != 4:  # the KM=64 companion shares the KM=32 descriptors
+                k = kind_name[kind]
+                for d in range(int(Lr["first"]), int(Lr["first"]) + int(Lr["count"])):
+                    if rank in owner[packed.desc_op[k][d]]:
+                        execute_desc(kind, d)
+            li += 1
+        for src, slots in sorted(plan.get(lv, {}).items()):
+            for s in sorted(slots):
+                off, ln = slot_region(L, s)
+                lf = L.leaves[s]
+                buf = np.zeros(ln + 1)
+                if rank == src:
+                    buf[:ln] = pool[off:off + ln]
+                    if lf.kind != DENSE:
+                        buf[ln] = ranks_arr[L.rk[id(lf)][2]]
+                import torch
+
+                _ship(dist, rank, src, None, off, ln, lf, L, pool, ranks_arr, buf)
+    if slot_owner is not None:  # final gather of every owned slot to one rank
+        for s in range(len(L.leaves)):
+            src = int(slot_owner[s])
+            if src == gather_to:
+                continue
+            off, ln = slot_region(L, s)
+            _ship(dist, rank, src, gather_to, off, ln, L.leaves[s], L, pool, ranks_arr, np.zeros(ln + 1))
+
+
+def _ship(dist, rank, src, dst, off, ln, lf, L, pool, ranks_arr, buf):
+    """Broadcast (dst None) or point-to-point copy of one slot's payload + rank."""
+    import torch
+
+    if rank == src:
+        buf[:ln] = pool[off:off + ln]
+        if lf.kind != DENSE:
+            buf[ln] = ranks_arr[L.rk[id(lf)][2]]
+    t = torch.from_numpy(buf)
+    if dst is None:
+        dist.broadcast(t, src)
+    elif rank == src:
+        dist.send(t, dst)
+    elif rank == dst:
+        dist.recv(t, src)
+    else:
+        return
+    if rank != src:
+        pool[off:off + ln] = t.numpy()[:ln]
+        if lf.kind != DENSE:
+            ranks_arr[L.rk[id(lf)][2]] = int(t.numpy()[ln])

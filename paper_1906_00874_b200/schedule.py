@@ -140,6 +140,7 @@ class Packed:
     lu_op_ids: np.ndarray
     lu_labels: list
     op_levels: np.ndarray
+    desc_op: dict = None  # kind name -> op index of every descriptor (Python planner only)
 
 
 def _view_rec(v):
@@ -165,11 +166,13 @@ def pack(pl: Planner, arena_base: int):
     kinds = np.array([_KIND_ORDER[o.kind] for o in ops], dtype=np.int64)
     order = np.lexsort((np.arange(len(ops)), kinds, levels))
     getrf, trsm, gemm, terms, rkt, parts = [], [], [], [], [], []
+    desc_op = {"getrf": [], "trsm": [], "gemm": [], "rkt": []}
     launches = []
     cur = None
     for i in order:
         op = ops[i]
         lv = int(levels[i])
+        desc_op[op.kind].append(int(i))
         if op.kind == "getrf":
             v, op_id, lu_idx = op.payload
             getrf.append((fv(v), op_id, lu_idx))
@@ -225,7 +228,7 @@ def pack(pl: Planner, arena_base: int):
         arena_doubles=arena, flop_formula=flop_formula, flop_coef=flop_coef, flop_log=flop_log,
         nlog=max(pl.nlog, 1), nranks=max(pl.nslots_rank, 1),
         lu_op_ids=np.array(pl.lu_ops, dtype=np.int64), lu_labels=list(pl.lu_labels),
-        op_levels=levels,
+        op_levels=levels, desc_op={k: np.array(v, dtype=np.int64) for k, v in desc_op.items()},
     )
 
 
