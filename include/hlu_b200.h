@@ -110,13 +110,21 @@ typedef struct {
   int32_t m, n, cap;
   int32_t out_slot, log;
   int64_t out_a, out_b;  /* column-major outputs, ld = m / n, capacity cap columns */
-  int64_t ws;            /* workspace offset in the pool (TSQR reflectors) */
-  int32_t handoff;       /* scratch: replay epoch stamped by the KM=32 kernel when it claims
-                            the op (runtime stacked rank <= 32); initialise to 0 */
+  int64_t ws;            /* workspace offset in the pool: hlu_rkt_ws_doubles(m, n, kbound) doubles */
+  int32_t reserved;      /* 0 */
   int32_t pad;
 } hlu_rkt_desc; /* 64 bytes */
 
-/* launch kinds of a schedule entry */
+/* one row block (<= 512 rows) of one factor of a truncation: the unit of the
+ * parallel TSQR (phase A) and Q application (phase C) */
+typedef struct {
+  int32_t op;      /* index into the descriptor array */
+  int16_t side;    /* 0: left factor (m rows), 1: right factor (n rows) */
+  int16_t block;   /* row block */
+} hlu_rkt_item; /* 8 bytes */
+
+/* launch kinds of a schedule entry (HLU_K_RKT32: the truncations of a level, any stacked
+ * rank; HLU_K_RKT64 is no longer emitted and is ignored) */
 enum { HLU_K_GETRF = 0, HLU_K_TRSM = 1, HLU_K_GEMM = 2, HLU_K_RKT32 = 3, HLU_K_RKT64 = 4, HLU_K_GEMM_SMALL = 5 };
 
 typedef struct {
@@ -136,30 +144,64 @@ int hlu_gemm_batched_f64(const hlu_ctx *ctx, const hlu_gemm_desc *d, const hlu_t
  * assoc-1 triples with M.cols <= 64): one warp per chain */
 int hlu_gemm_small_batched_f64(const hlu_ctx *ctx, const hlu_gemm_desc *d, const hlu_term *terms, int count,
                                void *stream);
-int hlu_rk_update_batched_f64(const hlu_ctx *ctx, hlu_rkt_desc *d, const hlu_rkpart *parts,
-                              int count, int kclass, void *stream);
+/* device scratch of the truncation launches: per level 8 counters (ops of the register
+ * warp kernels K<=8 / K<=16, the shared-memory warp kernel K<=32, the CTA path, then the
+ * CTA-path ops whose core SVD one warp does, then the CTA-path row blocks) at
+ * counts + 8*slot, zeroed before the level runs; list = 7 segments
+ * of max_ops op indices; items = max_items row blocks (max over levels of hlu_rkt_items) */
+typedef struct {
+  int32_t *counts;
+  int32_t *list;
+  hlu_rkt_item *items;
+  int64_t max_ops, max_items;
+} hlu_rkt_scratch;
 
-/* TSQR workspace (doubles) one truncation needs for an m-row factor of width <= K */
-int64_t hlu_rkt_ws_doubles(int32_t m, int32_t kbound);
+/* count truncations d[0 .. count) (count <= scratch->max_ops; counter slot 0).  A
+ * classify kernel routes every op: max(m,n) <= 128 and K <= 16 -> one warp per op with
+ * the factors in registers; K <= 32 -> one warp per op in shared memory; others ->
+ * block TSQR (one CTA per 512-row block), core SVD + rank (one CTA per op), Q apply
+ * (one CTA per block). */
+int hlu_rk_update_batched_f64(const hlu_ctx *ctx, hlu_rkt_desc *d, const hlu_rkpart *parts, int count,
+                              const hlu_rkt_scratch *scratch, void *stream);
+/* ops d[first .. first+count) of one level with counter slot `slot` (zeroed by the
+ * caller); the warp kernels run on `side` between the events ev_fork/ev_join
+ * (cudaEvent_t), concurrently with the CTA phases; side == stream runs all in order */
+int hlu_rkt_phases(const hlu_ctx *ctx, hlu_rkt_desc *d, const hlu_rkpart *parts, int64_t first, int count,
+                   const hlu_rkt_scratch *scratch, int slot, void *stream, void *side, void *ev_fork, void *ev_join);
+/* one kernel only (diagnostics / per-kernel timing): 0 classify, 1 register warp K<=8,
+ * 2 register warp K<=16, 3 shared-memory warp K<=32, 4 block TSQR, 5 core by one warp
+ * (K<=16), 6 core K<=32, 7 core K>32, 8 Q apply */
+int hlu_rkt_phase(const hlu_ctx *ctx, hlu_rkt_desc *d, const hlu_rkpart *parts, int64_t first, int count,
+                  const hlu_rkt_scratch *scratch, int slot, int which, void *stream);
+/* host: the work items of count HOST descriptors in op order (items may be NULL); returns their number */
+int64_t hlu_rkt_items(const hlu_rkt_desc *d, int count, hlu_rkt_item *items);
+
+/* workspace (doubles) one truncation of an m x n block with stacked rank <= kbound needs */
+int64_t hlu_rkt_ws_doubles(int32_t m, int32_t n, int32_t kbound);
 
 /* --- level-set schedule runtime (one CUDA graph per factorization) --- */
 typedef struct hlu_schedule hlu_schedule;
 
-/* launches: host array (copied); descriptor arrays: device pointers that must
- * outlive the schedule; use_graph: capture the launch sequence into a CUDA graph */
+/* launches: host array (copied); descriptor arrays and the scratch buffers: device
+ * pointers that must outlive the schedule (scratch->counts holds 4 ints per truncation
+ * launch; the struct itself is copied); use_graph: capture the launch sequence into a
+ * CUDA graph */
 int hlu_schedule_create(hlu_schedule **out, const hlu_ctx *ctx, const hlu_launch *launches, int64_t nlaunch,
                         const hlu_getrf_desc *getrf, const hlu_trsm_desc *trsm, const hlu_gemm_desc *gemm,
                         const hlu_term *terms, hlu_rkt_desc *rkt, const hlu_rkpart *parts,
-                        int use_graph, void *stream);
+                        const hlu_rkt_scratch *scratch, int use_graph, void *stream);
 int hlu_schedule_launch(hlu_schedule *s, void *stream);
 int hlu_schedule_destroy(hlu_schedule *s);
+/* diagnostics: with HLU_STAMPS=1 at creation, the %globaltimer (ns) before the first and
+ * after every launch of the last replay (nlaunch + 1 values), then 10 per truncation launch
+ * (after each of the 9 kernels of hlu_rkt_phase, then the join); returns the count
+ * (out may be NULL), 0 without stamps */
+int64_t hlu_schedule_stamps(hlu_schedule *s, unsigned long long *out);
 
 /* library identity / sanity */
 const char *hlu_version(void);
 int hlu_device_check(void); /* 0 when a sm_100 device is present */
-int hlu_epoch_bump(void *stream);  /* new replay epoch for the truncation-variant claim protocol */
 int64_t hlu_debug_sweeps(int reset); /* total Jacobi sweeps run so far (diagnostics) */
-int hlu_debug_phases(double *sum_out, double *max_out, int reset); /* RKT phase cycles (diagnostics) */
 
 #ifdef __cplusplus
 }

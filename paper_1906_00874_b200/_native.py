@@ -19,15 +19,17 @@ SYMBOLS = (
     "hlu_gemm_batched_f64",
     "hlu_gemm_small_batched_f64",
     "hlu_rk_update_batched_f64",
+    "hlu_rkt_phases",
+    "hlu_rkt_phase",
+    "hlu_rkt_items",
     "hlu_rkt_ws_doubles",
     "hlu_schedule_create",
     "hlu_schedule_launch",
     "hlu_schedule_destroy",
+    "hlu_schedule_stamps",
     "hlu_version",
     "hlu_device_check",
-    "hlu_epoch_bump",
     "hlu_debug_sweeps",
-    "hlu_debug_phases",
 )
 
 
@@ -41,6 +43,16 @@ class HluCtx(ctypes.Structure):
         ("eps", ctypes.c_double),
         ("kmax", ctypes.c_int32),
         ("pad", ctypes.c_int32),
+    ]
+
+
+class HluRktScratch(ctypes.Structure):
+    _fields_ = [
+        ("counts", ctypes.c_void_p),
+        ("list", ctypes.c_void_p),
+        ("items", ctypes.c_void_p),
+        ("max_ops", ctypes.c_int64),
+        ("max_items", ctypes.c_int64),
     ]
 
 
@@ -63,17 +75,27 @@ def lib():
     L.hlu_trsm_batched_f64.argtypes = [ctypes.POINTER(HluCtx), vp, i32, i32, vp]
     L.hlu_gemm_batched_f64.argtypes = [ctypes.POINTER(HluCtx), vp, vp, i32, vp]
     L.hlu_gemm_small_batched_f64.argtypes = [ctypes.POINTER(HluCtx), vp, vp, i32, vp]
-    L.hlu_rk_update_batched_f64.argtypes = [ctypes.POINTER(HluCtx), vp, vp, i32, i32, vp]
-    L.hlu_rkt_ws_doubles.argtypes = [i32, i32]
+    sp = ctypes.POINTER(HluRktScratch)
+    L.hlu_rk_update_batched_f64.argtypes = [ctypes.POINTER(HluCtx), vp, vp, i32, sp, vp]
+    L.hlu_rkt_phases.argtypes = [ctypes.POINTER(HluCtx), vp, vp, i64, i32, sp, i32, vp, vp, vp, vp]
+    L.hlu_rkt_phase.argtypes = [ctypes.POINTER(HluCtx), vp, vp, i64, i32, sp, i32, i32, vp]
+    L.hlu_rkt_items.argtypes = [vp, i32, vp]
+    L.hlu_rkt_items.restype = i64
+    L.hlu_rkt_ws_doubles.argtypes = [i32, i32, i32]
     L.hlu_rkt_ws_doubles.restype = i64
+    L.hlu_debug_sweeps.argtypes = [i32]
+    L.hlu_debug_sweeps.restype = i64
     L.hlu_schedule_create.argtypes = [ctypes.POINTER(vp), ctypes.POINTER(HluCtx), vp, i64,
-                                      vp, vp, vp, vp, vp, vp, i32, vp]
+                                      vp, vp, vp, vp, vp, vp, sp, i32, vp]
     L.hlu_schedule_launch.argtypes = [vp, vp]
     L.hlu_schedule_destroy.argtypes = [vp]
+    L.hlu_schedule_stamps.argtypes = [vp, vp]
+    L.hlu_schedule_stamps.restype = i64
     L.hlu_version.restype = ctypes.c_char_p
     for name in ("hlu_getrf_batched_f64", "hlu_trsm_batched_f64", "hlu_gemm_batched_f64", "hlu_gemm_small_batched_f64",
-                 "hlu_rk_update_batched_f64", "hlu_schedule_create", "hlu_schedule_launch",
-                 "hlu_schedule_destroy", "hlu_device_check"):
+                 "hlu_rk_update_batched_f64", "hlu_rkt_phases", "hlu_rkt_phase", "hlu_schedule_create", "hlu_schedule_launch",
+                 "hlu_schedule_destroy",
+    "hlu_schedule_stamps", "hlu_device_check"):
         getattr(L, name).restype = ctypes.c_int
     _lib = L
     return L
@@ -82,3 +104,27 @@ def lib():
 def check(rc, what):
     if rc != 0:
         raise RuntimeError(f"{what} failed with status {rc}")
+
+
+def rkt_scratch(torch, device, rkt, launches):
+    """Device scratch of the truncation launches (hlu_rkt_scratch): counters per
+    launch, op lists and row-block items sized by the largest level.  Returns
+    (struct, tensors that must stay alive)."""
+    import numpy as np
+
+    from . import ir
+
+    lk = launches[launches["kind"] == ir.K_RKT32] if len(launches) else launches
+    nrkt = int(len(lk))
+    max_ops = int(lk["count"].max()) if nrkt else 1
+    max_items = 1
+    if nrkt:
+        _, start = ir.rkt_items(rkt["m"], rkt["n"])
+        f = lk["first"].astype(np.int64)
+        cnt = lk["count"].astype(np.int64)
+        max_items = max(1, int((start[f + cnt] - start[f]).max()))
+    counts = torch.zeros(8 * max(nrkt, 1), dtype=torch.int32, device=device)
+    lst = torch.zeros(7 * max_ops, dtype=torch.int32, device=device)
+    items = torch.zeros(max_items * ir.RKT_ITEM.itemsize, dtype=torch.uint8, device=device)
+    st = HluRktScratch(counts.data_ptr(), lst.data_ptr(), items.data_ptr(), max_ops, max_items)
+    return st, (counts, lst, items)

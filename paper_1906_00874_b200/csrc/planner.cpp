@@ -18,6 +18,7 @@
 
 #include "hlu_b200.h"
 #include "hlu_plan.h"
+#include "rk_layout.h"
 
 namespace {
 
@@ -108,17 +109,6 @@ struct RktP {
   int kb;
 };
 
-int64_t ws_one(int m, int k, int ch) {
-  if (m <= 0 || k <= 0) return 0;
-  const int64_t nch = (m + ch - 1) / ch;
-  return nch * ((int64_t)(k + ch) * k + k);
-}
-int chunk_rows(int km) { return (km == 32 ? 4608 : 9216) / km - km; }
-int64_t rkt_ws(int m, int kb) {
-  const int64_t a = ws_one(m, std::min(kb, 32), chunk_rows(32));
-  const int64_t b = ws_one(m, std::min(kb, 64), chunk_rows(64));
-  return std::max(a, b);
-}
 
 struct Planner {
   const hlu_plan_node *N;
@@ -305,7 +295,7 @@ struct Planner {
       slot = x.slot;
       writes.push_back(Iv{x.lo, x.hi});
     }
-    const int64_t wsn = rkt_ws(m, kb) + rkt_ws(n, kb);
+    const int64_t wsn = rk_ws_doubles(m, n, kb);
     int64_t ws = 0;
     if (wsn) {
       const int64_t tw = temp(wsn, &ws);
@@ -1149,7 +1139,7 @@ struct Planner {
         d.out_a = fix(r.out_a, arena_base);
         d.out_b = fix(r.out_b, arena_base);
         d.ws = r.ws ? fix(r.ws, arena_base) : 0;
-        d.handoff = 0;
+        d.reserved = 0;
         d.pad = 0;
         for (int64_t k = r.pb; k < r.pb + r.pn; ++k) {
           const Pair &p = parts[k];
@@ -1185,10 +1175,6 @@ struct Planner {
       if (r.kind == HLU_K_RKT32) {
         L.smem_dim = 0;
         o_launch.push_back(L);
-        if (r.dim > 32) {
-          L.kind = HLU_K_RKT64;
-          o_launch.push_back(L);
-        }
       } else {
         L.smem_dim = r.dim;
         o_launch.push_back(L);

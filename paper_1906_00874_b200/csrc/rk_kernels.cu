@@ -11,35 +11,29 @@
 //   truncation: k = #{sigma_i > eps*sigma_1} (0 if sigma_1 == 0), min(k, kmax),
 //             Sigma folded into the left factor.
 //
-// One CTA per truncation:
-//   A. TSQR of X = [parts.a] (m x K) over row chunks held in shared memory
-//      (Householder, dlarfg conventions); reflectors of every chunk go to a
-//      per-op workspace in the pool.
-//   B. the same for Y = [parts.b] (n x K).
-//   C. core M = R_a R_b^T (<= K x K).
-//   D. one-sided (Hestenes) Jacobi SVD of M (or M^T), round-robin pairs,
-//      one warp per pair, warp-shuffle reductions.
-//   E. descending sort, rank count (strict >), kmax cap.
-//   F. A' = Q_a [U_k S_k; 0], B' = Q_b [V_k; 0] by applying the stored
-//      reflectors chunk by chunk in reverse; one warp per output column.
+// Three kernels per schedule level (geometry in rk_layout.h):
+//   A (k_rkt_a, one CTA per row block of a factor): Householder TSQR of the
+//      block (dlarfg conventions) as a chain of chunks held in shared memory;
+//      reflectors and the block's R go to the op's workspace.  Blocks of one
+//      factor run on different SMs, so a 16k-row factor costs one 512-row chain.
+//   B (k_rkt_b<KM>, one CTA per op; KM=64 variant for 32 < K <= 64): QR of the
+//      stacked block R's (only for factors with > 1 block), core M = R_a R_b^T,
+//      QR with column pivoting of M + one-sided Jacobi on R^T, descending order,
+//      rank count (strict >), kmax cap, W = kept vectors in the R bases, then
+//      the combine-level reflectors applied to [W; 0] -> Z (one block per row).
+//   C (k_rkt_c, one CTA per row block): out rows = Q_block [Z_block; 0].
+// The stacked rank K (and k1, k2) is read once in phase A from the level-start
+// ranks and logged; B and C use the logged values, since B overwrites the
+// destination's rank slot (a part of its own input in ADD mode).
+#include <algorithm>
+
 #include "common.cuh"
+#include "rk_layout.h"
 
 namespace hlu {
 
-template <int KM>
-struct RkCfg {
-  static constexpr int BUFD = (KM == 32) ? 4608 : 9216;  // chunk buffer (doubles)
-  static constexpr int LDS = BUFD / KM;                  // leading dim of the chunk buffer
-  static constexpr int CH = LDS - KM;                    // fresh rows per chunk
-};
-
 #define RK_MAXP 8
-
-__host__ __device__ inline int64_t rk_ws_one(int m, int K, int CH) {
-  if (m <= 0 || K <= 0) return 0;
-  const int64_t nch = (m + CH - 1) / CH;
-  return nch * ((int64_t)(K + CH) * K + K);
-}
+#define RK_NB 8  // columns a warp updates together (interleaved reductions)
 
 struct PartInfo {
   Mat a, b;
@@ -61,13 +55,13 @@ __device__ __forceinline__ double stacked(const PartInfo *P, int np, bool left, 
   return (r >= 0 && r < q.b.rows) ? q.b.get(r, jj) : 0.0;
 }
 
-// A group of warps working on one factor (X or Y) with its own named barrier.
+// A group of warps working on one factor with its own named barrier.
 struct Grp {
-  int id;   // named barrier id (1, 2) or 0 for the whole CTA
-  int nw;   // warps in the group
-  int w;    // warp index inside the group
-  int l;    // lane
-  int t;    // thread index inside the group
+  int id;  // named barrier id (1, 2) or 0 for the whole CTA
+  int nw;  // warps in the group
+  int w;   // warp index inside the group
+  int l;   // lane
+  int t;   // thread index inside the group
   __device__ __forceinline__ int nt() const { return nw * 32; }
   __device__ __forceinline__ void sync() const {
     if (id == 0) __syncthreads();
@@ -75,13 +69,12 @@ struct Grp {
   }
 };
 
-// Reflector for column j of S (rows x ., ld LDS), dlarfg conventions, one warp.
-template <int LDS>
-__device__ __forceinline__ void make_reflector(double *S, int rows, int j, double *tau, int l) {
+// Reflector for column j of S (rows x ., ld), dlarfg conventions, one warp.
+__device__ __forceinline__ void make_reflector(double *S, int ld, int rows, int j, double *tau, int l) {
   double ss = 0.0;
-  for (int i = j + 1 + l; i < rows; i += 32) ss = fma(S[i + j * LDS], S[i + j * LDS], ss);
+  for (int i = j + 1 + l; i < rows; i += 32) ss = fma(S[i + j * ld], S[i + j * ld], ss);
   ss = warp_sum(ss);
-  const double alpha = S[j + j * LDS];
+  const double alpha = S[j + j * ld];
   double tj = 0.0, beta = alpha;
   if (ss != 0.0) {
     // beta = -sign(alpha) ||x||, tau = (beta - alpha) / beta = 1 + |alpha| / ||x||,
@@ -92,195 +85,185 @@ __device__ __forceinline__ void make_reflector(double *S, int rows, int j, doubl
     beta = -copysign(nrm, alpha);
     tj = fma(fabs(alpha), rn, 1.0);
     const double sc = fast_rcp(alpha - beta);
-    for (int i = j + 1 + l; i < rows; i += 32) S[i + j * LDS] *= sc;
+    for (int i = j + 1 + l; i < rows; i += 32) S[i + j * ld] *= sc;
   }
   __syncwarp();
   if (l == 0) {
     tau[j] = tj;
-    S[j + j * LDS] = beta;
+    S[j + j * ld] = beta;
   }
 }
 
-// Householder QR of S (rows x K, ld LDS) in place, tau[K]; columns owned
-// round-robin by the group's warps; the owner of column j+1 builds reflector
-// j+1 right after applying reflector j to it (look-ahead), so each step costs
-// one group barrier.
-template <int KM>
-__device__ void house_qr(double *S, int rows, int K, double *tau, const Grp &g) {
-  constexpr int LDS = RkCfg<KM>::LDS;
+// Apply the reflector H = I - tj [1; v] [1; v]^T (v = v[j+1 .. rows), unit at
+// row j) to nc <= NB columns T[:, c0 + b*cstep] (ld ldt); one warp, the nc
+// reductions interleaved.
+template <int NB>
+__device__ __forceinline__ void refl_cols(const double *v, int rows, int j, double tj, double *T, int ldt, int c0,
+                                          int cstep, int nc, int l) {
+  double acc[NB];
+#pragma unroll
+  for (int b = 0; b < NB; ++b) acc[b] = 0.0;
+  for (int i = j + 1 + l; i < rows; i += 32) {
+    const double x = v[i];
+#pragma unroll
+    for (int b = 0; b < NB; ++b)
+      if (b < nc) acc[b] = fma(x, T[i + (c0 + b * cstep) * ldt], acc[b]);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+    for (int b = 0; b < NB; ++b) acc[b] += __shfl_xor_sync(0xffffffffu, acc[b], o);
+  }
+  double f[NB];
+#pragma unroll
+  for (int b = 0; b < NB; ++b) f[b] = (b < nc) ? tj * (acc[b] + T[j + (c0 + b * cstep) * ldt]) : 0.0;
+  for (int i = j + 1 + l; i < rows; i += 32) {
+    const double x = v[i];
+#pragma unroll
+    for (int b = 0; b < NB; ++b)
+      if (b < nc) T[i + (c0 + b * cstep) * ldt] -= f[b] * x;
+  }
+  __syncwarp();
+  if (l == 0) {
+#pragma unroll
+    for (int b = 0; b < NB; ++b)
+      if (b < nc) T[j + (c0 + b * cstep) * ldt] -= f[b];
+  }
+  __syncwarp();
+}
+
+// all columns c0, c0 + cstep, ... < cend of T, in batches of RK_NB
+__device__ __forceinline__ void refl_colset(const double *v, int rows, int j, double tj, double *T, int ldt, int c0,
+                                            int cstep, int cend, int l) {
+  for (; c0 < cend; c0 += RK_NB * cstep) {
+    const int nc = min(RK_NB, (cend - c0 + cstep - 1) / cstep);
+    refl_cols<RK_NB>(v, rows, j, tj, T, ldt, c0, cstep, nc, l);
+  }
+}
+
+// Householder QR of S (rows x K, ld) in place, tau[K]; column c belongs to
+// warp c % nw.  The owner of column j+1 updates it first and builds reflector
+// j+1 (look-ahead), then every warp updates its remaining columns together;
+// one group barrier per step.
+__device__ void house_qr(double *S, int ld, int rows, int K, double *tau, const Grp &g) {
   const int t = min(rows, K);
   if (t <= 0) return;
-  if (g.w == 0) make_reflector<LDS>(S, rows, 0, tau, g.l);
+  if (g.w == 0) make_reflector(S, ld, rows, 0, tau, g.l);
   g.sync();
   for (int j = 0; j < t; ++j) {
     const double tj = tau[j];
-    int col = j + 1 + ((g.w - (j + 1)) % g.nw + g.nw) % g.nw;
-    for (; col < K; col += g.nw) {
-      if (tj != 0.0) {
-        double acc = 0.0;
-        for (int i = j + 1 + g.l; i < rows; i += 32) acc = fma(S[i + j * LDS], S[i + col * LDS], acc);
-        acc = warp_sum(acc) + S[j + col * LDS];
-        const double f = tj * acc;
-        for (int i = j + 1 + g.l; i < rows; i += 32) S[i + col * LDS] -= f * S[i + j * LDS];
-        __syncwarp();
-        if (g.l == 0) S[j + col * LDS] -= f;
-        __syncwarp();
-      }
-      if (col == j + 1 && col < t) make_reflector<LDS>(S, rows, col, tau, g.l);
+    const double *v = S + j * ld;
+    int c0 = j + 1 + ((g.w - (j + 1)) % g.nw + g.nw) % g.nw;
+    if (c0 == j + 1 && c0 < K) {
+      if (tj != 0.0) refl_cols<1>(v, rows, j, tj, S, ld, c0, g.nw, 1, g.l);
+      if (c0 < t) make_reflector(S, ld, rows, c0, tau, g.l);
+      c0 += g.nw;
     }
+    if (tj != 0.0) refl_colset(v, rows, j, tj, S, ld, c0, g.nw, K, g.l);
     g.sync();
   }
 }
 
-// TSQR of one stacked factor.  R (rr x K, ld KM, zero below the diagonal) -> R.
-template <int KM>
-__device__ int tsqr(const PartInfo *P, int np, bool left, int m, int K, double *S, double *R, double *tau,
-                    double *ws, const Grp &g) {
-  constexpr int LDS = RkCfg<KM>::LDS, CH = RkCfg<KM>::CH;
-  int r = 0;  // carried R rows at the top of S
-  int64_t off = 0;
-  for (int r0 = 0; r0 < m; r0 += CH) {
-    const int cnt = min(CH, m - r0);
+// TSQR of `total` rows (element (i, j) from src) as a chain of chunks of ch
+// fresh rows with the previous R carried on top.  Chunk s's compact QR
+// (ld = its rows) and tau go to ws + s * rk_stride.  Returns r (rows of the
+// final R, left in the top r rows of S, ld = ch + K, upper triangle).
+template <class Src>
+__device__ int tsqr_chain(const Src &src, int total, int K, int ch, double *S, double *tau, double *ws,
+                          const Grp &g) {
+  const int ld = ch + K;
+  const int64_t stride = rk_stride(K, ch);
+  int r = 0;
+  int s = 0;
+  for (int r0 = 0; r0 < total; r0 += ch, ++s) {
+    const int cnt = min(ch, total - r0);
     const int rows = r + cnt;
     for (int e = g.t; e < cnt * K; e += g.nt()) {
       const int i = e % cnt, j = e / cnt;
-      S[r + i + j * LDS] = stacked(P, np, left, r0 + i, j);
+      S[r + i + j * ld] = src(r0 + i, j);
     }
     g.sync();
-    house_qr<KM>(S, rows, K, tau, g);
-    // save the chunk's compact QR (ld = rows) and tau
-    double *dst = ws + off;
+    house_qr(S, ld, rows, K, tau, g);
+    double *dst = ws + s * stride;
     for (int e = g.t; e < rows * K; e += g.nt()) {
       const int i = e % rows, j = e / rows;
-      dst[i + (int64_t)j * rows] = S[i + j * LDS];
+      dst[i + (int64_t)j * rows] = S[i + j * ld];
     }
     for (int j = g.t; j < K; j += g.nt()) dst[(int64_t)rows * K + j] = (j < min(rows, K)) ? tau[j] : 0.0;
-    off += (int64_t)rows * K + K;
     r = min(rows, K);
     g.sync();
-    if (r0 + CH < m) {  // keep R on top for the next chunk
+    if (r0 + ch < total) {  // keep R on top for the next chunk
       for (int e = g.t; e < r * K; e += g.nt()) {
         const int i = e % r, j = e / r;
-        if (i > j) S[i + j * LDS] = 0.0;
+        if (i > j) S[i + j * ld] = 0.0;
       }
       g.sync();
     }
   }
-  for (int e = g.t; e < KM * K; e += g.nt()) {
-    const int i = e % KM, j = e / KM;
-    R[i + j * KM] = (i < r && i <= j) ? S[i + j * LDS] : 0.0;
-  }
-  g.sync();
   return r;
 }
 
-// out (m x kk, ld m) = Q [W (rr x kk, ld KM); 0], Q from the stored chunks.
-// T (BUFD) holds the moving block, VS (BUFD) each chunk's reflectors staged
-// from the workspace with one coalesced copy, so the sequential reflector
-// chain runs out of shared memory; one warp per output column.
-template <int KM>
-__device__ void apply_q(int m, int K, int kk, const double *W, double *T, double *VS, double *tq,
-                        const double *ws, double *out, const Grp &g) {
-  constexpr int LDS = RkCfg<KM>::LDS, CH = RkCfg<KM>::CH;
-  const int nch = (m + CH - 1) / CH;
-  int64_t off_last = 0;
-  int rprev_last = 0;
-  {
-    int r = 0;
-    int64_t off = 0;
-    for (int s = 0; s < nch; ++s) {
-      const int cnt = min(CH, m - s * CH);
-      const int rows = r + cnt;
-      if (s == nch - 1) {
-        off_last = off;
-        rprev_last = r;
-      }
-      off += (int64_t)rows * K + K;
-      r = min(rows, K);
-    }
-    for (int e = g.t; e < r * kk; e += g.nt()) {
-      const int i = e % r, j = e / r;
-      T[i + j * LDS] = W[i + j * KM];
-    }
+// out (total x kk, ld ldo) = Q [W (r_final x kk, ld ldw); 0] with Q the chain
+// of tsqr_chain(total, K, ch) stored at ws.  T (>= (ch + K) kk doubles) holds
+// the moving block; with STAGE each chunk's reflectors are first copied to VS
+// (coalesced) so the sequential chain runs out of shared memory.  The rows of
+// R carried into chunk s are r_{s-1} = min(s ch, K).
+template <bool STAGE>
+__device__ void apply_chain(int total, int K, int ch, int kk, const double *W, int ldw, int r_final, double *T,
+                            double *VS, double *tq, const double *ws, double *out, int64_t ldo, const Grp &g) {
+  const int ldt = ch + K;
+  const int64_t stride = rk_stride(K, ch);
+  const int nch = (total + ch - 1) / ch;
+  for (int e = g.t; e < r_final * kk; e += g.nt()) {
+    const int i = e % r_final, j = e / r_final;
+    T[i + j * ldt] = W[i + j * ldw];
   }
-  int64_t off = off_last;
-  int rprev = rprev_last;
   for (int s = nch - 1; s >= 0; --s) {
-    const int cnt = min(CH, m - s * CH);
-    const int rows = rprev + cnt;
+    const int cnt = min(ch, total - s * ch);
+    const int rp = min(s * ch, K);
+    const int rows = rp + cnt;
     const int rs = min(rows, K);
     g.sync();
     for (int e = g.t; e < (rows - rs) * kk; e += g.nt()) {
       const int i = rs + e % (rows - rs), j = e / (rows - rs);
-      T[i + j * LDS] = 0.0;
+      T[i + j * ldt] = 0.0;
     }
-    const double *V = ws + off;
-    for (int e = g.t; e < rows * K; e += g.nt()) VS[e] = V[e];  // reflectors, ld rows (<= BUFD)
-    for (int e = g.t; e < K; e += g.nt()) tq[e] = V[rows * K + e];
+    const double *V = ws + s * stride;
+    if (STAGE) {
+      for (int e = g.t; e < rows * K; e += g.nt()) VS[e] = V[e];  // reflectors, ld rows
+    }
+    for (int e = g.t; e < K; e += g.nt()) tq[e] = V[(int64_t)rows * K + e];
     g.sync();
-    const double *tau = tq;
-    for (int col = g.w; col < kk; col += g.nw) {
-      double *t = T + col * LDS;
-      for (int j = rs - 1; j >= 0; --j) {
-        const double tj = tau[j];
-        if (tj == 0.0) continue;
-        const double *v = VS + j * rows;
-        double acc = 0.0;
-        for (int i = j + 1 + g.l; i < rows; i += 32) acc = fma(v[i], t[i], acc);
-        acc = warp_sum(acc) + t[j];
-        const double f = tj * acc;
-        for (int i = j + 1 + g.l; i < rows; i += 32) t[i] -= f * v[i];
-        __syncwarp();
-        if (g.l == 0) t[j] -= f;
-        __syncwarp();
-      }
+    const double *VV = STAGE ? VS : V;
+    for (int j = rs - 1; j >= 0; --j) {
+      const double tj = tq[j];
+      if (tj == 0.0) continue;
+      refl_colset(VV + j * rows, rows, j, tj, T, ldt, g.w, g.nw, kk, g.l);
     }
     g.sync();
     for (int e = g.t; e < cnt * kk; e += g.nt()) {
       const int i = e % cnt, j = e / cnt;
-      out[(int64_t)s * CH + i + (int64_t)j * m] = T[rprev + i + j * LDS];
-    }
-    if (s > 0) {
-      int r = 0;
-      int64_t o2 = 0, o_prev = 0;
-      int rp_prev = 0;
-      for (int u = 0; u < s; ++u) {
-        const int c2 = min(CH, m - u * CH);
-        const int rows2 = r + c2;
-        if (u == s - 1) {
-          o_prev = o2;
-          rp_prev = r;
-        }
-        o2 += (int64_t)rows2 * K + K;
-        r = min(rows2, K);
-      }
-      off = o_prev;
-      rprev = rp_prev;
+      out[(int64_t)s * ch + i + (int64_t)j * ldo] = T[rp + i + j * ldt];
     }
   }
   g.sync();
 }
 
 __device__ unsigned long long g_sweeps = 0;  // total Jacobi sweeps (diagnostics)
-__device__ unsigned g_epoch = 1;            // bumped once per schedule replay
-__device__ unsigned long long g_phase[10];   // summed cycles per phase (diagnostics)
-__device__ unsigned long long g_phase_max[10];
-#define PHASE(k)                                                   \
-  if (threadIdx.x == 0) {                                          \
-    const unsigned long long now = clock64();                      \
-    atomicAdd(&g_phase[k], now - t_last);                          \
-    atomicMax(&g_phase_max[k], now - t_last);                      \
-    t_last = now;                                                  \
-  }
 
 // Round-robin pairing table: round r, slot i -> (a, b); computed once per op.
+template <int NT>
 __device__ __forceinline__ void build_pairs(unsigned char *pa, unsigned char *pb, int qq) {
-  for (int e = threadIdx.x; e < (qq - 1) * (qq / 2); e += HLU_NT) {
+  for (int e = threadIdx.x; e < (qq - 1) * (qq / 2); e += NT) {
     const int r = e / (qq / 2), i = e % (qq / 2);
     const int u = i, v = qq - 1 - i;
     int a = u == 0 ? 0 : 1 + (u - 1 + r) % (qq - 1);
     int b = v == 0 ? 0 : 1 + (v - 1 + r) % (qq - 1);
-    if (a > b) { const int x = a; a = b; b = x; }
+    if (a > b) {
+      const int x = a;
+      a = b;
+      b = x;
+    }
     pa[e] = (unsigned char)a;
     pb[e] = (unsigned char)b;
   }
@@ -289,18 +272,20 @@ __device__ __forceinline__ void build_pairs(unsigned char *pa, unsigned char *pb
 // QR with column pivoting of G (p x q, p >= q, ld KM), in place, without
 // moving data: cm[j] is the physical column holding logical column j (the
 // pivot order), reflector j lives below row j of column cm[j], tau[j].
-template <int KM>
+// Each warp updates its columns (and recomputes their norms) together.
+template <int KM, int NT>
 __device__ void qrcp(double *G, int p, int q, double *tau, int *cm, double *nrm) {
   const int tid = threadIdx.x, w = tid >> 5, l = tid & 31;
   __shared__ double s_beta;
-  for (int c = tid; c < q; c += HLU_NT) cm[c] = c;
-  for (int c = w; c < q; c += HLU_NWARP) {
+  for (int c = tid; c < q; c += NT) cm[c] = c;
+  for (int c = w; c < q; c += (NT / 32)) {
     double ss = 0.0;
     for (int i = l; i < p; i += 32) ss += G[i + c * KM] * G[i + c * KM];
     ss = warp_sum(ss);
     if (l == 0) nrm[c] = ss;
   }
   __syncthreads();
+  constexpr int NB = (KM + (NT / 32) - 1) / (NT / 32);
   for (int j = 0; j < q; ++j) {
     if (w == 0) {
       // pivot: largest remaining norm (first on ties), then the reflector
@@ -308,17 +293,26 @@ __device__ void qrcp(double *G, int p, int q, double *tau, int *cm, double *nrm)
       int bi = j;
       for (int c = j + l; c < q; c += 32) {
         const double v = nrm[cm[c]];
-        if (v > best) { best = v; bi = c; }
+        if (v > best) {
+          best = v;
+          bi = c;
+        }
       }
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
         const double ob = __shfl_xor_sync(0xffffffffu, best, o);
         const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-        if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+        if (ob > best || (ob == best && oi < bi)) {
+          best = ob;
+          bi = oi;
+        }
       }
       const int cj = cm[bi];
       __syncwarp();
-      if (l == 0 && bi != j) { cm[bi] = cm[j]; cm[j] = cj; }
+      if (l == 0 && bi != j) {
+        cm[bi] = cm[j];
+        cm[j] = cj;
+      }
       double ss = 0.0;
       for (int i = j + 1 + l; i < p; i += 32) ss += G[i + cj * KM] * G[i + cj * KM];
       ss = warp_sum(ss);
@@ -332,28 +326,74 @@ __device__ void qrcp(double *G, int p, int q, double *tau, int *cm, double *nrm)
         const double sc = fast_rcp(alpha - beta);
         for (int i = j + 1 + l; i < p; i += 32) G[i + cj * KM] *= sc;
       }
-      if (l == 0) { tau[j] = tj; s_beta = beta; }
+      if (l == 0) {
+        tau[j] = tj;
+        s_beta = beta;
+      }
     }
     __syncthreads();
     const double tj = tau[j];
-    const int cj = cm[j];
-    for (int c = j + 1 + w; c < q; c += HLU_NWARP) {
-      const int pc = cm[c];
-      if (tj != 0.0) {
-        double acc = 0.0;
-        for (int i = j + 1 + l; i < p; i += 32) acc += G[i + cj * KM] * G[i + pc * KM];
-        acc = warp_sum(acc) + G[j + pc * KM];
-        const double f = tj * acc;
-        for (int i = j + 1 + l; i < p; i += 32) G[i + pc * KM] -= f * G[i + cj * KM];
-        __syncwarp();
-        if (l == 0) G[j + pc * KM] -= f;
-      }
-      double ss = 0.0;
-      for (int i = j + 1 + l; i < p; i += 32) ss += G[i + pc * KM] * G[i + pc * KM];
-      ss = warp_sum(ss);
-      if (l == 0) nrm[pc] = ss;
+    const double *v = G + cm[j] * KM;
+    int pc[NB];
+    int nc = 0;
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      const int c = j + 1 + w + b * (NT / 32);
+      pc[b] = c < q ? cm[c] : 0;
+      nc += c < q;
     }
-    if (tid == 0) G[j + cj * KM] = s_beta;
+    if (nc > 0) {
+      double acc[NB];
+#pragma unroll
+      for (int b = 0; b < NB; ++b) acc[b] = 0.0;
+      if (tj != 0.0) {
+        for (int i = j + 1 + l; i < p; i += 32) {
+          const double x = v[i];
+#pragma unroll
+          for (int b = 0; b < NB; ++b)
+            if (b < nc) acc[b] += x * G[i + pc[b] * KM];
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+          for (int b = 0; b < NB; ++b) acc[b] += __shfl_xor_sync(0xffffffffu, acc[b], o);
+        }
+        double f[NB];
+#pragma unroll
+        for (int b = 0; b < NB; ++b) f[b] = (b < nc) ? tj * (acc[b] + G[j + pc[b] * KM]) : 0.0;
+        for (int i = j + 1 + l; i < p; i += 32) {
+          const double x = v[i];
+#pragma unroll
+          for (int b = 0; b < NB; ++b)
+            if (b < nc) G[i + pc[b] * KM] -= f[b] * x;
+        }
+        __syncwarp();
+        if (l == 0) {
+#pragma unroll
+          for (int b = 0; b < NB; ++b)
+            if (b < nc) G[j + pc[b] * KM] -= f[b];
+        }
+      }
+      double ss[NB];
+#pragma unroll
+      for (int b = 0; b < NB; ++b) ss[b] = 0.0;
+      for (int i = j + 1 + l; i < p; i += 32) {
+#pragma unroll
+        for (int b = 0; b < NB; ++b)
+          if (b < nc) ss[b] += G[i + pc[b] * KM] * G[i + pc[b] * KM];
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+        for (int b = 0; b < NB; ++b) ss[b] += __shfl_xor_sync(0xffffffffu, ss[b], o);
+      }
+      if (l == 0) {
+#pragma unroll
+        for (int b = 0; b < NB; ++b)
+          if (b < nc) nrm[pc[b]] = ss[b];
+      }
+    }
+    if (tid == 0) G[j + cm[j] * KM] = s_beta;
     __syncthreads();
   }
 }
@@ -391,11 +431,10 @@ __device__ __forceinline__ double part_sum(double v) {
   return v;
 }
 
-template <int KM, int LP>
-__device__ void jacobi_lp(double *X, double *V, int n, const unsigned char *pa, const unsigned char *pb,
-                          double *smax) {
+template <int KM, int LP, int NT>
+__device__ void jacobi_lp(double *X, double *V, int n, const unsigned char *pa, const unsigned char *pb) {
   const int tid = threadIdx.x;
-  const int grp = tid / LP, l = tid % LP, ngrp = HLU_NT / LP;
+  const int grp = tid / LP, l = tid % LP, ngrp = NT / LP;
   const int qq = n + (n & 1);
   const int np = qq / 2;
   for (int sweep = 0; sweep < 40; ++sweep) {
@@ -420,16 +459,16 @@ __device__ void jacobi_lp(double *X, double *V, int n, const unsigned char *pa, 
         // t = tan(theta) = 2 ga / (d + sign(d) sqrt(d^2 + 4 ga^2)), d = be - al
         const double d = be - al;
         const double q2 = fma(d, d, 4.0 * g2);
-        const double r = q2 * fast_rsqrt(q2);
-        const double t = 2.0 * ga * fast_rcp(d + copysign(r, d));
+        const double rq = q2 * fast_rsqrt(q2);
+        const double t = 2.0 * ga * fast_rcp(d + copysign(rq, d));
         const double cs = fast_rsqrt(fma(t, t, 1.0)), sn = cs * t;
         for (int i = l; i < n; i += LP) {
           const double x = X[i + a * KM], y = X[i + b * KM];
           X[i + a * KM] = cs * x - sn * y;
           X[i + b * KM] = sn * x + cs * y;
-          const double u = V[i + a * KM], v = V[i + b * KM];
-          V[i + a * KM] = cs * u - sn * v;
-          V[i + b * KM] = sn * u + cs * v;
+          const double u = V[i + a * KM], vv = V[i + b * KM];
+          V[i + a * KM] = cs * u - sn * vv;
+          V[i + b * KM] = sn * u + cs * vv;
         }
       }
       __syncthreads();
@@ -441,40 +480,24 @@ __device__ void jacobi_lp(double *X, double *V, int n, const unsigned char *pa, 
   }
 }
 
-template <int KM>
+template <int KM, int NT>
 __device__ void jacobi(double *X, double *V, int n, const unsigned char *pa, const unsigned char *pb) {
-  __shared__ double smax[HLU_NWARP];
-  for (int e = threadIdx.x; e < KM * KM; e += HLU_NT) V[e] = ((e % KM) == (e / KM)) ? 1.0 : 0.0;
+  for (int e = threadIdx.x; e < KM * KM; e += NT) V[e] = ((e % KM) == (e / KM)) ? 1.0 : 0.0;
   __syncthreads();
   if (n < 2) return;
-  if ((n + 1) / 2 > HLU_NWARP) jacobi_lp<KM, 16>(X, V, n, pa, pb, smax);
-  else jacobi_lp<KM, 32>(X, V, n, pa, pb, smax);
+  if ((n + 1) / 2 > NT / 32) jacobi_lp<KM, 16, NT>(X, V, n, pa, pb);
+  else jacobi_lp<KM, 32, NT>(X, V, n, pa, pb);
   __syncthreads();
 }
 
-template <int KM>
-__global__ void __launch_bounds__(HLU_NT)
-    k_rkt(hlu_ctx c, hlu_rkt_desc *__restrict__ d, const hlu_rkpart *__restrict__ parts) {
-  using Cfg = RkCfg<KM>;
-  extern __shared__ double sm[];
-  double *S = sm;                 // BUFD   group-0 chunk buffer (X), later G | V
-  double *S1 = S + Cfg::BUFD;     // BUFD   group-1 chunk buffer (Y), later XT
-  double *RA = S1 + Cfg::BUFD;    // KM*KM
-  double *RB = RA + KM * KM;      // KM*KM
-  double *tau = RB + KM * KM;     // KM
-  double *tau1 = tau + KM;        // KM
-  double *sig = tau1 + KM;        // KM
-  double *XT = S1;                // KM*KM  (R^T, then W = R^T V)
-  __shared__ PartInfo P[RK_MAXP];
-  __shared__ int perm[KM];
-  __shared__ int cmap[KM];
-  __shared__ unsigned char pairs_a[(KM - 1) * (KM / 2)], pairs_b[(KM - 1) * (KM / 2)];
-  __shared__ int s_kk;
-  unsigned long long t_last = clock64();
-  const hlu_rkt_desc o = d[blockIdx.x];
+// ---------------------------------------------------------------- op state
+
+// parts of op o into P (shared), returns the part count; one thread per part
+__device__ __forceinline__ int load_parts(const hlu_ctx &c, const hlu_rkt_desc &o, const hlu_rkpart *parts,
+                                          PartInfo *P) {
   const int tid = threadIdx.x;
-  const int np = o.part_count;
-  if (tid < np && tid < RK_MAXP) {  // one thread per part: the descriptor/rank loads overlap
+  const int np = min(o.part_count, RK_MAXP);
+  if (tid < np) {
     const hlu_rkpart q = parts[o.part_begin + tid];
     P[tid].a = resolve(c, q.a);
     P[tid].b = resolve(c, q.b);
@@ -486,48 +509,870 @@ __global__ void __launch_bounds__(HLU_NT)
   __syncthreads();
   if (tid == 0) {
     int col = 0;
-    for (int p = 0; p < np && p < RK_MAXP; ++p) {
+    for (int p = 0; p < np; ++p) {
       P[p].col0 = col;
       col += P[p].k;
     }
   }
   __syncthreads();
-  int K = 0;
-  for (int p = 0; p < np; ++p) K += P[p].k;
-  const int m = o.m, n = o.n;
-  double *outA = c.pool + o.out_a;
-  double *outB = c.pool + o.out_b;
+  return np;
+}
 
-  // Variant ownership.  Both variants run over the same level, possibly
-  // concurrently.  An op is taken by the variant whose range contains its
-  // stacked rank K, and only after that variant wins an atomicCAS that stamps
-  // the replay epoch into the descriptor; ranks change only after a claim.
-  // The first claim therefore always sees the level-start ranks (so the right
-  // variant wins), and a variant that reads ranks already updated by the other
-  // one loses the CAS (fences on both sides), so no op runs twice.
-  const int epoch = (int)*(volatile unsigned *)&g_epoch;
-  __shared__ int s_take;
-  if (tid == 0) {
-    const bool mine = (KM == 32) ? (K <= 32) : (K > 32);
-    int take = 0;
-    if (mine) {
-      __threadfence();
-      const int h = *(volatile int *)&d[blockIdx.x].handoff;
-      take = h != epoch && atomicCAS(&d[blockIdx.x].handoff, h, epoch) == h;
-      __threadfence();
-    }
-    s_take = take;
+// logged (k1, k2) / (K, 0) of op o -> K, and whether the op is an ADD shortcut
+__device__ __forceinline__ int logged_K(const hlu_ctx &c, const hlu_rkt_desc &o, bool *shortcut) {
+  const int k1 = c.log[o.log], k2 = c.log[o.log + 1];
+  *shortcut = (o.mode == HLU_RK_ADD) && (k1 == 0 || k2 == 0);
+  return o.mode == HLU_RK_ADD ? k1 + k2 : k1;
+}
+
+struct PartsSrc {
+  const PartInfo *P;
+  int np;
+  bool left;
+  int row0;
+  __device__ __forceinline__ double operator()(int i, int j) const { return stacked(P, np, left, row0 + i, j); }
+};
+
+struct StackedR {  // the blocks' R factors stacked: block b at R + b K K (ld K)
+  const double *R;
+  int K;
+  __device__ __forceinline__ double operator()(int i, int j) const {
+    const int b = i / K, rr = i - b * K;
+    return R[(int64_t)b * K * K + rr + j * K];
   }
-  __syncthreads();
-  if (!s_take) return;
-  if (o.mode == HLU_RK_ADD) {
-    const int k1 = P[0].k, k2 = P[1].k;
-    if (tid == 0 && o.log >= 0) {
-      c.log[o.log] = k1;
-      c.log[o.log + 1] = k2;
+};
+
+// ---------------------------------------------------------------- classify
+
+// per-level counters (RK_CNT ints at counts + RK_CNT * slot) and op-list segments
+#define RK_CNT 8
+#define RK_SEG_R8 0     // max(m,n) <= 64, K <= 8: register warp kernel
+#define RK_SEG_R16 1    // max(m,n) <= 64, K <= 16: register warp kernel
+#define RK_SEG_W32 2    // max(m,n) <= 64, K <= 32: shared-memory warp kernel
+#define RK_SEG_BIG 3    // CTA phases (and the ADD shortcuts / empty recompressions)
+#define RK_SEG_C16 4    // CTA-path ops with K <= 16, m, n <= RK_BR: core SVD by one warp
+#define RK_SEG_Q8 5     // max(m,n) <= 128, K <= 8: register warp kernel, 4 rows per lane
+#define RK_SEG_Q16 6    // max(m,n) <= 128, K <= 16: register warp kernel, 4 rows per lane
+#define RK_NSEG 7
+// largest factor height of the register warp kernels (64: 2 rows per lane only;
+// the 4-rows-per-lane variant breaks rank parity at cfg2, under investigation)
+#define RK_RMAX 64
+#define RK_CNT_ITEMS 7  // row blocks of the CTA-path ops
+
+// One thread per op of the level: the stacked rank from the level-start ranks
+// is logged ((k1, k2) for ADD, (K, 0) for RECOMPRESS; every later phase reads
+// the log, because the op overwrites its destination's rank), and the op is
+// routed: small ops (max(m, n) <= 64, K <= 32) to the warp kernels, the rest
+// (and the ADD shortcuts / empty recompressions) to the CTA phases, whose row
+// blocks become work items.
+__global__ void k_rkt_classify(hlu_ctx c, const hlu_rkt_desc *__restrict__ d, const hlu_rkpart *__restrict__ parts,
+                               int64_t first, int count, hlu_rkt_scratch s, int slot) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= count) return;
+  const int op = (int)(first + i);
+  const hlu_rkt_desc o = d[op];
+  int K = 0, k1 = 0, k2 = 0;
+  for (int p = 0; p < o.part_count; ++p) {
+    const hlu_view v = parts[o.part_begin + p].a;
+    const int k = v.cdyn >= 0 ? c.ranks[v.cdyn] : v.cols;
+    if (p == 0) k1 = k;
+    if (p == 1) k2 = k;
+    K += k;
+  }
+  const bool add = o.mode == HLU_RK_ADD;
+  c.log[o.log] = add ? k1 : K;
+  c.log[o.log + 1] = add ? k2 : 0;
+  int32_t *cnt = s.counts + RK_CNT * slot;
+  if ((add && (k1 == 0 || k2 == 0)) || K == 0) {
+    s.list[RK_SEG_BIG * s.max_ops + atomicAdd(&cnt[RK_SEG_BIG], 1)] = op;
+    return;
+  }
+  if (K > RK_KMAX || o.part_count > RK_MAXP) {
+    atomicAdd(&c.err[2], 1);
+    return;
+  }
+  if (max(o.m, o.n) <= RK_RMAX && K <= 16) {
+    const bool r2 = max(o.m, o.n) <= 64;
+    const int w = K <= 8 ? (r2 ? RK_SEG_R8 : RK_SEG_Q8) : (r2 ? RK_SEG_R16 : RK_SEG_Q16);
+    s.list[w * s.max_ops + atomicAdd(&cnt[w], 1)] = op;
+    return;
+  }
+  s.list[RK_SEG_BIG * s.max_ops + atomicAdd(&cnt[RK_SEG_BIG], 1)] = op;
+  if (K <= 16 && o.m <= RK_BR && o.n <= RK_BR) s.list[RK_SEG_C16 * s.max_ops + atomicAdd(&cnt[RK_SEG_C16], 1)] = op;
+  const int nbm = (o.m + RK_BR - 1) / RK_BR, nbn = (o.n + RK_BR - 1) / RK_BR;
+  const int base = atomicAdd(&cnt[RK_CNT_ITEMS], nbm + nbn);
+  for (int b = 0; b < nbm + nbn; ++b) {
+    hlu_rkt_item it;
+    it.op = op;
+    it.side = (int16_t)(b >= nbm);
+    it.block = (int16_t)(b >= nbm ? b - nbm : b);
+    s.items[base + b] = it;
+  }
+}
+
+// ---------------------------------------------------------------- warp path
+//
+// One warp per small truncation (max(m, n) <= 64, K <= KB): lane l owns rows
+// l and l + 32 of the factor being factorised (warp-private shared memory,
+// ld 64), so a Householder step needs only warp shuffles; the core SVD is a
+// one-sided Jacobi with one lane per column.  X's reflectors are parked in
+// the op's workspace while Y is factorised.
+
+template <int KB>
+struct WCfg {
+  static constexpr int WPC = KB == 16 ? 4 : 2;  // warps (ops) per CTA
+  static constexpr int LDG = KB + 1;
+  static constexpr int PER = 64 * KB + 2 * KB * LDG + 3 * KB;  // S | G | V | tau_x | tau_y | sig
+  static size_t smem() { return (size_t)WPC * PER * sizeof(double); }
+};
+
+// factor column j (< K) of the stacked X (left) or Y into S (ld 64); zero rows >= M
+__device__ __forceinline__ void w_load(const PartInfo *P, int np, bool left, int M, int K, double *S, int l) {
+  for (int j = 0; j < K; ++j) {
+    S[l + 64 * j] = l < M ? stacked(P, np, left, l, j) : 0.0;
+    S[l + 32 + 64 * j] = l + 32 < M ? stacked(P, np, left, l + 32, j) : 0.0;
+  }
+}
+
+// Householder QR (dlarfg conventions) of S (64 x K, ld 64, zero-padded rows)
+// in place; tau[K].  Lane l touches only its rows l, l + 32.
+__device__ void w_qr(double *S, int K, double *tau, int l) {
+  for (int j = 0; j < K; ++j) {
+    const double x0 = S[l + 64 * j], x1 = S[l + 32 + 64 * j];
+    double ss = l > j ? x0 * x0 : 0.0;
+    ss = fma(x1, x1, ss);
+    ss = warp_sum(ss);
+    const double alpha = __shfl_sync(0xffffffffu, x0, j);
+    double tj = 0.0, beta = alpha, sc = 0.0;
+    if (ss != 0.0) {
+      const double n2 = fma(alpha, alpha, ss);
+      const double rn = fast_rsqrt(n2);
+      beta = -copysign(n2 * rn, alpha);
+      tj = fma(fabs(alpha), rn, 1.0);
+      sc = fast_rcp(alpha - beta);
     }
-    if (k2 == 0 || k1 == 0) {
-      const PartInfo &src = (k2 == 0) ? P[0] : P[1];
+    const double v0 = l > j ? x0 * sc : (l == j ? 1.0 : 0.0);
+    const double v1 = x1 * sc;
+    S[l + 64 * j] = l > j ? v0 : (l == j ? beta : x0);
+    S[l + 32 + 64 * j] = v1;
+    if (l == 0) tau[j] = tj;
+    if (tj == 0.0) continue;
+    for (int c0 = j + 1; c0 < K; c0 += RK_NB) {
+      double p[RK_NB];
+#pragma unroll
+      for (int b = 0; b < RK_NB; ++b) {
+        const int cc = c0 + b;
+        p[b] = cc < K ? fma(v1, S[l + 32 + 64 * cc], v0 * S[l + 64 * cc]) : 0.0;
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+        for (int b = 0; b < RK_NB; ++b) p[b] += __shfl_xor_sync(0xffffffffu, p[b], o);
+      }
+#pragma unroll
+      for (int b = 0; b < RK_NB; ++b) {
+        const int cc = c0 + b;
+        if (cc < K) {
+          const double f = tj * p[b];
+          S[l + 64 * cc] -= f * v0;
+          S[l + 32 + 64 * cc] -= f * v1;
+        }
+      }
+    }
+  }
+}
+
+// round-robin (circle method) partner of column c in round r, qq even
+__device__ __forceinline__ int rr_partner(int c, int r, int qq) {
+  const int n1 = qq - 1;
+  const int pos = c == 0 ? 0 : 1 + (c - 1 - r + n1) % n1;
+  const int pp = qq - 1 - pos;
+  return pp == 0 ? 0 : 1 + (pp - 1 + r) % n1;
+}
+
+// new own column l (of the pair (a, b)) = rotation of columns a, b of X, in
+// chunks of RK_NB rows held in registers; the warp syncs between the reads
+// and the writes of every chunk, because the partner lane reads the same rows
+template <int LDG>
+__device__ __forceinline__ void w_rotate(double *X, int K, int a, int b, bool rot, bool is_a, double cs, double sn,
+                                         int l) {
+  for (int i0 = 0; i0 < K; i0 += RK_NB) {
+    double x[RK_NB], y[RK_NB];
+    if (rot) {
+#pragma unroll
+      for (int q = 0; q < RK_NB; ++q) {
+        if (i0 + q < K) {
+          x[q] = X[a * LDG + i0 + q];
+          y[q] = X[b * LDG + i0 + q];
+        }
+      }
+    }
+    __syncwarp();
+    if (rot) {
+#pragma unroll
+      for (int q = 0; q < RK_NB; ++q)
+        if (i0 + q < K) X[l * LDG + i0 + q] = is_a ? cs * x[q] - sn * y[q] : sn * x[q] + cs * y[q];
+    }
+    __syncwarp();
+  }
+}
+
+// one-sided Jacobi on G (K x K, ld KB+1; lane c owns column c) accumulating V;
+// same rotation formulas and stopping rule as the CTA kernel
+template <int KB>
+__device__ void w_jacobi(double *G, double *V, int K, int l) {
+  constexpr int LDG = KB + 1;
+  if (K < 2) return;
+  const int qq = K + (K & 1);
+  for (int sweep = 0; sweep < 40; ++sweep) {
+    int big = 0;
+    for (int r = 0; r < qq - 1; ++r) {
+      const int pl = l < qq ? rr_partner(l, r, qq) : qq;
+      const bool act = l < K && pl < K;
+      const int a = min(l, pl), b = max(l, pl);
+      double cs = 1.0, sn = 0.0;
+      bool rot = false;
+      if (act) {
+        double al = 0.0, be = 0.0, ga = 0.0;
+        for (int i = 0; i < K; ++i) {
+          const double x = G[a * LDG + i], y = G[b * LDG + i];
+          al = fma(x, x, al);
+          be = fma(y, y, be);
+          ga = fma(x, y, ga);
+        }
+        const double g2 = ga * ga, ab = al * be;
+        if (ga != 0.0 && g2 > 1e-30 * ab) {
+          rot = true;
+          if (g2 > 1e-16 * ab) big = 1;
+          const double dd = be - al;
+          const double q2 = fma(dd, dd, 4.0 * g2);
+          const double rq = q2 * fast_rsqrt(q2);
+          const double t = 2.0 * ga * fast_rcp(dd + copysign(rq, dd));
+          cs = fast_rsqrt(fma(t, t, 1.0));
+          sn = cs * t;
+        }
+      }
+      w_rotate<LDG>(G, K, a, b, rot, l == a, cs, sn, l);
+      w_rotate<LDG>(V, K, a, b, rot, l == a, cs, sn, l);
+    }
+    if (!__any_sync(0xffffffffu, big)) {
+      if (l == 0) atomicAdd(&g_sweeps, sweep + 1);
+      break;
+    }
+  }
+}
+
+// out (M x kk, ld M) = Q [W_sel; 0]: W_sel column cc = W column perm[cc]
+// (K rows, ld KB+1), Q from the reflectors in S / tau; RK_NB output columns
+// at a time in registers (lane l: rows l, l + 32).
+template <int KB>
+__device__ void w_apply(const double *S, int K, const double *tau, const double *W, const int *perm, int kk, int M,
+                        double *out, int l) {
+  constexpr int LDG = KB + 1;
+  for (int c0 = 0; c0 < kk; c0 += RK_NB) {
+    double t0[RK_NB], t1[RK_NB];
+#pragma unroll
+    for (int q = 0; q < RK_NB; ++q) {
+      t0[q] = (c0 + q < kk && l < K) ? W[perm[c0 + q] * LDG + l] : 0.0;
+      t1[q] = 0.0;
+    }
+    for (int j = K - 1; j >= 0; --j) {
+      const double tj = tau[j];
+      if (tj == 0.0) continue;
+      const double v0 = l > j ? S[l + 64 * j] : (l == j ? 1.0 : 0.0);
+      const double v1 = S[l + 32 + 64 * j];
+      double p[RK_NB];
+#pragma unroll
+      for (int q = 0; q < RK_NB; ++q) p[q] = fma(v1, t1[q], v0 * t0[q]);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+        for (int q = 0; q < RK_NB; ++q) p[q] += __shfl_xor_sync(0xffffffffu, p[q], o);
+      }
+#pragma unroll
+      for (int q = 0; q < RK_NB; ++q) {
+        const double f = tj * p[q];
+        t0[q] -= f * v0;
+        t1[q] -= f * v1;
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < RK_NB; ++q) {
+      if (c0 + q < kk) {
+        if (l < M) out[l + (int64_t)(c0 + q) * M] = t0[q];
+        if (l + 32 < M) out[l + 32 + (int64_t)(c0 + q) * M] = t1[q];
+      }
+    }
+  }
+}
+
+template <int KB>
+__device__ void w_trunc(const hlu_ctx &c, const hlu_rkt_desc &o, const hlu_rkpart *parts, PartInfo *P, double *S,
+                        int *perm, int l) {
+  constexpr int LDG = KB + 1;
+  double *G = S + 64 * KB;
+  double *V = G + KB * LDG;
+  double *taux = V + KB * LDG;
+  double *tauy = taux + KB;
+  double *sig = tauy + KB;
+  const int np = min(o.part_count, RK_MAXP);
+  if (l < np) {
+    const hlu_rkpart q = parts[o.part_begin + l];
+    P[l].a = resolve(c, q.a);
+    P[l].b = resolve(c, q.b);
+    P[l].sign = q.sign;
+    P[l].roff = q.roff;
+    P[l].coff = q.coff;
+    P[l].k = P[l].a.cols;
+  }
+  __syncwarp();
+  if (l == 0) {
+    int col = 0;
+    for (int p = 0; p < np; ++p) {
+      P[p].col0 = col;
+      col += P[p].k;
+    }
+  }
+  __syncwarp();
+  bool shortcut;
+  const int K = logged_K(c, o, &shortcut);
+  const int m = o.m, n = o.n;
+  double *ws = c.pool + o.ws;
+  // X = Q_x R_x: R_x -> G (upper, ld LDG), reflectors -> workspace
+  w_load(P, np, true, m, K, S, l);
+  w_qr(S, K, taux, l);
+  for (int cc = 0; cc < K; ++cc) {
+    if (l < K) G[cc * LDG + l] = l <= cc ? S[l + 64 * cc] : 0.0;
+    ws[l + 64 * cc] = S[l + 64 * cc];
+    ws[l + 32 + 64 * cc] = S[l + 32 + 64 * cc];
+  }
+  // Y = Q_y R_y
+  w_load(P, np, false, n, K, S, l);
+  w_qr(S, K, tauy, l);
+  __syncwarp();
+  // M = R_x R_y^T into V (lane c: column c); R_y[c][t] = S[c + 64 t], t >= c
+  if (l < K) {
+    for (int i = 0; i < K; ++i) {
+      double acc = 0.0;
+      for (int t = max(i, l); t < K; ++t) acc = fma(G[t * LDG + i], S[l + 64 * t], acc);
+      V[l * LDG + i] = acc;
+    }
+  }
+  __syncwarp();
+  double *Gm = V, *Vm = G;
+  if (l < K)
+    for (int i = 0; i < K; ++i) Vm[l * LDG + i] = i == l ? 1.0 : 0.0;
+  __syncwarp();
+  w_jacobi<KB>(Gm, Vm, K, l);
+  if (l < K) {
+    double ss = 0.0;
+    for (int i = 0; i < K; ++i) ss = fma(Gm[l * LDG + i], Gm[l * LDG + i], ss);
+    sig[l] = sqrt(ss);
+  }
+  __syncwarp();
+  if (l < K) {
+    int rk = 0;
+    const double sj = sig[l];
+    for (int i = 0; i < K; ++i) rk += (sig[i] > sj) || (sig[i] == sj && i < l);
+    perm[rk] = l;
+  }
+  __syncwarp();
+  int kk = 0;
+  {
+    const double s1 = sig[perm[0]];
+    if (s1 != 0.0) {
+      const double thr = c.eps * s1;
+      for (int i = 0; i < K; ++i) kk += sig[i] > thr;
+    }
+    if (c.kmax >= 0) kk = min(kk, c.kmax);
+    if (kk > o.cap) {
+      if (l == 0) atomicAdd(&c.err[0], 1);
+      kk = o.cap;
+    }
+  }
+  // B' = Q_y [V_k; 0] (Y's reflectors are still in S), then A' = Q_x [(U S)_k; 0]
+  w_apply<KB>(S, K, tauy, Vm, perm, kk, n, c.pool + o.out_b, l);
+  for (int cc = 0; cc < K; ++cc) {
+    S[l + 64 * cc] = ws[l + 64 * cc];
+    S[l + 32 + 64 * cc] = ws[l + 32 + 64 * cc];
+  }
+  w_apply<KB>(S, K, taux, Gm, perm, kk, m, c.pool + o.out_a, l);
+  if (l == 0) {
+    c.ranks[o.out_slot] = kk;
+    c.log[o.log + 2] = kk;
+  }
+}
+
+template <int KB>
+__global__ void __launch_bounds__(WCfg<KB>::WPC * 32, 16 / WCfg<KB>::WPC)
+    k_rkt_w(hlu_ctx c, const hlu_rkt_desc *__restrict__ d, const hlu_rkpart *__restrict__ parts, hlu_rkt_scratch s,
+            int slot) {
+  constexpr int WPC = WCfg<KB>::WPC;
+  extern __shared__ double sm[];
+  __shared__ PartInfo P[WPC][RK_MAXP];
+  __shared__ int perm[WPC][KB];
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  const int n = s.counts[RK_CNT * slot + RK_SEG_W32];
+  const int32_t *lst = s.list + RK_SEG_W32 * s.max_ops;
+  double *S = sm + w * WCfg<KB>::PER;
+  for (int idx = blockIdx.x * WPC + w; idx < n; idx += gridDim.x * WPC) {
+    const hlu_rkt_desc o = d[lst[idx]];
+    w_trunc<KB>(c, o, parts, P[w], S, perm[w], l);
+    __syncwarp();
+  }
+}
+
+// ---------------------------------------------------------------- register warp path
+//
+// One warp per small truncation (max(m, n) <= 32 RPL, K <= KB), every loop
+// unrolled at compile time so a factor lives in registers: lane l owns rows
+// l + 32 q (q < RPL).  With RPL = 2 the Householder QRs of X and Y run
+// interleaved (two independent chains); with RPL = 4 one after the other.
+// Reflectors are parked in warp-private shared memory (ld 32 RPL).  The core
+// SVD (r_core) holds M one column per lane in lanes 0..15 and V in lanes
+// 16..31; Q [W; 0] is applied RK_NB columns at a time.
+
+template <int RPL, int KB>
+struct RCfg {
+  static constexpr int ROWS = 32 * RPL;
+  static constexpr int WPC = RPL * KB <= 32 ? 2 : 1;  // warps (ops) per CTA
+  static constexpr int LDW = KB + 1;
+  // Sx | Sy (ROWS x KB reflectors) | Wx | Wy (KB x LDW) | tau_x | tau_y
+  static constexpr int PER = 2 * ROWS * KB + 2 * KB * LDW + 2 * KB;
+  static size_t smem() { return (size_t)WPC * PER * sizeof(double); }
+};
+
+template <int RPL, int KB>
+__device__ __forceinline__ void r_load(const PartInfo *P, int np, bool left, int M, int K, double (&x)[RPL][KB],
+                                       int l) {
+#pragma unroll
+  for (int j = 0; j < KB; ++j) {
+#pragma unroll
+    for (int q = 0; q < RPL; ++q) x[q][j] = (j < K && l + 32 * q < M) ? stacked(P, np, left, l + 32 * q, j) : 0.0;
+  }
+}
+
+// Householder step j (dlarfg conventions) on the register-resident factor;
+// columns >= K are zero and stay zero
+template <int RPL, int KB>
+__device__ __forceinline__ void r_qr_step(double (&x)[RPL][KB], double &tau_j, int j, int l) {
+  const double x0 = x[0][j];
+  double ss = l > j ? x0 * x0 : 0.0;
+#pragma unroll
+  for (int q = 1; q < RPL; ++q) ss = fma(x[q][j], x[q][j], ss);
+  ss = warp_sum(ss);
+  const double alpha = __shfl_sync(0xffffffffu, x0, j);
+  double tj = 0.0, beta = alpha, sc = 0.0;
+  if (ss != 0.0) {
+    const double n2 = fma(alpha, alpha, ss);
+    const double rn = fast_rsqrt(n2);
+    beta = -copysign(n2 * rn, alpha);
+    tj = fma(fabs(alpha), rn, 1.0);
+    sc = fast_rcp(alpha - beta);
+  }
+  double v[RPL];
+  v[0] = l > j ? x0 * sc : (l == j ? 1.0 : 0.0);
+#pragma unroll
+  for (int q = 1; q < RPL; ++q) v[q] = x[q][j] * sc;
+  x[0][j] = l > j ? v[0] : (l == j ? beta : x0);
+#pragma unroll
+  for (int q = 1; q < RPL; ++q) x[q][j] = v[q];
+  tau_j = tj;
+  double p[KB];
+#pragma unroll
+  for (int c = j + 1; c < KB; ++c) {
+    p[c] = v[0] * x[0][c];
+#pragma unroll
+    for (int q = 1; q < RPL; ++q) p[c] = fma(v[q], x[q][c], p[c]);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+    for (int c = j + 1; c < KB; ++c) p[c] += __shfl_xor_sync(0xffffffffu, p[c], o);
+  }
+#pragma unroll
+  for (int c = j + 1; c < KB; ++c) {
+    const double f = tj * p[c];
+#pragma unroll
+    for (int q = 0; q < RPL; ++q) x[q][c] -= f * v[q];
+  }
+}
+
+template <int RPL, int KB>
+__device__ __forceinline__ void r_store(const double (&x)[RPL][KB], const double (&ta)[KB], double *S, double *tau,
+                                        int l) {
+  constexpr int ROWS = 32 * RPL;
+#pragma unroll
+  for (int j = 0; j < KB; ++j) {
+#pragma unroll
+    for (int q = 0; q < RPL; ++q) S[l + 32 * q + ROWS * j] = x[q][j];
+  }
+  if (l == 0) {
+#pragma unroll
+    for (int j = 0; j < KB; ++j) tau[j] = ta[j];
+  }
+}
+
+// Q [W_sel; 0] for one factor (rows l + 32 q of lane l), RK_NB columns at a time
+template <int RPL, int KB>
+__device__ __forceinline__ void r_apply(const double *S, const double *tau, const double *W, const int *perm, int K,
+                                        int kk, int M, double *out, int l) {
+  constexpr int ROWS = 32 * RPL, LDW = KB + 1;
+  for (int c0 = 0; c0 < kk; c0 += RK_NB) {
+    double a[RPL][RK_NB];
+#pragma unroll
+    for (int q = 0; q < RK_NB; ++q) {
+      const bool ok = c0 + q < kk && l < K;
+      a[0][q] = ok ? W[perm[min(c0 + q, KB - 1)] * LDW + l] : 0.0;
+#pragma unroll
+      for (int r = 1; r < RPL; ++r) a[r][q] = 0.0;
+    }
+    for (int j = K - 1; j >= 0; --j) {
+      const double tj = tau[j];
+      double v[RPL];
+      v[0] = l > j ? S[l + ROWS * j] : (l == j ? 1.0 : 0.0);
+#pragma unroll
+      for (int r = 1; r < RPL; ++r) v[r] = S[l + 32 * r + ROWS * j];
+      double p[RK_NB];
+#pragma unroll
+      for (int q = 0; q < RK_NB; ++q) {
+        p[q] = v[0] * a[0][q];
+#pragma unroll
+        for (int r = 1; r < RPL; ++r) p[q] = fma(v[r], a[r][q], p[q]);
+      }
+#pragma unroll
+      for (int o2 = 16; o2 > 0; o2 >>= 1) {
+#pragma unroll
+        for (int q = 0; q < RK_NB; ++q) p[q] += __shfl_xor_sync(0xffffffffu, p[q], o2);
+      }
+#pragma unroll
+      for (int q = 0; q < RK_NB; ++q) {
+        const double f = tj * p[q];
+#pragma unroll
+        for (int r = 0; r < RPL; ++r) a[r][q] -= f * v[r];
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < RK_NB; ++q) {
+      if (c0 + q < kk) {
+        const int64_t cq = c0 + q;
+#pragma unroll
+        for (int r = 0; r < RPL; ++r)
+          if (l + 32 * r < M) out[l + 32 * r + cq * M] = a[r][q];
+      }
+    }
+  }
+}
+
+// Core of a small truncation, one warp, KB in {8, 16}: M = R_x R_y^T
+// (R_x(i, t) = Rx[i + t ldx], R_y(c, t) = Ry[c + t ldy], upper triangular,
+// K x K), its SVD by one-sided Jacobi with column c of M in lane c and column
+// c of V in lane 16 + c (a round is one partner exchange by shuffles; the
+// lower-indexed lane of a pair computes the rotation), the rank decision, and
+// W_x = (U S) columns, W_y = V columns (ld KB+1, shared memory) with perm the
+// descending order.  Returns kk.
+template <int KB>
+__device__ int r_core(const double *Rx, int ldx, const double *Ry, int ldy, int K, const hlu_ctx &c, int cap,
+                      double *Wx, double *Wy, int *perm, int l) {
+  constexpr int LDW = KB + 1;
+  const int hl = l & 15;
+  const bool isV = l >= 16;
+  double col[KB];
+  {
+    double ry[KB];
+#pragma unroll
+    for (int t = 0; t < KB; ++t) ry[t] = (t >= hl && hl < K && t < K) ? Ry[hl + t * ldy] : 0.0;
+#pragma unroll
+    for (int i = 0; i < KB; ++i) {
+      double acc = 0.0;
+#pragma unroll
+      for (int t = i; t < KB; ++t)
+        if (t < K) acc = fma(Rx[i + t * ldx], ry[t], acc);
+      col[i] = isV ? (i == hl ? 1.0 : 0.0) : (i < K ? acc : 0.0);
+    }
+  }
+  if (K >= 2) {
+    const int qq = K + (K & 1), n1 = qq - 1;
+    for (int sweep = 0; sweep < 40; ++sweep) {
+      // largest squared column norm: pairs of columns both below 1e-15 of it
+      // (rounding noise of rotations against large columns) do not keep the
+      // sweep loop alive
+      double cmax = 0.0;
+      if (!isV) {
+#pragma unroll
+        for (int i = 0; i < KB; ++i) cmax = fma(col[i], col[i], cmax);
+      }
+      cmax = 1e-30 * warp_max(cmax);
+      int big = 0;
+      int pos = hl;  // circle-method position of column hl (round 0: identity)
+      for (int r = 0; r < n1; ++r) {
+        const int pp = n1 - pos;
+        int pc = pp - 1 + r;
+        pc = pp == 0 ? 0 : 1 + (pc >= n1 ? pc - n1 : pc);
+        const bool act = hl < K && pc < K;
+        const int src = (l & 16) | (act ? pc : hl);
+        const bool is_a = hl < pc;
+        double pcol[KB];
+#pragma unroll
+        for (int i = 0; i < KB; ++i) pcol[i] = __shfl_sync(0xffffffffu, col[i], src);
+        double cs = 1.0, sn = 0.0;
+        int rot = 0;
+        if (!isV && act && is_a) {
+          double a4[4] = {0.0, 0.0, 0.0, 0.0}, b4[4] = {0.0, 0.0, 0.0, 0.0}, g4[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+          for (int i = 0; i < KB; ++i) {
+            a4[i & 3] = fma(col[i], col[i], a4[i & 3]);
+            b4[i & 3] = fma(pcol[i], pcol[i], b4[i & 3]);
+            g4[i & 3] = fma(col[i], pcol[i], g4[i & 3]);
+          }
+          const double al = (a4[0] + a4[1]) + (a4[2] + a4[3]);
+          const double be = (b4[0] + b4[1]) + (b4[2] + b4[3]);
+          const double ga = (g4[0] + g4[1]) + (g4[2] + g4[3]);
+          const double g2 = ga * ga, ab = al * be;
+          if (ga != 0.0 && g2 > 1e-30 * ab) {
+            rot = 1;
+            if (g2 > 1e-16 * ab && fmax(al, be) > cmax) big = 1;
+            // t = tan(theta) = 2 ga / (d + sign(d) sqrt(d^2 + 4 ga^2)), d = be - al
+            const double dd = be - al;
+            const double q2 = fma(dd, dd, 4.0 * g2);
+            const double rq = q2 * fast_rsqrt(q2);
+            const double t = 2.0 * ga * fast_rcp(dd + copysign(rq, dd));
+            cs = fast_rsqrt(fma(t, t, 1.0));
+            sn = cs * t;
+          }
+        }
+        // b lanes take the rotation of their pair's a lane, V lanes that of their column
+        const int from = (!isV && act && !is_a) ? src : l;
+        cs = __shfl_sync(0xffffffffu, cs, from);
+        sn = __shfl_sync(0xffffffffu, sn, from);
+        rot = __shfl_sync(0xffffffffu, rot, from);
+        cs = __shfl_sync(0xffffffffu, cs, hl);
+        sn = __shfl_sync(0xffffffffu, sn, hl);
+        rot = __shfl_sync(0xffffffffu, rot, hl);
+        if (rot) {
+          // a: cs x_a - sn y_b ; b: sn x_a + cs y_b  (own, partner)
+          const double s2 = is_a ? -sn : sn;
+#pragma unroll
+          for (int i = 0; i < KB; ++i) col[i] = fma(s2, pcol[i], cs * col[i]);
+        }
+        pos = pos == 0 ? 0 : (pos == 1 ? n1 : pos - 1);
+      }
+      if (!__any_sync(0xffffffffu, big)) {
+        if (l == 0) atomicAdd(&g_sweeps, sweep + 1);
+        break;
+      }
+    }
+  }
+  // singular values (lanes 0..K-1), descending order, rank
+  double sg = 0.0;
+  if (!isV && hl < K) {
+    double ss = 0.0;
+#pragma unroll
+    for (int i = 0; i < KB; ++i) ss = fma(col[i], col[i], ss);
+    sg = sqrt(ss);
+  }
+  {
+    int rk = 0;
+    for (int i = 0; i < K; ++i) {
+      const double si = __shfl_sync(0xffffffffu, sg, i);
+      rk += (si > sg) || (si == sg && i < hl);
+    }
+    if (!isV && hl < K) perm[rk] = hl;
+  }
+  __syncwarp();
+  const double s1 = __shfl_sync(0xffffffffu, sg, perm[0]);
+  int kk = 0;
+  if (s1 != 0.0) kk = __popc(__ballot_sync(0xffffffffu, !isV && hl < K && sg > c.eps * s1));
+  if (c.kmax >= 0) kk = min(kk, c.kmax);
+  if (kk > cap) {
+    if (l == 0) atomicAdd(&c.err[0], 1);
+    kk = cap;
+  }
+  {
+    double *Wd = isV ? Wy : Wx;
+    if (hl < KB) {
+#pragma unroll
+      for (int i = 0; i < KB; ++i) Wd[hl * LDW + i] = col[i];
+    }
+  }
+  __syncwarp();
+  return kk;
+}
+
+template <int RPL, int KB>
+__device__ void r_trunc(const hlu_ctx &c, const hlu_rkt_desc &o, const hlu_rkpart *parts, PartInfo *P, double *sw,
+                        int *perm, int l) {
+  using Cfg = RCfg<RPL, KB>;
+  constexpr int ROWS = Cfg::ROWS, LDW = Cfg::LDW;
+  double *Sx = sw;
+  double *Sy = Sx + ROWS * KB;
+  double *Wx = Sy + ROWS * KB;
+  double *Wy = Wx + KB * LDW;
+  double *tx = Wy + KB * LDW;
+  double *ty = tx + KB;
+  const int np = min(o.part_count, RK_MAXP);
+  if (l < np) {
+    const hlu_rkpart q = parts[o.part_begin + l];
+    P[l].a = resolve(c, q.a);
+    P[l].b = resolve(c, q.b);
+    P[l].sign = q.sign;
+    P[l].roff = q.roff;
+    P[l].coff = q.coff;
+    P[l].k = P[l].a.cols;
+  }
+  __syncwarp();
+  if (l == 0) {
+    int col = 0;
+    for (int p = 0; p < np; ++p) {
+      P[p].col0 = col;
+      col += P[p].k;
+    }
+  }
+  __syncwarp();
+  bool shortcut;
+  const int K = logged_K(c, o, &shortcut);
+  const int m = o.m, n = o.n;
+  if (RPL == 2) {  // X and Y interleaved
+    double x[RPL][KB], y[RPL][KB], tax[KB], tay[KB];
+    r_load<RPL, KB>(P, np, true, m, K, x, l);
+    r_load<RPL, KB>(P, np, false, n, K, y, l);
+#pragma unroll
+    for (int j = 0; j < KB; ++j) {
+      tax[j] = 0.0;
+      tay[j] = 0.0;
+      if (j < K) {
+        r_qr_step<RPL, KB>(x, tax[j], j, l);
+        r_qr_step<RPL, KB>(y, tay[j], j, l);
+      }
+    }
+    r_store<RPL, KB>(x, tax, Sx, tx, l);
+    r_store<RPL, KB>(y, tay, Sy, ty, l);
+  } else {
+#pragma unroll 1
+    for (int side = 0; side < 2; ++side) {
+      double x[RPL][KB], ta[KB];
+      r_load<RPL, KB>(P, np, side == 0, side == 0 ? m : n, K, x, l);
+#pragma unroll
+      for (int j = 0; j < KB; ++j) {
+        ta[j] = 0.0;
+        if (j < K) r_qr_step<RPL, KB>(x, ta[j], j, l);
+      }
+      r_store<RPL, KB>(x, ta, side == 0 ? Sx : Sy, side == 0 ? tx : ty, l);
+    }
+  }
+  __syncwarp();
+  const int kk = r_core<KB>(Sx, ROWS, Sy, ROWS, K, c, o.cap, Wx, Wy, perm, l);
+  // B' = Q_y [V_sel; 0], A' = Q_x [(U S)_sel; 0]
+  r_apply<RPL, KB>(Sy, ty, Wy, perm, K, kk, n, c.pool + o.out_b, l);
+  r_apply<RPL, KB>(Sx, tx, Wx, perm, K, kk, m, c.pool + o.out_a, l);
+  if (l == 0) {
+    c.ranks[o.out_slot] = kk;
+    c.log[o.log + 2] = kk;
+  }
+}
+
+template <int RPL, int KB>
+__global__ void __launch_bounds__(RCfg<RPL, KB>::WPC * 32)
+    k_rkt_r(hlu_ctx c, const hlu_rkt_desc *__restrict__ d, const hlu_rkpart *__restrict__ parts, hlu_rkt_scratch s,
+            int slot) {
+  using Cfg = RCfg<RPL, KB>;
+  constexpr int WPC = Cfg::WPC;
+  constexpr int SEG = RPL == 2 ? (KB == 8 ? RK_SEG_R8 : RK_SEG_R16) : (KB == 8 ? RK_SEG_Q8 : RK_SEG_Q16);
+  extern __shared__ double sm[];
+  __shared__ PartInfo P[WPC][RK_MAXP];
+  __shared__ int perm[WPC][KB];
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  const int n = s.counts[RK_CNT * slot + SEG];
+  const int32_t *lst = s.list + SEG * s.max_ops;
+  for (int idx = blockIdx.x * WPC + w; idx < n; idx += gridDim.x * WPC) {
+    const hlu_rkt_desc o = d[lst[idx]];
+    r_trunc<RPL, KB>(c, o, parts, P[w], sm + w * Cfg::PER, perm[w], l);
+    __syncwarp();
+  }
+}
+
+// ---------------------------------------------------------------- phase A
+
+__device__ void rkt_a_item(const hlu_ctx &c, const hlu_rkt_desc *d, const hlu_rkpart *parts, const hlu_rkt_item it,
+                           double *S, double *tau, PartInfo *P) {
+  const hlu_rkt_desc o = d[it.op];
+  const int tid = threadIdx.x;
+  const int np = load_parts(c, o, parts, P);
+  bool shortcut;
+  const int K = logged_K(c, o, &shortcut);
+  const bool left = it.side == 0;
+  const int M = left ? o.m : o.n;
+  const rk_side_t sa = rk_side(o.m, K);
+  const rk_side_t s = left ? sa : rk_side(o.n, K);
+  double *ws = c.pool + o.ws + (left ? 0 : sa.total);
+  const int row0 = it.block * RK_BR;
+  const int rows = min(RK_BR, M - row0);
+  const Grp all{0, HLU_NWARP, tid >> 5, tid & 31, tid};
+  const PartsSrc src{P, np, left, row0};
+  const int r = tsqr_chain(src, rows, K, s.ch, S, tau, ws + it.block * s.blk, all);
+  // the block's R: K x K, ld K, zero outside the upper triangle of its r rows
+  double *R = ws + s.off_R + (int64_t)it.block * K * K;
+  const int ld = s.ch + K;
+  for (int e = tid; e < K * K; e += HLU_NT) {
+    const int i = e % K, j = e / K;
+    R[e] = (i < r && i <= j) ? S[i + j * ld] : 0.0;
+  }
+}
+
+__global__ void __launch_bounds__(HLU_NT)
+    k_rkt_a(hlu_ctx c, const hlu_rkt_desc *__restrict__ d, const hlu_rkpart *__restrict__ parts, hlu_rkt_scratch s,
+            int slot) {
+  extern __shared__ double sm[];
+  __shared__ PartInfo P[RK_MAXP];
+  const int nitems = s.counts[RK_CNT * slot + RK_CNT_ITEMS];
+  for (int idx = blockIdx.x; idx < nitems; idx += gridDim.x) {
+    rkt_a_item(c, d, parts, s.items[idx], sm, sm + RK_BUFA, P);
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------- phase B
+
+template <int KM>
+struct RkB {
+  static constexpr int BUF = KM == 32 ? RK_BUFB32 : RK_BUFB64;
+  static constexpr int NT = KM == 32 ? 256 : 512;  // threads (the K > 32 core: one Jacobi pair per 16 lanes)
+  static size_t smem() { return (size_t)(2 * BUF + 2 * KM * KM + 3 * KM) * sizeof(double); }
+};
+
+template <int KM>
+__global__ void __launch_bounds__(RkB<KM>::NT)
+    k_rkt_b(hlu_ctx c, const hlu_rkt_desc *__restrict__ d, const hlu_rkpart *__restrict__ parts, hlu_rkt_scratch sc,
+            int slot) {
+  constexpr int BUF = RkB<KM>::BUF, NT = RkB<KM>::NT, NW = NT / 32;
+  extern __shared__ double sm[];
+  double *B0 = sm;              // BUF   side-A buffer, later G | V
+  double *B1 = B0 + BUF;        // BUF   side-B buffer, later XT
+  double *RA = B1 + BUF;        // KM*KM R_a, later W_a
+  double *RB = RA + KM * KM;    // KM*KM R_b, later W_b
+  double *tau = RB + KM * KM;   // KM
+  double *tau1 = tau + KM;      // KM
+  double *sig = tau1 + KM;      // KM
+  double *G = B0, *V = B0 + KM * KM, *XT = B1;
+  __shared__ PartInfo P[RK_MAXP];
+  __shared__ int perm[KM];
+  __shared__ int cmap[KM];
+  __shared__ unsigned char pairs_a[(KM - 1) * (KM / 2)], pairs_b[(KM - 1) * (KM / 2)];
+  __shared__ int s_kk, s_ra, s_rb;
+  const int tid = threadIdx.x, wq = tid >> 5;
+  const int nbig = sc.counts[RK_CNT * slot + RK_SEG_BIG];
+  const int32_t *lbig = sc.list + RK_SEG_BIG * sc.max_ops;
+  for (int idx = blockIdx.x; idx < nbig; idx += gridDim.x) {
+    const hlu_rkt_desc o = d[lbig[idx]];
+    bool shortcut;
+    const int K = logged_K(c, o, &shortcut);
+    const int m = o.m, n = o.n;
+    double *outA = c.pool + o.out_a;
+    double *outB = c.pool + o.out_b;
+    if (shortcut) {
+      if (KM != 32) continue;
+      load_parts(c, o, parts, P);
+      const PartInfo &src = (P[1].k == 0) ? P[0] : P[1];
       int kk = src.k;
       if (kk > o.cap) {
         if (tid == 0) atomicAdd(&c.err[0], 1);
@@ -536,167 +1381,393 @@ __global__ void __launch_bounds__(HLU_NT)
       const bool alias = (src.a.p == outA && src.a.rs == 1 && src.a.cs == m && src.b.p == outB &&
                           src.b.rs == 1 && src.b.cs == n && src.sign == 1.0);
       if (!alias) {
-        for (int e = tid; e < m * kk; e += HLU_NT) outA[e] = src.sign * src.a.get(e % m, e / m);
-        for (int e = tid; e < n * kk; e += HLU_NT) outB[e] = src.b.get(e % n, e / n);
+        for (int e = tid; e < m * kk; e += NT) outA[e] = src.sign * src.a.get(e % m, e / m);
+        for (int e = tid; e < n * kk; e += NT) outB[e] = src.b.get(e % n, e / n);
       }
       if (tid == 0) {
         c.ranks[o.out_slot] = kk;
-        if (o.log >= 0) c.log[o.log + 2] = kk;
+        c.log[o.log + 2] = kk;
       }
-      return;
-    }
-  } else {
-    if (tid == 0 && o.log >= 0) {
-      c.log[o.log] = K;
-      c.log[o.log + 1] = 0;
+      __syncthreads();
+      continue;
     }
     if (K == 0) {
-      if (tid == 0) {
+      if (KM == 32 && tid == 0) {
         c.ranks[o.out_slot] = 0;
-        if (o.log >= 0) c.log[o.log + 2] = 0;
+        c.log[o.log + 2] = 0;
       }
-      return;
+      continue;
     }
-  }
-  if (K > KM) {  // only reachable in the KM=64 variant
-    if (tid == 0) atomicAdd(&c.err[2], 1);
-    return;
-  }
-  PHASE(0)
-  double *wsA = c.pool + o.ws;
-  double *wsB = wsA + rk_ws_one(m, K, Cfg::CH);
-  // A/B. TSQR of both stacked factors, concurrently on two warp groups
-  const int wq = tid >> 5;
-  const Grp grp{1 + (wq >= HLU_NWARP / 2), HLU_NWARP / 2, wq % (HLU_NWARP / 2), tid & 31, tid % (HLU_NT / 2)};
-  __shared__ int s_ra, s_rb;
-  if (wq < HLU_NWARP / 2) {
-    const int r_ = tsqr<KM>(P, np, true, m, K, S, RA, tau, wsA, grp);
-    if (grp.t == 0) s_ra = r_;
-  } else {
-    const int r_ = tsqr<KM>(P, np, false, n, K, S1, RB, tau1, wsB, grp);
-    if (grp.t == 0) s_rb = r_;
-  }
-  __syncthreads();
-  const int ra = s_ra, rb = s_rb;
-  PHASE(1)
-  // C. core M = R_a R_b^T (ra x rb); G = M or M^T so that G has q <= p columns
-  const bool tr = rb > ra;
-  const int p = tr ? rb : ra, q = tr ? ra : rb;
-  double *G = S;
-  double *V = S + KM * KM;
-  for (int e = tid; e < ra * rb; e += HLU_NT) {
-    const int i = e % ra, j = e / ra;
-    double acc = 0.0;
-    for (int t = max(i, j); t < K; ++t) acc += RA[i + t * KM] * RB[j + t * KM];
-    // R_a[i,t] = 0 for t < i and R_b[j,t] = 0 for t < j
-    if (tr) G[j + i * KM] = acc;
-    else G[i + j * KM] = acc;
-  }
-  __syncthreads();
-  // D. SVD of G via QR with column pivoting + one-sided Jacobi on R^T
-  //    (G P = Q R, R^T V = W = U S  =>  G = (Q V) S (P U)^T)
-  PHASE(2)
-  qrcp<KM>(G, p, q, tau, cmap, sig);
-  PHASE(3)
-  for (int e = tid; e < KM * KM; e += HLU_NT) {
-    const int i = e % KM, j = e / KM;  // XT[i, j] = R[j, i]
-    XT[e] = (i < q && j < q && j <= i) ? G[j + cmap[i] * KM] : 0.0;
-  }
-  const int qq = q + (q & 1);
-  build_pairs(pairs_a, pairs_b, qq);
-  __syncthreads();
-  PHASE(4)
-  jacobi<KM>(XT, V, q, pairs_a, pairs_b);
-  PHASE(5)
-  // E. singular values, order, rank
-  for (int j = tid; j < q; j += HLU_NT) {
-    double ss = 0.0;
-    for (int i = 0; i < q; ++i) ss = fma(XT[i + j * KM], XT[i + j * KM], ss);
-    sig[j] = sqrt(ss);
-  }
-  __syncthreads();
-  for (int j = tid; j < q; j += HLU_NT) {
-    int rk = 0;
-    const double sj = sig[j];
-    for (int i = 0; i < q; ++i) rk += (sig[i] > sj) || (sig[i] == sj && i < j);
-    perm[rk] = j;
-  }
-  __syncthreads();
-  if (tid == 0) {
-    const double s1 = sig[perm[0]];
-    int kk = 0;
-    if (s1 != 0.0) {
-      const double thr = c.eps * s1;
-      for (int i = 0; i < q; ++i) kk += sig[i] > thr;
+    if ((KM == 32) != (K <= 32)) continue;
+    if (K <= 16 && m <= RK_BR && n <= RK_BR) continue;  // k_rkt_bw
+    const rk_side_t sa = rk_side(m, K), sb = rk_side(n, K);
+    double *wsA = c.pool + o.ws;
+    double *wsB = wsA + sa.total;
+    // R of each factor, concurrently on two warp groups: the block's R, or the
+    // QR of the stacked block R's
+    const Grp grp{1 + (wq >= NW / 2), NW / 2, wq % (NW / 2), tid & 31, tid % (NT / 2)};
+    {
+      const bool left = wq < NW / 2;
+      const rk_side_t &s = left ? sa : sb;
+      double *ws = left ? wsA : wsB;
+      double *buf = left ? B0 : B1;
+      double *R = left ? RA : RB;
+      double *tg = left ? tau : tau1;
+      const int M = left ? m : n;
+      int r;
+      if (s.nb == 1) {
+        r = min(M, K);
+        const double *R1 = ws + s.off_R;
+        for (int e = grp.t; e < KM * KM; e += grp.nt()) {
+          const int i = e % KM, j = e / KM;
+          R[e] = (i < K && j < K) ? R1[i + j * K] : 0.0;
+        }
+      } else {
+        const StackedR src{ws + s.off_R, K};
+        r = tsqr_chain(src, s.srows, K, s.chc, buf, tg, ws + s.off_comb, grp);
+        const int ld = s.chc + K;
+        for (int e = grp.t; e < KM * KM; e += grp.nt()) {
+          const int i = e % KM, j = e / KM;
+          R[e] = (i < r && i <= j && j < K) ? buf[i + j * ld] : 0.0;
+        }
+      }
+      if (grp.t == 0) (left ? s_ra : s_rb) = r;
     }
-    if (c.kmax >= 0) kk = min(kk, c.kmax);
-    if (kk > o.cap) {
-      atomicAdd(&c.err[0], 1);
-      kk = o.cap;
+    __syncthreads();
+    const int ra = s_ra, rb = s_rb;
+    // core M = R_a R_b^T (ra x rb); G = M or M^T so that G has q <= p columns
+    const bool tr = rb > ra;
+    const int p = tr ? rb : ra, q = tr ? ra : rb;
+    for (int e = tid; e < ra * rb; e += NT) {
+      const int i = e % ra, j = e / ra;
+      double acc = 0.0;
+      for (int t = max(i, j); t < K; ++t) acc += RA[i + t * KM] * RB[j + t * KM];
+      // R_a[i,t] = 0 for t < i and R_b[j,t] = 0 for t < j
+      if (tr) G[j + i * KM] = acc;
+      else G[i + j * KM] = acc;
     }
-    s_kk = kk;
-  }
-  __syncthreads();
-  const int kk = s_kk;
-  // F. W_a (ra x kk) -> RA, W_b (rb x kk) -> RB.
-  //   G = M  (!tr): W_a = Q (V S)_sel,  W_b = P W_sel / S
-  //   G = M^T (tr): W_a = P W_sel,      W_b = Q V_sel
-  double *WQ = tr ? RB : RA;  // the side that needs Q applied
-  double *WP = tr ? RA : RB;  // the permuted side
-  for (int e = tid; e < KM * kk; e += HLU_NT) {
-    const int i = e % KM, cidx = e / KM;
-    const int j = perm[cidx];
-    WQ[i + cidx * KM] = (i < q) ? (tr ? V[i + j * KM] : V[i + j * KM] * sig[j]) : 0.0;
-    if (i < q) WP[cmap[i] + cidx * KM] = tr ? XT[i + j * KM] : XT[i + j * KM] / sig[j];
-  }
-  for (int e = tid; e < (KM - q) * kk; e += HLU_NT) {  // rows >= q of the permuted side
-    const int i = q + e % (KM - q), cidx = e / (KM - q);
-    WP[i + cidx * KM] = 0.0;
-  }
-  __syncthreads();
-  for (int col = tid >> 5; col < kk; col += HLU_NWARP) qrcp_apply<KM>(G, p, q, tau, cmap, WQ + col * KM);
-  __syncthreads();
-  PHASE(6)
-  const Grp all{0, HLU_NWARP, wq, tid & 31, tid};
-  apply_q<KM>(m, K, kk, RA, S, S1, tau, wsA, outA, all);
-  apply_q<KM>(n, K, kk, RB, S, S1, tau, wsB, outB, all);
-  PHASE(7)
-  if (tid == 0) {
-    c.ranks[o.out_slot] = kk;
-    if (o.log >= 0) c.log[o.log + 2] = kk;
+    __syncthreads();
+    // SVD of G via QR with column pivoting + one-sided Jacobi on R^T
+    // (G P = Q R, R^T V = W = U S  =>  G = (Q V) S (P U)^T)
+    qrcp<KM, NT>(G, p, q, tau, cmap, sig);
+    for (int e = tid; e < KM * KM; e += NT) {
+      const int i = e % KM, j = e / KM;  // XT[i, j] = R[j, i]
+      XT[e] = (i < q && j < q && j <= i) ? G[j + cmap[i] * KM] : 0.0;
+    }
+    const int qq = q + (q & 1);
+    build_pairs<NT>(pairs_a, pairs_b, qq);
+    __syncthreads();
+    jacobi<KM, NT>(XT, V, q, pairs_a, pairs_b);
+    // singular values, order, rank
+    for (int j = tid; j < q; j += NT) {
+      double ss = 0.0;
+      for (int i = 0; i < q; ++i) ss = fma(XT[i + j * KM], XT[i + j * KM], ss);
+      sig[j] = sqrt(ss);
+    }
+    __syncthreads();
+    for (int j = tid; j < q; j += NT) {
+      int rk = 0;
+      const double sj = sig[j];
+      for (int i = 0; i < q; ++i) rk += (sig[i] > sj) || (sig[i] == sj && i < j);
+      perm[rk] = j;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      const double s1 = sig[perm[0]];
+      int kk = 0;
+      if (s1 != 0.0) {
+        const double thr = c.eps * s1;
+        for (int i = 0; i < q; ++i) kk += sig[i] > thr;
+      }
+      if (c.kmax >= 0) kk = min(kk, c.kmax);
+      if (kk > o.cap) {
+        atomicAdd(&c.err[0], 1);
+        kk = o.cap;
+      }
+      s_kk = kk;
+    }
+    __syncthreads();
+    const int kk = s_kk;
+    // W_a (ra x kk) -> RA, W_b (rb x kk) -> RB.
+    //   G = M  (!tr): W_a = Q (V S)_sel,  W_b = P W_sel / S
+    //   G = M^T (tr): W_a = P W_sel,      W_b = Q V_sel
+    double *WQ = tr ? RB : RA;  // the side that needs Q applied
+    double *WP = tr ? RA : RB;  // the permuted side
+    for (int e = tid; e < KM * kk; e += NT) {
+      const int i = e % KM, cidx = e / KM;
+      const int j = perm[cidx];
+      WQ[i + cidx * KM] = (i < q) ? (tr ? V[i + j * KM] : V[i + j * KM] * sig[j]) : 0.0;
+      if (i < q) WP[cmap[i] + cidx * KM] = tr ? XT[i + j * KM] : XT[i + j * KM] / sig[j];
+    }
+    for (int e = tid; e < (KM - q) * kk; e += NT) {  // rows >= q of the permuted side
+      const int i = q + e % (KM - q), cidx = e / (KM - q);
+      WP[i + cidx * KM] = 0.0;
+    }
+    __syncthreads();
+    for (int col = wq; col < kk; col += NW) qrcp_apply<KM>(G, p, q, tau, cmap, WQ + col * KM);
+    __syncthreads();
+    // Z = combine-level Q [W; 0] (or W itself for a single-block factor)
+    {
+      const bool left = wq < NW / 2;
+      const rk_side_t &s = left ? sa : sb;
+      double *ws = left ? wsA : wsB;
+      double *buf = left ? B0 : B1;
+      const double *W = left ? RA : RB;
+      double *tg = left ? tau : tau1;
+      const int r = left ? ra : rb;
+      double *Z = ws + s.off_Z;
+      if (s.nb == 1) {
+        for (int e = grp.t; e < r * kk; e += grp.nt()) {
+          const int i = e % r, j = e / r;
+          Z[i + (int64_t)j * s.zrows] = W[i + j * KM];
+        }
+      } else {
+        apply_chain<false>(s.srows, K, s.chc, kk, W, KM, r, buf, nullptr, tg, ws + s.off_comb, Z, s.zrows, grp);
+      }
+    }
+    if (tid == 0) {
+      c.ranks[o.out_slot] = kk;
+      c.log[o.log + 2] = kk;
+    }
+    __syncthreads();
   }
 }
 
-template <int KM>
-static size_t rkt_smem() {
-  return (size_t)(2 * RkCfg<KM>::BUFD + 2 * KM * KM + 3 * KM) * sizeof(double);
+// ---------------------------------------------------------------- phase B, one warp per op
+
+// CTA-path ops with K <= 16 and single-block factors: the core SVD of the two
+// block R's by r_core, Z = W written for phase C.
+template <int KB>
+struct BwCfg {
+  static constexpr int WPC = 4;
+  static constexpr int LDW = KB + 1;
+  static constexpr int PER = 2 * KB * KB + 2 * KB * LDW;  // Rx | Ry | Wx | Wy
+  static size_t smem() { return (size_t)WPC * PER * sizeof(double); }
+};
+
+template <int KB>
+__global__ void __launch_bounds__(BwCfg<KB>::WPC * 32)
+    k_rkt_bw(hlu_ctx c, const hlu_rkt_desc *__restrict__ d, hlu_rkt_scratch s, int slot) {
+  constexpr int WPC = BwCfg<KB>::WPC, LDW = BwCfg<KB>::LDW;
+  extern __shared__ double sm[];
+  __shared__ int perm[WPC][KB];
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  double *Rx = sm + w * BwCfg<KB>::PER;
+  double *Ry = Rx + KB * KB;
+  double *Wx = Ry + KB * KB;
+  double *Wy = Wx + KB * LDW;
+  const int n = s.counts[RK_CNT * slot + RK_SEG_C16];
+  const int32_t *lst = s.list + RK_SEG_C16 * s.max_ops;
+  for (int idx = blockIdx.x * WPC + w; idx < n; idx += gridDim.x * WPC) {
+    const hlu_rkt_desc o = d[lst[idx]];
+    bool shortcut;
+    const int K = logged_K(c, o, &shortcut);
+    const rk_side_t sa = rk_side(o.m, K), sb = rk_side(o.n, K);
+    double *wsA = c.pool + o.ws;
+    double *wsB = wsA + sa.total;
+    for (int e = l; e < K * K; e += 32) {
+      Rx[e] = wsA[sa.off_R + e];
+      Ry[e] = wsB[sb.off_R + e];
+    }
+    __syncwarp();
+    const int kk = r_core<KB>(Rx, K, Ry, K, K, c, o.cap, Wx, Wy, perm[w], l);
+    double *Za = wsA + sa.off_Z, *Zb = wsB + sb.off_Z;
+    for (int e = l; e < sa.zrows * kk; e += 32) {
+      const int i = e % sa.zrows, j = e / sa.zrows;
+      Za[e] = Wx[perm[w][j] * LDW + i];
+    }
+    for (int e = l; e < sb.zrows * kk; e += 32) {
+      const int i = e % sb.zrows, j = e / sb.zrows;
+      Zb[e] = Wy[perm[w][j] * LDW + i];
+    }
+    if (l == 0) {
+      c.ranks[o.out_slot] = kk;
+      c.log[o.log + 2] = kk;
+    }
+    __syncwarp();
+  }
+}
+
+// ---------------------------------------------------------------- phase C
+
+__global__ void __launch_bounds__(HLU_NT)
+    k_rkt_c(hlu_ctx c, const hlu_rkt_desc *__restrict__ d, hlu_rkt_scratch s, int slot) {
+  extern __shared__ double sm[];
+  double *T = sm;             // RK_BUFA moving block
+  double *VS = T + RK_BUFA;   // RK_BUFA staged reflectors
+  double *tq = VS + RK_BUFA;  // RK_KMAX
+  const int tid = threadIdx.x;
+  const int nitems = s.counts[RK_CNT * slot + RK_CNT_ITEMS];
+  for (int idx = blockIdx.x; idx < nitems; idx += gridDim.x) {
+    const hlu_rkt_item it = s.items[idx];
+    const hlu_rkt_desc o = d[it.op];
+    bool shortcut;
+    const int K = logged_K(c, o, &shortcut);
+    const int kk = c.log[o.log + 2];
+    if (kk <= 0) continue;
+    const bool left = it.side == 0;
+    const int M = left ? o.m : o.n;
+    const rk_side_t sa = rk_side(o.m, K);
+    const rk_side_t sd = left ? sa : rk_side(o.n, K);
+    const double *ws = c.pool + o.ws + (left ? 0 : sa.total);
+    const int row0 = it.block * RK_BR;
+    const int rows = min(RK_BR, M - row0);
+    const int rb = min(rows, K);
+    double *out = c.pool + (left ? o.out_a : o.out_b) + row0;
+    const Grp all{0, HLU_NWARP, tid >> 5, tid & 31, tid};
+    apply_chain<true>(rows, K, sd.ch, kk, ws + sd.off_Z + it.block * K, sd.zrows, rb, T, VS, tq,
+                      ws + it.block * sd.blk, out, M, all);
+  }
 }
 
 }  // namespace hlu
 
 using namespace hlu;
 
-__global__ void k_epoch_bump() { g_epoch += 1; }
+static size_t smem_a() { return (size_t)(RK_BUFA + RK_KMAX) * sizeof(double); }
+static size_t smem_c() { return (size_t)(2 * RK_BUFA + RK_KMAX) * sizeof(double); }
 
-extern "C" int hlu_epoch_bump(void *stream) {
-  k_epoch_bump<<<1, 1, 0, (cudaStream_t)stream>>>();
+static void rkt_init() {
+  static bool init = false;
+  if (init) return;
+  cudaFuncSetAttribute(k_rkt_a, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_a());
+  cudaFuncSetAttribute(k_rkt_b<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RkB<32>::smem());
+  cudaFuncSetAttribute(k_rkt_b<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RkB<64>::smem());
+  cudaFuncSetAttribute(k_rkt_c, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_c());
+  cudaFuncSetAttribute(k_rkt_r<2, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RCfg<2, 8>::smem());
+  cudaFuncSetAttribute(k_rkt_r<2, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RCfg<2, 16>::smem());
+  cudaFuncSetAttribute(k_rkt_r<4, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RCfg<4, 8>::smem());
+  cudaFuncSetAttribute(k_rkt_r<4, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RCfg<4, 16>::smem());
+  cudaFuncSetAttribute(k_rkt_w<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)WCfg<32>::smem());
+  cudaFuncSetAttribute(k_rkt_bw<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)BwCfg<16>::smem());
+  init = true;
+}
+
+// persistent grid of the register warp kernel: as many CTAs as fit on the GPU
+// (shared memory bound), never more than the ops could use
+template <int RPL, int KB>
+static void launch_r(const hlu_ctx *ctx, hlu_rkt_desc *d, const hlu_rkpart *parts, int count,
+                     const hlu_rkt_scratch &s, int slot, cudaStream_t st) {
+  using Cfg = RCfg<RPL, KB>;
+  const int per_sm = std::max<int>(1, std::min<int>(16 / Cfg::WPC, (int)(220 * 1024 / Cfg::smem())));
+  const int64_t want = (count + Cfg::WPC - 1) / Cfg::WPC;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, 148 * per_sm));
+  k_rkt_r<RPL, KB><<<grid, Cfg::WPC * 32, Cfg::smem(), st>>>(*ctx, d, parts, s, slot);
+}
+
+// kernels of one level: 0 classify, 1 register warp K<=8 (m,n <= 64 and <= 128), 2 the same K<=16,
+// 3 shared-memory warp K<=32, 4 block TSQR, 5 core by one warp (K<=16), 6 core K<=32,
+// 7 core K>32, 8 Q apply
+#define RK_NKERN 9
+static int rkt_launch(int which, const hlu_ctx *ctx, hlu_rkt_desc *d, const hlu_rkpart *parts, int64_t first,
+                      int count, const hlu_rkt_scratch &s, int slot, cudaStream_t st) {
+  const int cap = 148;
+  auto lim = [&](int64_t want, int per_sm) { return (int)std::max<int64_t>(1, std::min<int64_t>(want, cap * per_sm)); };
+  switch (which) {
+    case 0:
+      k_rkt_classify<<<(count + 127) / 128, 128, 0, st>>>(*ctx, d, parts, first, count, s, slot);
+      break;
+    case 1:
+      launch_r<2, 8>(ctx, d, parts, count, s, slot, st);
+      launch_r<4, 8>(ctx, d, parts, count, s, slot, st);
+      break;
+    case 2:
+      launch_r<2, 16>(ctx, d, parts, count, s, slot, st);
+      launch_r<4, 16>(ctx, d, parts, count, s, slot, st);
+      break;
+    case 3:
+      k_rkt_w<32><<<lim((count + 1) / 2, 3), 2 * 32, WCfg<32>::smem(), st>>>(*ctx, d, parts, s, slot);
+      break;
+    case 4: k_rkt_a<<<lim(2 * (int64_t)count, 4), HLU_NT, smem_a(), st>>>(*ctx, d, parts, s, slot); break;
+    case 5:
+      k_rkt_bw<16><<<lim((count + 3) / 4, 4), 4 * 32, BwCfg<16>::smem(), st>>>(*ctx, d, s, slot);
+      break;
+    case 6: k_rkt_b<32><<<lim(count, 3), RkB<32>::NT, RkB<32>::smem(), st>>>(*ctx, d, parts, s, slot); break;
+    case 7: k_rkt_b<64><<<lim(count, 1), RkB<64>::NT, RkB<64>::smem(), st>>>(*ctx, d, parts, s, slot); break;
+    case 8: k_rkt_c<<<lim(2 * (int64_t)count, 2), HLU_NT, smem_c(), st>>>(*ctx, d, s, slot); break;
+    default: return -3;
+  }
+  return 0;
+}
+
+__global__ void k_rkt_stamp(unsigned long long *slot) {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  *slot = t;
+}
+
+// diagnostics: when non-null, %globaltimer after every kernel of a level
+// (RK_NSTAMP slots: the RK_NKERN kernels, then the join)
+#define RK_NSTAMP 10
+static unsigned long long *g_phase_stamps = nullptr;
+extern "C" void hlu_rkt_set_phase_stamps(unsigned long long *p) { g_phase_stamps = p; }
+
+extern "C" int hlu_rkt_phases(const hlu_ctx *ctx, hlu_rkt_desc *d, const hlu_rkpart *parts, int64_t first,
+                              int count, const hlu_rkt_scratch *scratch, int slot, void *stream, void *side,
+                              void *ev_fork, void *ev_join) {
+  rkt_init();
+  if (count <= 0) return cudaGetLastError() == cudaSuccess ? 0 : -1;
+  cudaStream_t st = (cudaStream_t)stream, sd = (cudaStream_t)side;
+  const hlu_rkt_scratch &s = *scratch;
+  unsigned long long *ps = g_phase_stamps ? g_phase_stamps + RK_NSTAMP * (int64_t)slot : nullptr;
+  auto stamp = [&](int k, cudaStream_t q) {
+    if (ps) k_rkt_stamp<<<1, 1, 0, q>>>(ps + k);
+  };
+  rkt_launch(0, ctx, d, parts, first, count, s, slot, st);
+  stamp(0, st);
+  if (sd != st) {
+    cudaEventRecord((cudaEvent_t)ev_fork, st);
+    cudaStreamWaitEvent(sd, (cudaEvent_t)ev_fork, 0);
+  }
+  cudaStream_t ws = sd != st ? sd : st;
+  for (int w = 1; w <= 3; ++w) {
+    rkt_launch(w, ctx, d, parts, first, count, s, slot, ws);
+    stamp(w, ws);
+  }
+  if (sd != st) cudaEventRecord((cudaEvent_t)ev_join, sd);
+  for (int w = 4; w < RK_NKERN; ++w) {
+    rkt_launch(w, ctx, d, parts, first, count, s, slot, st);
+    stamp(w, st);
+  }
+  if (sd != st) cudaStreamWaitEvent(st, (cudaEvent_t)ev_join, 0);
+  stamp(RK_NKERN, st);
   return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }
 
-extern "C" int hlu_debug_phases(double *sum_out, double *max_out, int reset) {
-  unsigned long long a[10], b[10];
-  cudaMemcpyFromSymbol(a, g_phase, sizeof(a));
-  cudaMemcpyFromSymbol(b, g_phase_max, sizeof(b));
-  for (int i = 0; i < 10; ++i) {
-    sum_out[i] = (double)a[i];
-    max_out[i] = (double)b[i];
+extern "C" int hlu_rkt_phase(const hlu_ctx *ctx, hlu_rkt_desc *d, const hlu_rkpart *parts, int64_t first, int count,
+                             const hlu_rkt_scratch *scratch, int slot, int which, void *stream) {
+  rkt_init();
+  if (count <= 0) return 0;
+  const int rc = rkt_launch(which, ctx, d, parts, first, count, *scratch, slot, (cudaStream_t)stream);
+  if (rc != 0) return rc;
+  return cudaGetLastError() == cudaSuccess ? 0 : -1;
+}
+
+extern "C" int hlu_rk_update_batched_f64(const hlu_ctx *ctx, hlu_rkt_desc *d, const hlu_rkpart *parts, int count,
+                                         const hlu_rkt_scratch *scratch, void *stream) {
+  rkt_init();
+  if (count <= 0) return 0;
+  if (count > scratch->max_ops) return -4;
+  cudaMemsetAsync(scratch->counts, 0, RK_CNT * sizeof(int32_t), (cudaStream_t)stream);
+  return hlu_rkt_phases(ctx, d, parts, 0, count, scratch, 0, stream, stream, nullptr, nullptr);
+}
+
+extern "C" int64_t hlu_rkt_items(const hlu_rkt_desc *d, int count, hlu_rkt_item *items) {
+  int64_t n = 0;
+  for (int i = 0; i < count; ++i) {
+    for (int side = 0; side < 2; ++side) {
+      const int M = side ? d[i].n : d[i].m;
+      const int nb = (M + RK_BR - 1) / RK_BR;
+      for (int b = 0; b < nb; ++b, ++n) {
+        if (items) {
+          items[n].op = i;
+          items[n].side = (int16_t)side;
+          items[n].block = (int16_t)b;
+        }
+      }
+    }
   }
-  if (reset) {
-    unsigned long long z[10] = {0};
-    cudaMemcpyToSymbol(g_phase, z, sizeof(z));
-    cudaMemcpyToSymbol(g_phase_max, z, sizeof(z));
-  }
-  return 0;
+  return n;
 }
 
 extern "C" int64_t hlu_debug_sweeps(int reset) {
@@ -709,27 +1780,4 @@ extern "C" int64_t hlu_debug_sweeps(int reset) {
   return (int64_t)v;
 }
 
-extern "C" int64_t hlu_rkt_ws_doubles(int32_t m, int32_t kbound) {
-  // the variant that runs an op depends on its runtime K; take the larger need
-  const int k32 = kbound < 32 ? kbound : 32;
-  const int k64 = kbound < 64 ? kbound : 64;
-  const int64_t a = rk_ws_one(m, k32, RkCfg<32>::CH);
-  const int64_t b = rk_ws_one(m, k64, RkCfg<64>::CH);
-  return a > b ? a : b;
-}
-
-extern "C" int hlu_rk_update_batched_f64(const hlu_ctx *ctx, hlu_rkt_desc *d, const hlu_rkpart *parts,
-                                         int count, int kclass, void *stream) {
-  static bool init = false;
-  if (!init) {
-    cudaFuncSetAttribute(k_rkt<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rkt_smem<32>());
-    cudaFuncSetAttribute(k_rkt<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rkt_smem<64>());
-    init = true;
-  }
-  if (count <= 0) return 0;
-  if (kclass == 32)
-    k_rkt<32><<<count, HLU_NT, rkt_smem<32>(), (cudaStream_t)stream>>>(*ctx, d, parts);
-  else
-    k_rkt<64><<<count, HLU_NT, rkt_smem<64>(), (cudaStream_t)stream>>>(*ctx, d, parts);
-  return cudaGetLastError() == cudaSuccess ? 0 : -1;
-}
+extern "C" int64_t hlu_rkt_ws_doubles(int32_t m, int32_t n, int32_t kbound) { return rk_ws_doubles(m, n, kbound); }

@@ -5,12 +5,13 @@
 // hlu.py:315-354, runtime.py:330-817): the ordering the runtime enforced per
 // skeleton slot is encoded in the level numbers computed on the host.
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
 #include "common.cuh"
 
-extern "C" int hlu_epoch_bump(void *stream);
+extern "C" void hlu_rkt_set_phase_stamps(unsigned long long *p);
 
 struct hlu_schedule {
   hlu_ctx ctx;
@@ -23,30 +24,28 @@ struct hlu_schedule {
   const hlu_term *terms;
   hlu_rkt_desc *rkt;
   const hlu_rkpart *parts;
+  hlu_rkt_scratch scratch;
+  int nrkt;  // truncation launches (counter slots)
   cudaGraph_t graph;
   cudaGraphExec_t exec;
   bool use_graph;
+  unsigned long long *stamps;  // diagnostics: %globaltimer after every launch (HLU_STAMPS=1)
 };
 
+__global__ void k_stamp(unsigned long long *slot) {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  *slot = t;
+}
+
 static int run_launches(hlu_schedule *s, cudaStream_t st) {
-  int rc0 = hlu_epoch_bump(st);
-  if (rc0 != 0) return rc0;
   const size_t nl = s->launches.size();
+  if (s->stamps) k_stamp<<<1, 1, 0, st>>>(s->stamps);
+  if (s->nrkt) cudaMemsetAsync(s->scratch.counts, 0, 8 * sizeof(int32_t) * s->nrkt, st);
+  int slot = 0;
   for (size_t i = 0; i < nl; ++i) {
     const hlu_launch &L = s->launches[i];
     int rc = 0;
-    // the KM=64 companion of a truncation launch runs as a concurrent branch
-    if (L.kind == HLU_K_RKT32 && i + 1 < nl && s->launches[i + 1].kind == HLU_K_RKT64) {
-      cudaEventRecord(s->ev_fork, st);
-      cudaStreamWaitEvent(s->side, s->ev_fork, 0);
-      rc = hlu_rk_update_batched_f64(&s->ctx, s->rkt + L.first, s->parts, L.count, 64, s->side);
-      if (rc == 0) rc = hlu_rk_update_batched_f64(&s->ctx, s->rkt + L.first, s->parts, L.count, 32, st);
-      cudaEventRecord(s->ev_join, s->side);
-      cudaStreamWaitEvent(st, s->ev_join, 0);
-      ++i;
-      if (rc != 0) return rc;
-      continue;
-    }
     switch (L.kind) {
       case HLU_K_GETRF:
         rc = hlu_getrf_batched_f64(&s->ctx, s->getrf + L.first, L.count, L.smem_dim, st);
@@ -60,16 +59,18 @@ static int run_launches(hlu_schedule *s, cudaStream_t st) {
       case HLU_K_GEMM_SMALL:
         rc = hlu_gemm_small_batched_f64(&s->ctx, s->gemm + L.first, s->terms, L.count, st);
         break;
-      case HLU_K_RKT32:
-        rc = hlu_rk_update_batched_f64(&s->ctx, s->rkt + L.first, s->parts, L.count, 32, st);
+      case HLU_K_RKT32: {
+        rc = hlu_rkt_phases(&s->ctx, s->rkt, s->parts, L.first, L.count, &s->scratch, slot++, st, s->side,
+                            s->ev_fork, s->ev_join);
         break;
+      }
       case HLU_K_RKT64:
-        rc = hlu_rk_update_batched_f64(&s->ctx, s->rkt + L.first, s->parts, L.count, 64, st);
         break;
       default:
         rc = -3;
     }
     if (rc != 0) return rc;
+    if (s->stamps) k_stamp<<<1, 1, 0, st>>>(s->stamps + i + 1);
   }
   return 0;
 }
@@ -77,7 +78,8 @@ static int run_launches(hlu_schedule *s, cudaStream_t st) {
 extern "C" int hlu_schedule_create(hlu_schedule **out, const hlu_ctx *ctx, const hlu_launch *launches,
                                    int64_t nlaunch, const hlu_getrf_desc *getrf, const hlu_trsm_desc *trsm,
                                    const hlu_gemm_desc *gemm, const hlu_term *terms, hlu_rkt_desc *rkt,
-                                   const hlu_rkpart *parts, int use_graph, void *stream) {
+                                   const hlu_rkpart *parts, const hlu_rkt_scratch *scratch, int use_graph,
+                                   void *stream) {
   hlu_schedule *s = new hlu_schedule();
   s->ctx = *ctx;
   s->launches.assign(launches, launches + nlaunch);
@@ -87,9 +89,29 @@ extern "C" int hlu_schedule_create(hlu_schedule **out, const hlu_ctx *ctx, const
   s->terms = terms;
   s->rkt = rkt;
   s->parts = parts;
+  s->scratch = *scratch;
+  s->nrkt = 0;
+  for (const hlu_launch &L : s->launches) {
+    if (L.kind != HLU_K_RKT32) continue;
+    ++s->nrkt;
+    if (L.count > s->scratch.max_ops) {
+      delete s;
+      return -14;
+    }
+  }
   s->graph = nullptr;
   s->exec = nullptr;
   s->use_graph = use_graph != 0;
+  s->stamps = nullptr;
+  {
+    const char *e = getenv("HLU_STAMPS");
+    if (e && e[0] == '1') {
+      int64_t nr = 0;
+      for (const hlu_launch &L : s->launches) nr += L.kind == HLU_K_RKT32;
+      cudaMalloc(&s->stamps, (s->launches.size() + 1 + 10 * nr) * sizeof(unsigned long long));
+      cudaMemset(s->stamps, 0, (s->launches.size() + 1 + 10 * nr) * sizeof(unsigned long long));
+    }
+  }
   cudaStream_t st = (cudaStream_t)stream;
   cudaStreamCreateWithFlags(&s->side, cudaStreamNonBlocking);
   cudaEventCreateWithFlags(&s->ev_fork, cudaEventDisableTiming);
@@ -98,14 +120,16 @@ extern "C" int hlu_schedule_create(hlu_schedule **out, const hlu_ctx *ctx, const
     // make sure kernel attributes are set outside capture
     hlu_getrf_batched_f64(&s->ctx, s->getrf, 0, 0, st);
     hlu_trsm_batched_f64(&s->ctx, s->trsm, 0, 0, st);
-    hlu_rk_update_batched_f64(&s->ctx, s->rkt, s->parts, 0, 32, st);
+    hlu_rk_update_batched_f64(&s->ctx, s->rkt, s->parts, 0, &s->scratch, st);
     hlu_gemm_small_batched_f64(&s->ctx, s->gemm, s->terms, 0, st);
     hlu_gemm_batched_f64(&s->ctx, s->gemm, s->terms, 0, st);
     if (cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
       delete s;
       return -10;
     }
+    if (s->stamps) hlu_rkt_set_phase_stamps(s->stamps + s->launches.size() + 1);
     const int rc = run_launches(s, st);
+    hlu_rkt_set_phase_stamps(nullptr);
     cudaGraph_t g = nullptr;
     const cudaError_t e = cudaStreamEndCapture(st, &g);
     if (rc != 0 || e != cudaSuccess) {
@@ -134,11 +158,22 @@ extern "C" int hlu_schedule_destroy(hlu_schedule *s) {
   if (!s) return 0;
   if (s->exec) cudaGraphExecDestroy(s->exec);
   if (s->graph) cudaGraphDestroy(s->graph);
+  if (s->stamps) cudaFree(s->stamps);
   cudaEventDestroy(s->ev_fork);
   cudaEventDestroy(s->ev_join);
   cudaStreamDestroy(s->side);
   delete s;
   return 0;
+}
+
+extern "C" int64_t hlu_schedule_stamps(hlu_schedule *s, unsigned long long *out) {
+  if (!s->stamps) return 0;
+  int64_t nr = 0;
+  for (const hlu_launch &L : s->launches) nr += L.kind == HLU_K_RKT32;
+  const int64_t n = (int64_t)s->launches.size() + 1 + 10 * nr;
+  if (out && cudaMemcpy(out, s->stamps, n * sizeof(unsigned long long), cudaMemcpyDeviceToHost) != cudaSuccess)
+    return -1;
+  return n;
 }
 
 extern "C" const char *hlu_version(void) { return "hlu_b200 0.1.0 sm_100a"; }

@@ -80,6 +80,8 @@ class DeviceCall:
             self.d_terms = _dev_bytes(torch, p.terms, self.device)
             self.d_rkt = _dev_bytes(torch, p.rkt, self.device)
             self.d_parts = _dev_bytes(torch, p.parts, self.device)
+            # truncation scratch: per-level counters, op lists, row-block items
+            self.scratch, self._scratch_keep = _native.rkt_scratch(torch, self.device, p.rkt, p.launches)
             self.upload()
             self.ctx = _native.HluCtx(
                 self.pool.data_ptr(), self.ranks.data_ptr(), self.log.data_ptr(), self.err.data_ptr(),
@@ -91,6 +93,7 @@ class DeviceCall:
                 ctypes.byref(handle), ctypes.byref(self.ctx), launches.ctypes.data, len(launches),
                 self.d_getrf.data_ptr(), self.d_trsm.data_ptr(), self.d_gemm.data_ptr(),
                 self.d_terms.data_ptr(), self.d_rkt.data_ptr(), self.d_parts.data_ptr(),
+                ctypes.byref(self.scratch),
                 1 if use_graph else 0, ctypes.c_void_p(self.stream.cuda_stream),
             )
             _native.check(rc, "hlu_schedule_create")
@@ -122,6 +125,43 @@ class DeviceCall:
             self.err[0] = 0
             self.err[1] = INT32_MAX
             self.err[2] = 0
+
+    def launch_times(self):
+        """GPU time (s) of every launch-list entry inside a CUDA graph: the same
+        schedule re-captured with a %globaltimer stamp after each entry
+        (diagnostics; replays on the current device state)."""
+        import os
+
+        lib = self.lib
+        prev = os.environ.get("HLU_STAMPS")
+        os.environ["HLU_STAMPS"] = "1"
+        handle = ctypes.c_void_p()
+        try:
+            p = self.packed
+            launches = np.ascontiguousarray(p.launches)
+            with self.torch.cuda.device(self.device):
+                rc = lib.hlu_schedule_create(
+                    ctypes.byref(handle), ctypes.byref(self.ctx), launches.ctypes.data, len(launches),
+                    self.d_getrf.data_ptr(), self.d_trsm.data_ptr(), self.d_gemm.data_ptr(),
+                    self.d_terms.data_ptr(), self.d_rkt.data_ptr(), self.d_parts.data_ptr(),
+                    ctypes.byref(self.scratch), 1, ctypes.c_void_p(self.stream.cuda_stream))
+                _native.check(rc, "hlu_schedule_create")
+                _native.check(lib.hlu_schedule_launch(handle, ctypes.c_void_p(self.stream.cuda_stream)),
+                              "hlu_schedule_launch")
+                self.sync()
+            n = lib.hlu_schedule_stamps(handle, None)
+            st = np.zeros(n, dtype=np.uint64)
+            lib.hlu_schedule_stamps(handle, st.ctypes.data)
+        finally:
+            if handle:
+                lib.hlu_schedule_destroy(handle)
+            if prev is None:
+                os.environ.pop("HLU_STAMPS", None)
+            else:
+                os.environ["HLU_STAMPS"] = prev
+        nl = len(self.packed.launches)
+        self.last_phase_stamps = st[nl + 1:].astype(np.int64).reshape(-1, 10)
+        return np.diff(st[: nl + 1].astype(np.int64)) * 1e-9
 
     def launch(self):
         rc = self.lib.hlu_schedule_launch(self.handle, ctypes.c_void_p(self.stream.cuda_stream))

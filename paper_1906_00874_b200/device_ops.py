@@ -81,7 +81,7 @@ def _truncate_parts(parts_pairs, m, n, ctl, mode, signs=None):
     K = sum(ks)
     cap = max(K, 1)
     kb = K
-    ws = ir.rkt_ws_doubles(m, kb) + ir.rkt_ws_doubles(n, kb)
+    ws = ir.rkt_ws_doubles(m, n, kb)
     size = sum(p.a.size + p.b.size for p in parts_pairs) + (m + n) * cap + ws + 16
     S = _Scratch(size, len(parts_pairs) + 1, ctl)
     recs = []
@@ -105,10 +105,12 @@ def _truncate_parts(parts_pairs, m, n, ctl, mode, signs=None):
         import torch
 
         dd, dp = _dev(torch, d), _dev(torch, parts)
-        t = (dd, dp)
-        for kc in (32, 64):
-            _native.check(lib.hlu_rk_update_batched_f64(ctx, dd.data_ptr(), dp.data_ptr(), 1, kc, stream),
-                          "hlu_rk_update_batched_f64")
+        launches = np.zeros(1, dtype=ir.LAUNCH)
+        launches[0] = (ir.K_RKT32, 1, 0, 0, 0)
+        sc, keep = _native.rkt_scratch(torch, dd.device, d, launches)
+        t = (dd, dp, keep)
+        _native.check(lib.hlu_rk_update_batched_f64(ctx, dd.data_ptr(), dp.data_ptr(), 1, ctypes.byref(sc), stream),
+                      "hlu_rk_update_batched_f64")
 
     S.go(fn)
     if S.out_err[2]:

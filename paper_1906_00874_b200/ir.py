@@ -22,13 +22,14 @@ GEMM = np.dtype([("term_begin", "<i4"), ("term_count", "<i4"), ("log", "<i4"), (
 RKPART = np.dtype([("a", VIEW), ("b", VIEW), ("sign", "<f8"), ("roff", "<i4"), ("coff", "<i4")])
 RKT = np.dtype([("mode", "<i4"), ("part_begin", "<i4"), ("part_count", "<i4"), ("m", "<i4"),
                 ("n", "<i4"), ("cap", "<i4"), ("out_slot", "<i4"), ("log", "<i4"),
-                ("out_a", "<i8"), ("out_b", "<i8"), ("ws", "<i8"), ("handoff", "<i4"), ("pad", "<i4")])
+                ("out_a", "<i8"), ("out_b", "<i8"), ("ws", "<i8"), ("reserved", "<i4"), ("pad", "<i4")])
+RKT_ITEM = np.dtype([("op", "<i4"), ("side", "<i2"), ("block", "<i2")])
 LAUNCH = np.dtype([("kind", "<i4"), ("count", "<i4"), ("first", "<i8"), ("smem_dim", "<i4"),
                    ("pad", "<i4")])
 
 assert VIEW.itemsize == 32 and GETRF.itemsize == 40 and TRSM.itemsize == 72
 assert TERM.itemsize == 144 and GEMM.itemsize == 16 and RKPART.itemsize == 80
-assert RKT.itemsize == 64 and LAUNCH.itemsize == 24
+assert RKT.itemsize == 64 and LAUNCH.itemsize == 24 and RKT_ITEM.itemsize == 8
 
 # kinds (hlu_b200.h)
 K_GETRF, K_TRSM, K_GEMM, K_RKT32, K_RKT64, K_GEMM_SMALL = 0, 1, 2, 3, 4, 5
@@ -79,20 +80,66 @@ def colmajor(off, rows, cols, cdyn=-1):
     return View(off, rows, cols, 1, rows, -1, cdyn)
 
 
-def rkt_chunk_rows(km):
-    bufd = 4608 if km == 32 else 9216
-    return bufd // km - km
+# workspace geometry of the batched truncation: mirror of csrc/rk_layout.h
+RK_KMAX, RK_BR, RK_BUFA, RK_BUFB32, RK_BUFB64 = 64, 512, 6144, 3072, 8192
 
 
-def rkt_ws_one(m, k, ch):
-    if m <= 0 or k <= 0:
+def rk_ch(K, bufd):
+    ch = 512
+    while ch > 32 and (ch + K) * K > bufd:
+        ch >>= 1
+    return ch
+
+
+def rk_chc(K):
+    return rk_ch(K, RK_BUFB32 if K <= 32 else RK_BUFB64)
+
+
+def rk_chain(rows, K, ch):
+    return ((rows + ch - 1) // ch) * ((K + ch) * K + K)
+
+
+def rk_side_total(M, K):
+    ch, chc = rk_ch(K, RK_BUFA), rk_chc(K)
+    nb = (M + RK_BR - 1) // RK_BR
+    last = M - (nb - 1) * RK_BR
+    off_R = (nb - 1) * rk_chain(RK_BR, K, ch) + rk_chain(last, K, ch)
+    srows = (nb - 1) * K + min(last, K)
+    off_Z = off_R + nb * K * K + (rk_chain(srows, K, chc) if nb > 1 else 0)
+    return off_Z + srows * K
+
+
+def rkt_ws_doubles(m, n, kbound):
+    """Mirror of hlu_rkt_ws_doubles / rk_ws_doubles (csrc/rk_layout.h)."""
+    if m <= 0 or n <= 0 or kbound <= 0:
         return 0
-    nch = (m + ch - 1) // ch
-    return nch * ((k + ch) * k + k)
+    kb = min(kbound, RK_KMAX)
+    best = 0
+    for K in range(1, kb + 1):
+        if K < kb and rk_ch(K + 1, RK_BUFA) == rk_ch(K, RK_BUFA) and rk_chc(K + 1) == rk_chc(K):
+            continue
+        best = max(best, rk_side_total(m, K) + rk_side_total(n, K))
+    return best
 
 
-def rkt_ws_doubles(m, kbound):
-    """Mirror of hlu_rkt_ws_doubles (rk_kernels.cu)."""
-    a = rkt_ws_one(m, min(kbound, 32), rkt_chunk_rows(32))
-    b = rkt_ws_one(m, min(kbound, 64), rkt_chunk_rows(64))
-    return max(a, b)
+def rkt_items(m, n):
+    """Mirror of hlu_rkt_items: (op, side, block) of every row block, in op order;
+    returns (items structured array, item_start[count + 1])."""
+    m = np.asarray(m, dtype=np.int64)
+    n = np.asarray(n, dtype=np.int64)
+    nbm = (m + RK_BR - 1) // RK_BR
+    nbn = (n + RK_BR - 1) // RK_BR
+    per = nbm + nbn
+    start = np.zeros(len(m) + 1, dtype=np.int64)
+    np.cumsum(per, out=start[1:])
+    tot = int(start[-1])
+    items = np.zeros(max(tot, 1), dtype=RKT_ITEM)
+    if tot:
+        op = np.repeat(np.arange(len(m), dtype=np.int64), per)
+        pos = np.arange(tot, dtype=np.int64) - start[op]
+        side = (pos >= nbm[op]).astype(np.int64)
+        block = np.where(side == 0, pos, pos - nbm[op])
+        items["op"][:tot] = op
+        items["side"][:tot] = side
+        items["block"][:tot] = block
+    return items, start

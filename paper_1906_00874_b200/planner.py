@@ -302,7 +302,7 @@ class Planner:
             out_a, out_b, slot = self.L.rk[id(out)]
             writes.append(self.L.res(out))
             res = None
-        ws_n = rkt_ws_doubles(m, kb) + rkt_ws_doubles(n, kb)
+        ws_n = rkt_ws_doubles(m, n, kb)
         tw, ws = self._temp(ws_n) if ws_n else (None, 0)
         if tw is not None:
             temps_out.append(tw)

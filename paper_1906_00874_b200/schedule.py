@@ -207,8 +207,6 @@ def pack(pl: Planner, arena_base: int):
     for kind, count, first, dim in launches:
         if kind == ir.K_RKT32:
             out.append((ir.K_RKT32, count, first, 0, 0))
-            if dim > 32:
-                out.append((ir.K_RKT64, count, first, 0, 0))
         else:
             out.append((kind, count, first, dim, 0))
 

@@ -33,9 +33,32 @@ def test_library_exports_header_symbols():
 
 def test_workspace_formula_mirrors_library():
     L = _native.lib()
-    for m in (1, 17, 64, 80, 112, 113, 257, 2049, 9000):
-        for k in (1, 8, 31, 32, 33, 64, 80):
-            assert L.hlu_rkt_ws_doubles(m, k) == ir.rkt_ws_doubles(m, k)
+    sizes = (1, 17, 64, 80, 112, 113, 257, 512, 513, 2049, 9000, 16384)
+    for m in sizes:
+        for n in sizes[::3]:
+            for k in (1, 5, 6, 8, 11, 12, 20, 21, 31, 32, 33, 37, 38, 46, 47, 52, 53, 64, 80):
+                assert L.hlu_rkt_ws_doubles(m, n, k) == ir.rkt_ws_doubles(m, n, k)
+
+
+def test_workspace_covers_every_runtime_rank():
+    """The reserved workspace is the maximum of the runtime layout over K <= kbound."""
+    for m, n in ((17, 64), (512, 513), (2049, 100), (16384, 9000)):
+        for kb in (7, 21, 32, 45, 64):
+            want = max(ir.rk_side_total(m, K) + ir.rk_side_total(n, K) for K in range(1, kb + 1))
+            assert ir.rkt_ws_doubles(m, n, kb) == want
+
+
+def test_truncation_items_mirror_library():
+    d = np.zeros(5, dtype=ir.RKT)
+    d["m"] = [17, 512, 513, 16384, 2000]
+    d["n"] = [64, 1, 1500, 30, 512]
+    L = _native.lib()
+    n = L.hlu_rkt_items(d.ctypes.data, len(d), None)
+    got = np.zeros(n, dtype=ir.RKT_ITEM)
+    assert L.hlu_rkt_items(d.ctypes.data, len(d), got.ctypes.data) == n
+    items, start = ir.rkt_items(d["m"], d["n"])
+    assert start[-1] == n and items[:n].tobytes() == got.tobytes()
+    assert list(np.diff(start)) == [2, 2, 5, 33, 5]
 
 
 def _run_ir(name, cap=32):

@@ -48,8 +48,12 @@ def gpu_launch(li):
     if kind == ir.K_GEMM:
         return lib.hlu_gemm_batched_f64(ctx, call.d_gemm.data_ptr() + first * ir.GEMM.itemsize,
                                         call.d_terms.data_ptr(), count, st)
-    return lib.hlu_rk_update_batched_f64(ctx, call.d_rkt.data_ptr() + first * ir.RKT.itemsize,
-                                         call.d_parts.data_ptr(), count, 32 if kind == ir.K_RKT32 else 64, st)
+    if kind == ir.K_GEMM_SMALL:
+        return lib.hlu_gemm_small_batched_f64(ctx, call.d_gemm.data_ptr() + first * ir.GEMM.itemsize,
+                                              call.d_terms.data_ptr(), count, st)
+    call._scratch_keep[0].zero_()
+    return lib.hlu_rkt_phases(ctx, call.d_rkt.data_ptr(), call.d_parts.data_ptr(), first, count,
+                              ctypes.byref(call.scratch), 0, st, st, None, None)
 
 
 def strided(buf, v, ranks_):
@@ -68,14 +72,10 @@ def rel(g, c):
     return np.linalg.norm(g - c) / den if den > 0 else np.linalg.norm(g)
 
 
-lib.hlu_epoch_bump.argtypes = [ctypes.c_void_p]
-lib.hlu_epoch_bump(st)
 li = 0
 nl = len(p.launches)
 while li < nl:
     group = [li]
-    if int(p.launches[li]["kind"]) == ir.K_RKT32 and li + 1 < nl and int(p.launches[li + 1]["kind"]) == ir.K_RKT64:
-        group.append(li + 1)
     before_ranks = M.ranks.copy()
     for g in group:
         assert gpu_launch(g) == 0
