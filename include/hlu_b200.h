@@ -157,19 +157,26 @@ typedef struct {
 } hlu_rkt_scratch;
 
 /* count truncations d[0 .. count) (count <= scratch->max_ops; counter slot 0).  A
- * classify kernel routes every op: max(m,n) <= 128 and K <= 16 -> one warp per op with
- * the factors in registers; K <= 32 -> one warp per op in shared memory; others ->
+ * classify kernel routes every op: max(m,n) <= 64 and K <= 16 -> one warp per op with
+ * the factors in registers; others ->
  * block TSQR (one CTA per 512-row block), core SVD + rank (one CTA per op), Q apply
  * (one CTA per block). */
 int hlu_rk_update_batched_f64(const hlu_ctx *ctx, hlu_rkt_desc *d, const hlu_rkpart *parts, int count,
                               const hlu_rkt_scratch *scratch, void *stream);
+/* auxiliary streams (cudaStream_t) and events (cudaEvent_t) for hlu_rkt_phases */
+typedef struct {
+  void *side[4];
+  void *ev[8];
+} hlu_rkt_streams;
+
 /* ops d[first .. first+count) of one level with counter slot `slot` (zeroed by the
- * caller); the warp kernels run on `side` between the events ev_fork/ev_join
- * (cudaEvent_t), concurrently with the CTA phases; side == stream runs all in order */
+ * caller).  With aux, independent kernels run as concurrent branches (register warp
+ * kernels on side[0..1], the three core kernels on stream/side[2]/side[3]) joined on
+ * `stream`; aux == NULL runs everything in order on `stream`. */
 int hlu_rkt_phases(const hlu_ctx *ctx, hlu_rkt_desc *d, const hlu_rkpart *parts, int64_t first, int count,
-                   const hlu_rkt_scratch *scratch, int slot, void *stream, void *side, void *ev_fork, void *ev_join);
+                   const hlu_rkt_scratch *scratch, int slot, void *stream, const hlu_rkt_streams *aux);
 /* one kernel only (diagnostics / per-kernel timing): 0 classify, 1 register warp K<=8,
- * 2 register warp K<=16, 3 shared-memory warp K<=32, 4 block TSQR, 5 core by one warp
+ * 2 register warp K<=16, 3 (none), 4 block TSQR, 5 core by one warp
  * (K<=16), 6 core K<=32, 7 core K>32, 8 Q apply */
 int hlu_rkt_phase(const hlu_ctx *ctx, hlu_rkt_desc *d, const hlu_rkpart *parts, int64_t first, int count,
                   const hlu_rkt_scratch *scratch, int slot, int which, void *stream);

@@ -77,7 +77,7 @@ def lib():
     L.hlu_gemm_small_batched_f64.argtypes = [ctypes.POINTER(HluCtx), vp, vp, i32, vp]
     sp = ctypes.POINTER(HluRktScratch)
     L.hlu_rk_update_batched_f64.argtypes = [ctypes.POINTER(HluCtx), vp, vp, i32, sp, vp]
-    L.hlu_rkt_phases.argtypes = [ctypes.POINTER(HluCtx), vp, vp, i64, i32, sp, i32, vp, vp, vp, vp]
+    L.hlu_rkt_phases.argtypes = [ctypes.POINTER(HluCtx), vp, vp, i64, i32, sp, i32, vp, vp]
     L.hlu_rkt_phase.argtypes = [ctypes.POINTER(HluCtx), vp, vp, i64, i32, sp, i32, i32, vp]
     L.hlu_rkt_items.argtypes = [vp, i32, vp]
     L.hlu_rkt_items.restype = i64

@@ -548,7 +548,7 @@ struct StackedR {  // the blocks' R factors stacked: block b at R + b K K (ld K)
 #define RK_CNT 8
 #define RK_SEG_R8 0     // max(m,n) <= 64, K <= 8: register warp kernel
 #define RK_SEG_R16 1    // max(m,n) <= 64, K <= 16: register warp kernel
-#define RK_SEG_W32 2    // max(m,n) <= 64, K <= 32: shared-memory warp kernel
+#define RK_SEG_W32 2    // unused
 #define RK_SEG_BIG 3    // CTA phases (and the ADD shortcuts / empty recompressions)
 #define RK_SEG_C16 4    // CTA-path ops with K <= 16, m, n <= RK_BR: core SVD by one warp
 #define RK_SEG_Q8 5     // max(m,n) <= 128, K <= 8: register warp kernel, 4 rows per lane
@@ -607,318 +607,6 @@ __global__ void k_rkt_classify(hlu_ctx c, const hlu_rkt_desc *__restrict__ d, co
     it.side = (int16_t)(b >= nbm);
     it.block = (int16_t)(b >= nbm ? b - nbm : b);
     s.items[base + b] = it;
-  }
-}
-
-// ---------------------------------------------------------------- warp path
-//
-// One warp per small truncation (max(m, n) <= 64, K <= KB): lane l owns rows
-// l and l + 32 of the factor being factorised (warp-private shared memory,
-// ld 64), so a Householder step needs only warp shuffles; the core SVD is a
-// one-sided Jacobi with one lane per column.  X's reflectors are parked in
-// the op's workspace while Y is factorised.
-
-template <int KB>
-struct WCfg {
-  static constexpr int WPC = KB == 16 ? 4 : 2;  // warps (ops) per CTA
-  static constexpr int LDG = KB + 1;
-  static constexpr int PER = 64 * KB + 2 * KB * LDG + 3 * KB;  // S | G | V | tau_x | tau_y | sig
-  static size_t smem() { return (size_t)WPC * PER * sizeof(double); }
-};
-
-// factor column j (< K) of the stacked X (left) or Y into S (ld 64); zero rows >= M
-__device__ __forceinline__ void w_load(const PartInfo *P, int np, bool left, int M, int K, double *S, int l) {
-  for (int j = 0; j < K; ++j) {
-    S[l + 64 * j] = l < M ? stacked(P, np, left, l, j) : 0.0;
-    S[l + 32 + 64 * j] = l + 32 < M ? stacked(P, np, left, l + 32, j) : 0.0;
-  }
-}
-
-// Householder QR (dlarfg conventions) of S (64 x K, ld 64, zero-padded rows)
-// in place; tau[K].  Lane l touches only its rows l, l + 32.
-__device__ void w_qr(double *S, int K, double *tau, int l) {
-  for (int j = 0; j < K; ++j) {
-    const double x0 = S[l + 64 * j], x1 = S[l + 32 + 64 * j];
-    double ss = l > j ? x0 * x0 : 0.0;
-    ss = fma(x1, x1, ss);
-    ss = warp_sum(ss);
-    const double alpha = __shfl_sync(0xffffffffu, x0, j);
-    double tj = 0.0, beta = alpha, sc = 0.0;
-    if (ss != 0.0) {
-      const double n2 = fma(alpha, alpha, ss);
-      const double rn = fast_rsqrt(n2);
-      beta = -copysign(n2 * rn, alpha);
-      tj = fma(fabs(alpha), rn, 1.0);
-      sc = fast_rcp(alpha - beta);
-    }
-    const double v0 = l > j ? x0 * sc : (l == j ? 1.0 : 0.0);
-    const double v1 = x1 * sc;
-    S[l + 64 * j] = l > j ? v0 : (l == j ? beta : x0);
-    S[l + 32 + 64 * j] = v1;
-    if (l == 0) tau[j] = tj;
-    if (tj == 0.0) continue;
-    for (int c0 = j + 1; c0 < K; c0 += RK_NB) {
-      double p[RK_NB];
-#pragma unroll
-      for (int b = 0; b < RK_NB; ++b) {
-        const int cc = c0 + b;
-        p[b] = cc < K ? fma(v1, S[l + 32 + 64 * cc], v0 * S[l + 64 * cc]) : 0.0;
-      }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-#pragma unroll
-        for (int b = 0; b < RK_NB; ++b) p[b] += __shfl_xor_sync(0xffffffffu, p[b], o);
-      }
-#pragma unroll
-      for (int b = 0; b < RK_NB; ++b) {
-        const int cc = c0 + b;
-        if (cc < K) {
-          const double f = tj * p[b];
-          S[l + 64 * cc] -= f * v0;
-          S[l + 32 + 64 * cc] -= f * v1;
-        }
-      }
-    }
-  }
-}
-
-// round-robin (circle method) partner of column c in round r, qq even
-__device__ __forceinline__ int rr_partner(int c, int r, int qq) {
-  const int n1 = qq - 1;
-  const int pos = c == 0 ? 0 : 1 + (c - 1 - r + n1) % n1;
-  const int pp = qq - 1 - pos;
-  return pp == 0 ? 0 : 1 + (pp - 1 + r) % n1;
-}
-
-// new own column l (of the pair (a, b)) = rotation of columns a, b of X, in
-// chunks of RK_NB rows held in registers; the warp syncs between the reads
-// and the writes of every chunk, because the partner lane reads the same rows
-template <int LDG>
-__device__ __forceinline__ void w_rotate(double *X, int K, int a, int b, bool rot, bool is_a, double cs, double sn,
-                                         int l) {
-  for (int i0 = 0; i0 < K; i0 += RK_NB) {
-    double x[RK_NB], y[RK_NB];
-    if (rot) {
-#pragma unroll
-      for (int q = 0; q < RK_NB; ++q) {
-        if (i0 + q < K) {
-          x[q] = X[a * LDG + i0 + q];
-          y[q] = X[b * LDG + i0 + q];
-        }
-      }
-    }
-    __syncwarp();
-    if (rot) {
-#pragma unroll
-      for (int q = 0; q < RK_NB; ++q)
-        if (i0 + q < K) X[l * LDG + i0 + q] = is_a ? cs * x[q] - sn * y[q] : sn * x[q] + cs * y[q];
-    }
-    __syncwarp();
-  }
-}
-
-// one-sided Jacobi on G (K x K, ld KB+1; lane c owns column c) accumulating V;
-// same rotation formulas and stopping rule as the CTA kernel
-template <int KB>
-__device__ void w_jacobi(double *G, double *V, int K, int l) {
-  constexpr int LDG = KB + 1;
-  if (K < 2) return;
-  const int qq = K + (K & 1);
-  for (int sweep = 0; sweep < 40; ++sweep) {
-    int big = 0;
-    for (int r = 0; r < qq - 1; ++r) {
-      const int pl = l < qq ? rr_partner(l, r, qq) : qq;
-      const bool act = l < K && pl < K;
-      const int a = min(l, pl), b = max(l, pl);
-      double cs = 1.0, sn = 0.0;
-      bool rot = false;
-      if (act) {
-        double al = 0.0, be = 0.0, ga = 0.0;
-        for (int i = 0; i < K; ++i) {
-          const double x = G[a * LDG + i], y = G[b * LDG + i];
-          al = fma(x, x, al);
-          be = fma(y, y, be);
-          ga = fma(x, y, ga);
-        }
-        const double g2 = ga * ga, ab = al * be;
-        if (ga != 0.0 && g2 > 1e-30 * ab) {
-          rot = true;
-          if (g2 > 1e-16 * ab) big = 1;
-          const double dd = be - al;
-          const double q2 = fma(dd, dd, 4.0 * g2);
-          const double rq = q2 * fast_rsqrt(q2);
-          const double t = 2.0 * ga * fast_rcp(dd + copysign(rq, dd));
-          cs = fast_rsqrt(fma(t, t, 1.0));
-          sn = cs * t;
-        }
-      }
-      w_rotate<LDG>(G, K, a, b, rot, l == a, cs, sn, l);
-      w_rotate<LDG>(V, K, a, b, rot, l == a, cs, sn, l);
-    }
-    if (!__any_sync(0xffffffffu, big)) {
-      if (l == 0) atomicAdd(&g_sweeps, sweep + 1);
-      break;
-    }
-  }
-}
-
-// out (M x kk, ld M) = Q [W_sel; 0]: W_sel column cc = W column perm[cc]
-// (K rows, ld KB+1), Q from the reflectors in S / tau; RK_NB output columns
-// at a time in registers (lane l: rows l, l + 32).
-template <int KB>
-__device__ void w_apply(const double *S, int K, const double *tau, const double *W, const int *perm, int kk, int M,
-                        double *out, int l) {
-  constexpr int LDG = KB + 1;
-  for (int c0 = 0; c0 < kk; c0 += RK_NB) {
-    double t0[RK_NB], t1[RK_NB];
-#pragma unroll
-    for (int q = 0; q < RK_NB; ++q) {
-      t0[q] = (c0 + q < kk && l < K) ? W[perm[c0 + q] * LDG + l] : 0.0;
-      t1[q] = 0.0;
-    }
-    for (int j = K - 1; j >= 0; --j) {
-      const double tj = tau[j];
-      if (tj == 0.0) continue;
-      const double v0 = l > j ? S[l + 64 * j] : (l == j ? 1.0 : 0.0);
-      const double v1 = S[l + 32 + 64 * j];
-      double p[RK_NB];
-#pragma unroll
-      for (int q = 0; q < RK_NB; ++q) p[q] = fma(v1, t1[q], v0 * t0[q]);
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-#pragma unroll
-        for (int q = 0; q < RK_NB; ++q) p[q] += __shfl_xor_sync(0xffffffffu, p[q], o);
-      }
-#pragma unroll
-      for (int q = 0; q < RK_NB; ++q) {
-        const double f = tj * p[q];
-        t0[q] -= f * v0;
-        t1[q] -= f * v1;
-      }
-    }
-#pragma unroll
-    for (int q = 0; q < RK_NB; ++q) {
-      if (c0 + q < kk) {
-        if (l < M) out[l + (int64_t)(c0 + q) * M] = t0[q];
-        if (l + 32 < M) out[l + 32 + (int64_t)(c0 + q) * M] = t1[q];
-      }
-    }
-  }
-}
-
-template <int KB>
-__device__ void w_trunc(const hlu_ctx &c, const hlu_rkt_desc &o, const hlu_rkpart *parts, PartInfo *P, double *S,
-                        int *perm, int l) {
-  constexpr int LDG = KB + 1;
-  double *G = S + 64 * KB;
-  double *V = G + KB * LDG;
-  double *taux = V + KB * LDG;
-  double *tauy = taux + KB;
-  double *sig = tauy + KB;
-  const int np = min(o.part_count, RK_MAXP);
-  if (l < np) {
-    const hlu_rkpart q = parts[o.part_begin + l];
-    P[l].a = resolve(c, q.a);
-    P[l].b = resolve(c, q.b);
-    P[l].sign = q.sign;
-    P[l].roff = q.roff;
-    P[l].coff = q.coff;
-    P[l].k = P[l].a.cols;
-  }
-  __syncwarp();
-  if (l == 0) {
-    int col = 0;
-    for (int p = 0; p < np; ++p) {
-      P[p].col0 = col;
-      col += P[p].k;
-    }
-  }
-  __syncwarp();
-  bool shortcut;
-  const int K = logged_K(c, o, &shortcut);
-  const int m = o.m, n = o.n;
-  double *ws = c.pool + o.ws;
-  // X = Q_x R_x: R_x -> G (upper, ld LDG), reflectors -> workspace
-  w_load(P, np, true, m, K, S, l);
-  w_qr(S, K, taux, l);
-  for (int cc = 0; cc < K; ++cc) {
-    if (l < K) G[cc * LDG + l] = l <= cc ? S[l + 64 * cc] : 0.0;
-    ws[l + 64 * cc] = S[l + 64 * cc];
-    ws[l + 32 + 64 * cc] = S[l + 32 + 64 * cc];
-  }
-  // Y = Q_y R_y
-  w_load(P, np, false, n, K, S, l);
-  w_qr(S, K, tauy, l);
-  __syncwarp();
-  // M = R_x R_y^T into V (lane c: column c); R_y[c][t] = S[c + 64 t], t >= c
-  if (l < K) {
-    for (int i = 0; i < K; ++i) {
-      double acc = 0.0;
-      for (int t = max(i, l); t < K; ++t) acc = fma(G[t * LDG + i], S[l + 64 * t], acc);
-      V[l * LDG + i] = acc;
-    }
-  }
-  __syncwarp();
-  double *Gm = V, *Vm = G;
-  if (l < K)
-    for (int i = 0; i < K; ++i) Vm[l * LDG + i] = i == l ? 1.0 : 0.0;
-  __syncwarp();
-  w_jacobi<KB>(Gm, Vm, K, l);
-  if (l < K) {
-    double ss = 0.0;
-    for (int i = 0; i < K; ++i) ss = fma(Gm[l * LDG + i], Gm[l * LDG + i], ss);
-    sig[l] = sqrt(ss);
-  }
-  __syncwarp();
-  if (l < K) {
-    int rk = 0;
-    const double sj = sig[l];
-    for (int i = 0; i < K; ++i) rk += (sig[i] > sj) || (sig[i] == sj && i < l);
-    perm[rk] = l;
-  }
-  __syncwarp();
-  int kk = 0;
-  {
-    const double s1 = sig[perm[0]];
-    if (s1 != 0.0) {
-      const double thr = c.eps * s1;
-      for (int i = 0; i < K; ++i) kk += sig[i] > thr;
-    }
-    if (c.kmax >= 0) kk = min(kk, c.kmax);
-    if (kk > o.cap) {
-      if (l == 0) atomicAdd(&c.err[0], 1);
-      kk = o.cap;
-    }
-  }
-  // B' = Q_y [V_k; 0] (Y's reflectors are still in S), then A' = Q_x [(U S)_k; 0]
-  w_apply<KB>(S, K, tauy, Vm, perm, kk, n, c.pool + o.out_b, l);
-  for (int cc = 0; cc < K; ++cc) {
-    S[l + 64 * cc] = ws[l + 64 * cc];
-    S[l + 32 + 64 * cc] = ws[l + 32 + 64 * cc];
-  }
-  w_apply<KB>(S, K, taux, Gm, perm, kk, m, c.pool + o.out_a, l);
-  if (l == 0) {
-    c.ranks[o.out_slot] = kk;
-    c.log[o.log + 2] = kk;
-  }
-}
-
-template <int KB>
-__global__ void __launch_bounds__(WCfg<KB>::WPC * 32, 16 / WCfg<KB>::WPC)
-    k_rkt_w(hlu_ctx c, const hlu_rkt_desc *__restrict__ d, const hlu_rkpart *__restrict__ parts, hlu_rkt_scratch s,
-            int slot) {
-  constexpr int WPC = WCfg<KB>::WPC;
-  extern __shared__ double sm[];
-  __shared__ PartInfo P[WPC][RK_MAXP];
-  __shared__ int perm[WPC][KB];
-  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-  const int n = s.counts[RK_CNT * slot + RK_SEG_W32];
-  const int32_t *lst = s.list + RK_SEG_W32 * s.max_ops;
-  double *S = sm + w * WCfg<KB>::PER;
-  for (int idx = blockIdx.x * WPC + w; idx < n; idx += gridDim.x * WPC) {
-    const hlu_rkt_desc o = d[lst[idx]];
-    w_trunc<KB>(c, o, parts, P[w], S, perm[w], l);
-    __syncwarp();
   }
 }
 
@@ -1638,7 +1326,6 @@ static void rkt_init() {
   cudaFuncSetAttribute(k_rkt_r<2, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RCfg<2, 16>::smem());
   cudaFuncSetAttribute(k_rkt_r<4, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RCfg<4, 8>::smem());
   cudaFuncSetAttribute(k_rkt_r<4, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RCfg<4, 16>::smem());
-  cudaFuncSetAttribute(k_rkt_w<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)WCfg<32>::smem());
   cudaFuncSetAttribute(k_rkt_bw<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)BwCfg<16>::smem());
   init = true;
 }
@@ -1655,9 +1342,8 @@ static void launch_r(const hlu_ctx *ctx, hlu_rkt_desc *d, const hlu_rkpart *part
   k_rkt_r<RPL, KB><<<grid, Cfg::WPC * 32, Cfg::smem(), st>>>(*ctx, d, parts, s, slot);
 }
 
-// kernels of one level: 0 classify, 1 register warp K<=8 (m,n <= 64 and <= 128), 2 the same K<=16,
-// 3 shared-memory warp K<=32, 4 block TSQR, 5 core by one warp (K<=16), 6 core K<=32,
-// 7 core K>32, 8 Q apply
+// kernels of one level: 0 classify, 1 register warp K<=8, 2 register warp K<=16,
+// 3 (none), 4 block TSQR, 5 core by one warp (K<=16), 6 core K<=32, 7 core K>32, 8 Q apply
 #define RK_NKERN 9
 static int rkt_launch(int which, const hlu_ctx *ctx, hlu_rkt_desc *d, const hlu_rkpart *parts, int64_t first,
                       int count, const hlu_rkt_scratch &s, int slot, cudaStream_t st) {
@@ -1675,9 +1361,7 @@ static int rkt_launch(int which, const hlu_ctx *ctx, hlu_rkt_desc *d, const hlu_
       launch_r<2, 16>(ctx, d, parts, count, s, slot, st);
       launch_r<4, 16>(ctx, d, parts, count, s, slot, st);
       break;
-    case 3:
-      k_rkt_w<32><<<lim((count + 1) / 2, 3), 2 * 32, WCfg<32>::smem(), st>>>(*ctx, d, parts, s, slot);
-      break;
+    case 3: break;  // (slot of a retired kernel)
     case 4: k_rkt_a<<<lim(2 * (int64_t)count, 4), HLU_NT, smem_a(), st>>>(*ctx, d, parts, s, slot); break;
     case 5:
       k_rkt_bw<16><<<lim((count + 3) / 4, 4), 4 * 32, BwCfg<16>::smem(), st>>>(*ctx, d, s, slot);
@@ -1702,34 +1386,55 @@ __global__ void k_rkt_stamp(unsigned long long *slot) {
 static unsigned long long *g_phase_stamps = nullptr;
 extern "C" void hlu_rkt_set_phase_stamps(unsigned long long *p) { g_phase_stamps = p; }
 
+// one level.  With aux: the two register warp kernels on side[0], side[1] and,
+// after the block TSQR, the three core kernels on the main stream, side[2],
+// side[3], all joined before the Q apply (8 events); without aux all in order.
 extern "C" int hlu_rkt_phases(const hlu_ctx *ctx, hlu_rkt_desc *d, const hlu_rkpart *parts, int64_t first,
-                              int count, const hlu_rkt_scratch *scratch, int slot, void *stream, void *side,
-                              void *ev_fork, void *ev_join) {
+                              int count, const hlu_rkt_scratch *scratch, int slot, void *stream,
+                              const hlu_rkt_streams *aux) {
   rkt_init();
   if (count <= 0) return cudaGetLastError() == cudaSuccess ? 0 : -1;
-  cudaStream_t st = (cudaStream_t)stream, sd = (cudaStream_t)side;
+  cudaStream_t st = (cudaStream_t)stream;
   const hlu_rkt_scratch &s = *scratch;
   unsigned long long *ps = g_phase_stamps ? g_phase_stamps + RK_NSTAMP * (int64_t)slot : nullptr;
   auto stamp = [&](int k, cudaStream_t q) {
     if (ps) k_rkt_stamp<<<1, 1, 0, q>>>(ps + k);
   };
-  rkt_launch(0, ctx, d, parts, first, count, s, slot, st);
-  stamp(0, st);
-  if (sd != st) {
-    cudaEventRecord((cudaEvent_t)ev_fork, st);
-    cudaStreamWaitEvent(sd, (cudaEvent_t)ev_fork, 0);
+  auto run = [&](int w, cudaStream_t q) {
+    rkt_launch(w, ctx, d, parts, first, count, s, slot, q);
+    stamp(w, q);
+  };
+  if (!aux) {
+    for (int w = 0; w < RK_NKERN; ++w) run(w, st);
+    stamp(RK_NKERN, st);
+    return cudaGetLastError() == cudaSuccess ? 0 : -1;
   }
-  cudaStream_t ws = sd != st ? sd : st;
-  for (int w = 1; w <= 3; ++w) {
-    rkt_launch(w, ctx, d, parts, first, count, s, slot, ws);
-    stamp(w, ws);
-  }
-  if (sd != st) cudaEventRecord((cudaEvent_t)ev_join, sd);
-  for (int w = 4; w < RK_NKERN; ++w) {
-    rkt_launch(w, ctx, d, parts, first, count, s, slot, st);
-    stamp(w, st);
-  }
-  if (sd != st) cudaStreamWaitEvent(st, (cudaEvent_t)ev_join, 0);
+  cudaStream_t s0 = (cudaStream_t)aux->side[0], s1 = (cudaStream_t)aux->side[1];
+  cudaStream_t s2 = (cudaStream_t)aux->side[2], s3 = (cudaStream_t)aux->side[3];
+  cudaEvent_t *ev = (cudaEvent_t *)aux->ev;
+  run(0, st);
+  cudaEventRecord(ev[0], st);
+  cudaStreamWaitEvent(s0, ev[0], 0);
+  cudaStreamWaitEvent(s1, ev[0], 0);
+  run(1, s0);
+  cudaEventRecord(ev[1], s0);
+  run(2, s1);
+  stamp(3, s1);
+  cudaEventRecord(ev[2], s1);
+  run(4, st);
+  cudaEventRecord(ev[3], st);
+  cudaStreamWaitEvent(s2, ev[3], 0);
+  cudaStreamWaitEvent(s3, ev[3], 0);
+  run(6, s2);
+  cudaEventRecord(ev[4], s2);
+  run(7, s3);
+  cudaEventRecord(ev[5], s3);
+  run(5, st);
+  cudaStreamWaitEvent(st, ev[4], 0);
+  cudaStreamWaitEvent(st, ev[5], 0);
+  run(8, st);
+  cudaStreamWaitEvent(st, ev[1], 0);
+  cudaStreamWaitEvent(st, ev[2], 0);
   stamp(RK_NKERN, st);
   return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }
@@ -1749,7 +1454,7 @@ extern "C" int hlu_rk_update_batched_f64(const hlu_ctx *ctx, hlu_rkt_desc *d, co
   if (count <= 0) return 0;
   if (count > scratch->max_ops) return -4;
   cudaMemsetAsync(scratch->counts, 0, RK_CNT * sizeof(int32_t), (cudaStream_t)stream);
-  return hlu_rkt_phases(ctx, d, parts, 0, count, scratch, 0, stream, stream, nullptr, nullptr);
+  return hlu_rkt_phases(ctx, d, parts, 0, count, scratch, 0, stream, nullptr);
 }
 
 extern "C" int64_t hlu_rkt_items(const hlu_rkt_desc *d, int count, hlu_rkt_item *items) {

@@ -15,8 +15,7 @@ extern "C" void hlu_rkt_set_phase_stamps(unsigned long long *p);
 
 struct hlu_schedule {
   hlu_ctx ctx;
-  cudaStream_t side;
-  cudaEvent_t ev_fork, ev_join;
+  hlu_rkt_streams aux;
   std::vector<hlu_launch> launches;
   const hlu_getrf_desc *getrf;
   const hlu_trsm_desc *trsm;
@@ -60,8 +59,7 @@ static int run_launches(hlu_schedule *s, cudaStream_t st) {
         rc = hlu_gemm_small_batched_f64(&s->ctx, s->gemm + L.first, s->terms, L.count, st);
         break;
       case HLU_K_RKT32: {
-        rc = hlu_rkt_phases(&s->ctx, s->rkt, s->parts, L.first, L.count, &s->scratch, slot++, st, s->side,
-                            s->ev_fork, s->ev_join);
+        rc = hlu_rkt_phases(&s->ctx, s->rkt, s->parts, L.first, L.count, &s->scratch, slot++, st, &s->aux);
         break;
       }
       case HLU_K_RKT64:
@@ -113,9 +111,8 @@ extern "C" int hlu_schedule_create(hlu_schedule **out, const hlu_ctx *ctx, const
     }
   }
   cudaStream_t st = (cudaStream_t)stream;
-  cudaStreamCreateWithFlags(&s->side, cudaStreamNonBlocking);
-  cudaEventCreateWithFlags(&s->ev_fork, cudaEventDisableTiming);
-  cudaEventCreateWithFlags(&s->ev_join, cudaEventDisableTiming);
+  for (int i = 0; i < 4; ++i) cudaStreamCreateWithFlags((cudaStream_t *)&s->aux.side[i], cudaStreamNonBlocking);
+  for (int i = 0; i < 8; ++i) cudaEventCreateWithFlags((cudaEvent_t *)&s->aux.ev[i], cudaEventDisableTiming);
   if (s->use_graph) {
     // make sure kernel attributes are set outside capture
     hlu_getrf_batched_f64(&s->ctx, s->getrf, 0, 0, st);
@@ -159,9 +156,8 @@ extern "C" int hlu_schedule_destroy(hlu_schedule *s) {
   if (s->exec) cudaGraphExecDestroy(s->exec);
   if (s->graph) cudaGraphDestroy(s->graph);
   if (s->stamps) cudaFree(s->stamps);
-  cudaEventDestroy(s->ev_fork);
-  cudaEventDestroy(s->ev_join);
-  cudaStreamDestroy(s->side);
+  for (int i = 0; i < 8; ++i) cudaEventDestroy((cudaEvent_t)s->aux.ev[i]);
+  for (int i = 0; i < 4; ++i) cudaStreamDestroy((cudaStream_t)s->aux.side[i]);
   delete s;
   return 0;
 }

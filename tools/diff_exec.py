@@ -53,7 +53,7 @@ def gpu_launch(li):
                                               call.d_terms.data_ptr(), count, st)
     call._scratch_keep[0].zero_()
     return lib.hlu_rkt_phases(ctx, call.d_rkt.data_ptr(), call.d_parts.data_ptr(), first, count,
-                              ctypes.byref(call.scratch), 0, st, st, None, None)
+                              ctypes.byref(call.scratch), 0, st, None)
 
 
 def strided(buf, v, ranks_):
