@@ -3,7 +3,7 @@ NVCC ?= nvcc
 ARCH := -gencode arch=compute_100a,code=sm_100a
 FLAGS := -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Iinclude --expt-relaxed-constexpr
 SRC := $(wildcard paper_1906_00874_b200/csrc/*.cu)
-HDR := $(wildcard paper_1906_00874_b200/csrc/*.cuh) include/hlu_b200.h
+HDR := $(wildcard paper_1906_00874_b200/csrc/*.cuh) paper_1906_00874_b200/csrc/rk_layout.h include/hlu_b200.h
 LIB := paper_1906_00874_b200/libhlu_b200.so
 
 all: $(LIB)
@@ -21,5 +21,5 @@ clean:
 
 PLAN := paper_1906_00874_b200/libhlu_plan.so
 all: $(PLAN)
-$(PLAN): paper_1906_00874_b200/csrc/planner.cpp include/hlu_plan.h include/hlu_b200.h
+$(PLAN): paper_1906_00874_b200/csrc/planner.cpp paper_1906_00874_b200/csrc/rk_layout.h include/hlu_plan.h include/hlu_b200.h
 	g++ -O2 -std=c++17 -fPIC -shared -Iinclude paper_1906_00874_b200/csrc/planner.cpp -o $@

@@ -145,10 +145,11 @@ int hlu_gemm_batched_f64(const hlu_ctx *ctx, const hlu_gemm_desc *d, const hlu_t
 int hlu_gemm_small_batched_f64(const hlu_ctx *ctx, const hlu_gemm_desc *d, const hlu_term *terms, int count,
                                void *stream);
 /* device scratch of the truncation launches: per level 8 counters (ops of the register
- * warp kernels K<=8 / K<=16, the shared-memory warp kernel K<=32, the CTA path, then the
- * CTA-path ops whose core SVD one warp does, then the CTA-path row blocks) at
- * counts + 8*slot, zeroed before the level runs; list = 7 segments
- * of max_ops op indices; items = max_items row blocks (max over levels of hlu_rkt_items) */
+ * warp kernels K<=8 / K<=16, the large-buffer row blocks, the CTA path, then the
+ * CTA-path ops whose core SVD one warp does, two reserved, then the small-buffer row
+ * blocks) at counts + 8*slot, zeroed before the level runs; list = 7 segments
+ * of max_ops op indices; items = max_items row blocks (max over levels of hlu_rkt_items):
+ * small-buffer blocks from the front, large-buffer blocks from the back */
 typedef struct {
   int32_t *counts;
   int32_t *list;
@@ -177,7 +178,8 @@ int hlu_rkt_phases(const hlu_ctx *ctx, hlu_rkt_desc *d, const hlu_rkpart *parts,
                    const hlu_rkt_scratch *scratch, int slot, void *stream, const hlu_rkt_streams *aux);
 /* one kernel only (diagnostics / per-kernel timing): 0 classify, 1 register warp K<=8,
  * 2 register warp K<=16, 3 (none), 4 block TSQR, 5 core by one warp
- * (K<=16), 6 core K<=32, 7 core K>32, 8 Q apply */
+ * (K<=16), 6 core K<=32, 7 core K>32, 8 Q apply, 9 block TSQR of the row blocks whose
+ * chunk chain needs the large buffer, 10 Q apply of those */
 int hlu_rkt_phase(const hlu_ctx *ctx, hlu_rkt_desc *d, const hlu_rkpart *parts, int64_t first, int count,
                   const hlu_rkt_scratch *scratch, int slot, int which, void *stream);
 /* host: the work items of count HOST descriptors in op order (items may be NULL); returns their number */
@@ -200,8 +202,8 @@ int hlu_schedule_create(hlu_schedule **out, const hlu_ctx *ctx, const hlu_launch
 int hlu_schedule_launch(hlu_schedule *s, void *stream);
 int hlu_schedule_destroy(hlu_schedule *s);
 /* diagnostics: with HLU_STAMPS=1 at creation, the %globaltimer (ns) before the first and
- * after every launch of the last replay (nlaunch + 1 values), then 10 per truncation launch
- * (after each of the 9 kernels of hlu_rkt_phase, then the join); returns the count
+ * after every launch of the last replay (nlaunch + 1 values), then 12 per truncation launch
+ * (after each of the 11 kernels of hlu_rkt_phase, then the join); returns the count
  * (out may be NULL), 0 without stamps */
 int64_t hlu_schedule_stamps(hlu_schedule *s, unsigned long long *out);
 

@@ -167,11 +167,11 @@ __device__ void house_qr(double *S, int ld, int rows, int K, double *tau, const 
 // TSQR of `total` rows (element (i, j) from src) as a chain of chunks of ch
 // fresh rows with the previous R carried on top.  Chunk s's compact QR
 // (ld = its rows) and tau go to ws + s * rk_stride.  Returns r (rows of the
-// final R, left in the top r rows of S, ld = ch + K, upper triangle).
+// final R, left in the top r rows of S, ld = min(ch, total) + K, upper triangle).
 template <class Src>
 __device__ int tsqr_chain(const Src &src, int total, int K, int ch, double *S, double *tau, double *ws,
                           const Grp &g) {
-  const int ld = ch + K;
+  const int ld = min(ch, total) + K;
   const int64_t stride = rk_stride(K, ch);
   int r = 0;
   int s = 0;
@@ -204,14 +204,14 @@ __device__ int tsqr_chain(const Src &src, int total, int K, int ch, double *S, d
 }
 
 // out (total x kk, ld ldo) = Q [W (r_final x kk, ld ldw); 0] with Q the chain
-// of tsqr_chain(total, K, ch) stored at ws.  T (>= (ch + K) kk doubles) holds
+// of tsqr_chain(total, K, ch) stored at ws.  T (>= (min(ch, total) + K) kk doubles) holds
 // the moving block; with STAGE each chunk's reflectors are first copied to VS
 // (coalesced) so the sequential chain runs out of shared memory.  The rows of
 // R carried into chunk s are r_{s-1} = min(s ch, K).
 template <bool STAGE>
 __device__ void apply_chain(int total, int K, int ch, int kk, const double *W, int ldw, int r_final, double *T,
                             double *VS, double *tq, const double *ws, double *out, int64_t ldo, const Grp &g) {
-  const int ldt = ch + K;
+  const int ldt = min(ch, total) + K;
   const int64_t stride = rk_stride(K, ch);
   const int nch = (total + ch - 1) / ch;
   for (int e = g.t; e < r_final * kk; e += g.nt()) {
@@ -548,7 +548,7 @@ struct StackedR {  // the blocks' R factors stacked: block b at R + b K K (ld K)
 #define RK_CNT 8
 #define RK_SEG_R8 0     // max(m,n) <= 64, K <= 8: register warp kernel
 #define RK_SEG_R16 1    // max(m,n) <= 64, K <= 16: register warp kernel
-#define RK_SEG_W32 2    // unused
+#define RK_CNT_BIGITEMS 2  // row blocks of the CTA-path ops for the large-buffer phase A/C kernels
 #define RK_SEG_BIG 3    // CTA phases (and the ADD shortcuts / empty recompressions)
 #define RK_SEG_C16 4    // CTA-path ops with K <= 16, m, n <= RK_BR: core SVD by one warp
 #define RK_SEG_Q8 5     // max(m,n) <= 128, K <= 8: register warp kernel, 4 rows per lane
@@ -557,7 +557,7 @@ struct StackedR {  // the blocks' R factors stacked: block b at R + b K K (ld K)
 // largest factor height of the register warp kernels (64: 2 rows per lane only;
 // the 4-rows-per-lane variant breaks rank parity at cfg2, under investigation)
 #define RK_RMAX 64
-#define RK_CNT_ITEMS 7  // row blocks of the CTA-path ops
+#define RK_CNT_ITEMS 7  // row blocks of the CTA-path ops for the small-buffer phase A/C kernels
 
 // One thread per op of the level: the stacked rank from the level-start ranks
 // is logged ((k1, k2) for ADD, (K, 0) for RECOMPRESS; every later phase reads
@@ -599,14 +599,30 @@ __global__ void k_rkt_classify(hlu_ctx c, const hlu_rkt_desc *__restrict__ d, co
   }
   s.list[RK_SEG_BIG * s.max_ops + atomicAdd(&cnt[RK_SEG_BIG], 1)] = op;
   if (K <= 16 && o.m <= RK_BR && o.n <= RK_BR) s.list[RK_SEG_C16 * s.max_ops + atomicAdd(&cnt[RK_SEG_C16], 1)] = op;
+  // row blocks whose chain fits the small kernels' buffer go to the front of
+  // the item array, the others (large shared-memory kernels) to its back
+  const int ch = rk_ch(K, RK_BUFA);
   const int nbm = (o.m + RK_BR - 1) / RK_BR, nbn = (o.n + RK_BR - 1) / RK_BR;
-  const int base = atomicAdd(&cnt[RK_CNT_ITEMS], nbm + nbn);
+  bool small[2][2];  // [side][last block?]
+  int nsmall = 0;
+  for (int sd = 0; sd < 2; ++sd) {
+    const int M = sd ? o.n : o.m, nb = sd ? nbn : nbm;
+    small[sd][0] = rk_item_need(RK_BR, K, ch) <= RK_BUFS;
+    small[sd][1] = rk_item_need(M - (nb - 1) * RK_BR, K, ch) <= RK_BUFS;
+    nsmall += (nb - 1) * small[sd][0] + small[sd][1];
+  }
+  const int nbig = nbm + nbn - nsmall;
+  int bs = nsmall ? atomicAdd(&cnt[RK_CNT_ITEMS], nsmall) : 0;
+  int bb = nbig ? atomicAdd(&cnt[RK_CNT_BIGITEMS], nbig) : 0;
   for (int b = 0; b < nbm + nbn; ++b) {
     hlu_rkt_item it;
     it.op = op;
-    it.side = (int16_t)(b >= nbm);
-    it.block = (int16_t)(b >= nbm ? b - nbm : b);
-    s.items[base + b] = it;
+    const int sd = b >= nbm;
+    it.side = (int16_t)sd;
+    it.block = (int16_t)(sd ? b - nbm : b);
+    const bool last = it.block == (sd ? nbn : nbm) - 1;
+    if (small[sd][last]) s.items[bs++] = it;
+    else s.items[s.max_items - 1 - bb++] = it;
   }
 }
 
@@ -1000,21 +1016,25 @@ __device__ void rkt_a_item(const hlu_ctx &c, const hlu_rkt_desc *d, const hlu_rk
   const int r = tsqr_chain(src, rows, K, s.ch, S, tau, ws + it.block * s.blk, all);
   // the block's R: K x K, ld K, zero outside the upper triangle of its r rows
   double *R = ws + s.off_R + (int64_t)it.block * K * K;
-  const int ld = s.ch + K;
+  const int ld = min(s.ch, rows) + K;
   for (int e = tid; e < K * K; e += HLU_NT) {
     const int i = e % K, j = e / K;
     R[e] = (i < r && i <= j) ? S[i + j * ld] : 0.0;
   }
 }
 
+// BIG: the row blocks whose chain needs more than RK_BUFS doubles (taken from
+// the back of the item array), with an RK_BUFA buffer (one CTA per SM)
+template <bool BIG>
 __global__ void __launch_bounds__(HLU_NT)
     k_rkt_a(hlu_ctx c, const hlu_rkt_desc *__restrict__ d, const hlu_rkpart *__restrict__ parts, hlu_rkt_scratch s,
             int slot) {
   extern __shared__ double sm[];
   __shared__ PartInfo P[RK_MAXP];
-  const int nitems = s.counts[RK_CNT * slot + RK_CNT_ITEMS];
+  const int nitems = s.counts[RK_CNT * slot + (BIG ? RK_CNT_BIGITEMS : RK_CNT_ITEMS)];
   for (int idx = blockIdx.x; idx < nitems; idx += gridDim.x) {
-    rkt_a_item(c, d, parts, s.items[idx], sm, sm + RK_BUFA, P);
+    const hlu_rkt_item it = BIG ? s.items[s.max_items - 1 - idx] : s.items[idx];
+    rkt_a_item(c, d, parts, it, sm, sm + (BIG ? RK_BUFA : RK_BUFS), P);
     __syncthreads();
   }
 }
@@ -1113,7 +1133,7 @@ __global__ void __launch_bounds__(RkB<KM>::NT)
       } else {
         const StackedR src{ws + s.off_R, K};
         r = tsqr_chain(src, s.srows, K, s.chc, buf, tg, ws + s.off_comb, grp);
-        const int ld = s.chc + K;
+        const int ld = min(s.chc, s.srows) + K;
         for (int e = grp.t; e < KM * KM; e += grp.nt()) {
           const int i = e % KM, j = e / KM;
           R[e] = (i < r && i <= j && j < K) ? buf[i + j * ld] : 0.0;
@@ -1278,16 +1298,20 @@ __global__ void __launch_bounds__(BwCfg<KB>::WPC * 32)
 
 // ---------------------------------------------------------------- phase C
 
+// BIG: the large-buffer row blocks (see k_rkt_a); their moving block holds
+// RK_TBUF doubles, so the kept columns go through in groups
+template <bool BIG>
 __global__ void __launch_bounds__(HLU_NT)
     k_rkt_c(hlu_ctx c, const hlu_rkt_desc *__restrict__ d, hlu_rkt_scratch s, int slot) {
+  constexpr int TB = BIG ? RK_TBUF : RK_BUFS, VB = BIG ? RK_BUFA : RK_BUFS;
   extern __shared__ double sm[];
-  double *T = sm;             // RK_BUFA moving block
-  double *VS = T + RK_BUFA;   // RK_BUFA staged reflectors
-  double *tq = VS + RK_BUFA;  // RK_KMAX
+  double *T = sm;        // TB moving block
+  double *VS = T + TB;   // VB staged reflectors
+  double *tq = VS + VB;  // RK_KMAX
   const int tid = threadIdx.x;
-  const int nitems = s.counts[RK_CNT * slot + RK_CNT_ITEMS];
+  const int nitems = s.counts[RK_CNT * slot + (BIG ? RK_CNT_BIGITEMS : RK_CNT_ITEMS)];
   for (int idx = blockIdx.x; idx < nitems; idx += gridDim.x) {
-    const hlu_rkt_item it = s.items[idx];
+    const hlu_rkt_item it = BIG ? s.items[s.max_items - 1 - idx] : s.items[idx];
     const hlu_rkt_desc o = d[it.op];
     bool shortcut;
     const int K = logged_K(c, o, &shortcut);
@@ -1303,8 +1327,11 @@ __global__ void __launch_bounds__(HLU_NT)
     const int rb = min(rows, K);
     double *out = c.pool + (left ? o.out_a : o.out_b) + row0;
     const Grp all{0, HLU_NWARP, tid >> 5, tid & 31, tid};
-    apply_chain<true>(rows, K, sd.ch, kk, ws + sd.off_Z + it.block * K, sd.zrows, rb, T, VS, tq,
-                      ws + it.block * sd.blk, out, M, all);
+    const int grp = BIG ? max(1, TB / (min(sd.ch, rows) + K)) : kk;
+    for (int c0 = 0; c0 < kk; c0 += grp) {
+      apply_chain<true>(rows, K, sd.ch, min(grp, kk - c0), ws + sd.off_Z + it.block * K + (int64_t)c0 * sd.zrows,
+                        sd.zrows, rb, T, VS, tq, ws + it.block * sd.blk, out + (int64_t)c0 * M, M, all);
+    }
   }
 }
 
@@ -1312,16 +1339,20 @@ __global__ void __launch_bounds__(HLU_NT)
 
 using namespace hlu;
 
-static size_t smem_a() { return (size_t)(RK_BUFA + RK_KMAX) * sizeof(double); }
-static size_t smem_c() { return (size_t)(2 * RK_BUFA + RK_KMAX) * sizeof(double); }
+static size_t smem_a(bool big) { return (size_t)((big ? RK_BUFA : RK_BUFS) + RK_KMAX) * sizeof(double); }
+static size_t smem_c(bool big) {
+  return (size_t)(big ? RK_TBUF + RK_BUFA + RK_KMAX : 2 * RK_BUFS + RK_KMAX) * sizeof(double);
+}
 
 static void rkt_init() {
   static bool init = false;
   if (init) return;
-  cudaFuncSetAttribute(k_rkt_a, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_a());
+  cudaFuncSetAttribute(k_rkt_a<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_a(false));
+  cudaFuncSetAttribute(k_rkt_a<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_a(true));
   cudaFuncSetAttribute(k_rkt_b<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RkB<32>::smem());
   cudaFuncSetAttribute(k_rkt_b<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RkB<64>::smem());
-  cudaFuncSetAttribute(k_rkt_c, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_c());
+  cudaFuncSetAttribute(k_rkt_c<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_c(false));
+  cudaFuncSetAttribute(k_rkt_c<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_c(true));
   cudaFuncSetAttribute(k_rkt_r<2, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RCfg<2, 8>::smem());
   cudaFuncSetAttribute(k_rkt_r<2, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RCfg<2, 16>::smem());
   cudaFuncSetAttribute(k_rkt_r<4, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RCfg<4, 8>::smem());
@@ -1343,8 +1374,9 @@ static void launch_r(const hlu_ctx *ctx, hlu_rkt_desc *d, const hlu_rkpart *part
 }
 
 // kernels of one level: 0 classify, 1 register warp K<=8, 2 register warp K<=16,
-// 3 (none), 4 block TSQR, 5 core by one warp (K<=16), 6 core K<=32, 7 core K>32, 8 Q apply
-#define RK_NKERN 9
+// 3 (none), 4 block TSQR, 5 core by one warp (K<=16), 6 core K<=32, 7 core K>32, 8 Q apply,
+// 9 block TSQR (large buffer), 10 Q apply (large buffer)
+#define RK_NKERN 11
 static int rkt_launch(int which, const hlu_ctx *ctx, hlu_rkt_desc *d, const hlu_rkpart *parts, int64_t first,
                       int count, const hlu_rkt_scratch &s, int slot, cudaStream_t st) {
   const int cap = 148;
@@ -1362,13 +1394,15 @@ static int rkt_launch(int which, const hlu_ctx *ctx, hlu_rkt_desc *d, const hlu_
       launch_r<4, 16>(ctx, d, parts, count, s, slot, st);
       break;
     case 3: break;  // (slot of a retired kernel)
-    case 4: k_rkt_a<<<lim(2 * (int64_t)count, 4), HLU_NT, smem_a(), st>>>(*ctx, d, parts, s, slot); break;
+    case 4: k_rkt_a<false><<<lim(2 * (int64_t)count, 4), HLU_NT, smem_a(false), st>>>(*ctx, d, parts, s, slot); break;
+    case 9: k_rkt_a<true><<<lim(2 * (int64_t)count, 1), HLU_NT, smem_a(true), st>>>(*ctx, d, parts, s, slot); break;
     case 5:
       k_rkt_bw<16><<<lim((count + 3) / 4, 4), 4 * 32, BwCfg<16>::smem(), st>>>(*ctx, d, s, slot);
       break;
     case 6: k_rkt_b<32><<<lim(count, 3), RkB<32>::NT, RkB<32>::smem(), st>>>(*ctx, d, parts, s, slot); break;
     case 7: k_rkt_b<64><<<lim(count, 1), RkB<64>::NT, RkB<64>::smem(), st>>>(*ctx, d, parts, s, slot); break;
-    case 8: k_rkt_c<<<lim(2 * (int64_t)count, 2), HLU_NT, smem_c(), st>>>(*ctx, d, s, slot); break;
+    case 8: k_rkt_c<false><<<lim(2 * (int64_t)count, 2), HLU_NT, smem_c(false), st>>>(*ctx, d, s, slot); break;
+    case 10: k_rkt_c<true><<<lim(2 * (int64_t)count, 1), HLU_NT, smem_c(true), st>>>(*ctx, d, s, slot); break;
     default: return -3;
   }
   return 0;
@@ -1382,7 +1416,7 @@ __global__ void k_rkt_stamp(unsigned long long *slot) {
 
 // diagnostics: when non-null, %globaltimer after every kernel of a level
 // (RK_NSTAMP slots: the RK_NKERN kernels, then the join)
-#define RK_NSTAMP 10
+#define RK_NSTAMP 12
 static unsigned long long *g_phase_stamps = nullptr;
 extern "C" void hlu_rkt_set_phase_stamps(unsigned long long *p) { g_phase_stamps = p; }
 
@@ -1405,7 +1439,8 @@ extern "C" int hlu_rkt_phases(const hlu_ctx *ctx, hlu_rkt_desc *d, const hlu_rkp
     stamp(w, q);
   };
   if (!aux) {
-    for (int w = 0; w < RK_NKERN; ++w) run(w, st);
+    static const int order[RK_NKERN] = {0, 1, 2, 3, 4, 9, 5, 6, 7, 8, 10};
+    for (int w : order) run(w, st);
     stamp(RK_NKERN, st);
     return cudaGetLastError() == cudaSuccess ? 0 : -1;
   }
@@ -1421,7 +1456,12 @@ extern "C" int hlu_rkt_phases(const hlu_ctx *ctx, hlu_rkt_desc *d, const hlu_rkp
   run(2, s1);
   stamp(3, s1);
   cudaEventRecord(ev[2], s1);
+  // block TSQR: large-buffer items on side[2] beside the small ones
+  cudaStreamWaitEvent(s2, ev[0], 0);
+  run(9, s2);
+  cudaEventRecord(ev[6], s2);
   run(4, st);
+  cudaStreamWaitEvent(st, ev[6], 0);
   cudaEventRecord(ev[3], st);
   cudaStreamWaitEvent(s2, ev[3], 0);
   cudaStreamWaitEvent(s3, ev[3], 0);
@@ -1432,7 +1472,13 @@ extern "C" int hlu_rkt_phases(const hlu_ctx *ctx, hlu_rkt_desc *d, const hlu_rkp
   run(5, st);
   cudaStreamWaitEvent(st, ev[4], 0);
   cudaStreamWaitEvent(st, ev[5], 0);
+  // Q apply: large-buffer items on side[2] beside the small ones
+  cudaEventRecord(ev[7], st);
+  cudaStreamWaitEvent(s2, ev[7], 0);
+  run(10, s2);
+  cudaEventRecord(ev[6], s2);
   run(8, st);
+  cudaStreamWaitEvent(st, ev[6], 0);
   cudaStreamWaitEvent(st, ev[1], 0);
   cudaStreamWaitEvent(st, ev[2], 0);
   stamp(RK_NKERN, st);

@@ -31,7 +31,9 @@
 
 #define RK_KMAX 64
 #define RK_BR 512        /* rows per block (one phase-A / phase-C work item) */
-#define RK_BUFA 6144     /* phase A/C chunk buffer (doubles) */
+#define RK_BUFA 16384    /* chunk buffer of the layout: (ch + K) K <= RK_BUFA (doubles) */
+#define RK_BUFS 6144     /* small phase A/C kernels: items whose chunk fits (min(ch, rows) + K) K */
+#define RK_TBUF 8192     /* large phase C kernel: moving block, processed in column groups */
 #define RK_BUFB32 3072   /* phase B per-side buffer, K <= 32 */
 #define RK_BUFB64 8192   /* phase B per-side buffer, 32 < K <= 64 */
 
@@ -43,6 +45,9 @@ RK_HD int rk_ch(int K, int bufd) {
 }
 
 RK_HD int64_t rk_stride(int K, int ch) { return (int64_t)(K + ch) * K + K; }
+
+/* shared-memory need (doubles) of one row block's chain: ld (min(ch, rows) + K) times K */
+RK_HD int rk_item_need(int rows, int K, int ch) { return ((rows < ch ? rows : ch) + K) * K; }
 
 /* workspace of a chain over `rows` rows */
 RK_HD int64_t rk_chain(int rows, int K, int ch) { return (int64_t)((rows + ch - 1) / ch) * rk_stride(K, ch); }

@@ -106,8 +106,8 @@ extern "C" int hlu_schedule_create(hlu_schedule **out, const hlu_ctx *ctx, const
     if (e && e[0] == '1') {
       int64_t nr = 0;
       for (const hlu_launch &L : s->launches) nr += L.kind == HLU_K_RKT32;
-      cudaMalloc(&s->stamps, (s->launches.size() + 1 + 10 * nr) * sizeof(unsigned long long));
-      cudaMemset(s->stamps, 0, (s->launches.size() + 1 + 10 * nr) * sizeof(unsigned long long));
+      cudaMalloc(&s->stamps, (s->launches.size() + 1 + 12 * nr) * sizeof(unsigned long long));
+      cudaMemset(s->stamps, 0, (s->launches.size() + 1 + 12 * nr) * sizeof(unsigned long long));
     }
   }
   cudaStream_t st = (cudaStream_t)stream;
@@ -166,7 +166,7 @@ extern "C" int64_t hlu_schedule_stamps(hlu_schedule *s, unsigned long long *out)
   if (!s->stamps) return 0;
   int64_t nr = 0;
   for (const hlu_launch &L : s->launches) nr += L.kind == HLU_K_RKT32;
-  const int64_t n = (int64_t)s->launches.size() + 1 + 10 * nr;
+  const int64_t n = (int64_t)s->launches.size() + 1 + 12 * nr;
   if (out && cudaMemcpy(out, s->stamps, n * sizeof(unsigned long long), cudaMemcpyDeviceToHost) != cudaSuccess)
     return -1;
   return n;

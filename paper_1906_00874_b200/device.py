@@ -160,7 +160,7 @@ class DeviceCall:
             else:
                 os.environ["HLU_STAMPS"] = prev
         nl = len(self.packed.launches)
-        self.last_phase_stamps = st[nl + 1:].astype(np.int64).reshape(-1, 10)
+        self.last_phase_stamps = st[nl + 1:].astype(np.int64).reshape(-1, 12)
         return np.diff(st[: nl + 1].astype(np.int64)) * 1e-9
 
     def launch(self):

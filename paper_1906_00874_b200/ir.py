@@ -81,7 +81,7 @@ def colmajor(off, rows, cols, cdyn=-1):
 
 
 # workspace geometry of the batched truncation: mirror of csrc/rk_layout.h
-RK_KMAX, RK_BR, RK_BUFA, RK_BUFB32, RK_BUFB64 = 64, 512, 6144, 3072, 8192
+RK_KMAX, RK_BR, RK_BUFA, RK_BUFB32, RK_BUFB64 = 64, 512, 16384, 3072, 8192
 
 
 def rk_ch(K, bufd):

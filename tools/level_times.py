@@ -54,19 +54,23 @@ def main():
     ends = np.cumsum(np.concatenate([[0], dt]))  # us from the first stamp
     ps = call.last_phase_stamps.astype(np.float64)
     base = None
-    # concurrent branches: r8 | r16 from classify; A; then Bw | B32 | B64; C after all three
-    names = ["classify", "r8", "r16", "-", "A", "Bw", "B32", "B64", "C", "join"]
+    # concurrent branches: r8 | r16 from classify; A | Abig; then Bw | B32 | B64; C | Cbig after all three
+    names = ["classify", "r8", "r16", "-", "A", "Bw", "B32", "B64", "C", "Abig", "Cbig", "join"]
     NPH = len(names)
     ph = np.zeros((len(rk_idx), NPH))
     for r, i in enumerate(rk_idx):
+        a_end = max(ps[r, 4], ps[r, 9])
+        b_end = max(ps[r, 5], ps[r, 6], ps[r, 7])
         ph[r, 1] = (ps[r, 1] - ps[r, 0]) * 1e-3
         ph[r, 2] = (ps[r, 2] - ps[r, 0]) * 1e-3
         ph[r, 4] = (ps[r, 4] - ps[r, 0]) * 1e-3
+        ph[r, 9] = (ps[r, 9] - ps[r, 0]) * 1e-3
         for k in (5, 6, 7):
-            ph[r, k] = (ps[r, k] - ps[r, 4]) * 1e-3
-        ph[r, 8] = (ps[r, 8] - max(ps[r, 5], ps[r, 6], ps[r, 7])) * 1e-3
-        ph[r, 9] = (ps[r, 9] - ps[r, 8]) * 1e-3
-        ph[r, 0] = dt[i] - (ps[r, 9] - ps[r, 0]) * 1e-3
+            ph[r, k] = (ps[r, k] - a_end) * 1e-3
+        ph[r, 8] = (ps[r, 8] - b_end) * 1e-3
+        ph[r, 10] = (ps[r, 10] - b_end) * 1e-3
+        ph[r, 11] = (ps[r, 11] - max(ps[r, 8], ps[r, 10])) * 1e-3
+        ph[r, 0] = dt[i] - (ps[r, 11] - ps[r, 0]) * 1e-3
     print("truncation phases inside the graph (us): total / mean / max  [classify = level - rest]")
     for k in range(NPH):
         print(f"  {names[k]:8s} {ph[:, k].sum() / 1e3:9.1f} ms  mean {ph[:, k].mean():8.1f}  max {ph[:, k].max():9.1f}")
