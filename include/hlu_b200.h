@@ -131,8 +131,9 @@ typedef struct {
   int32_t kind;
   int32_t count;
   int64_t first;     /* index of the first descriptor of this launch */
-  int32_t smem_dim;  /* largest square dimension (getrf / trsm) */
-  int32_t pad;
+  int32_t smem_dim;  /* largest square dimension (getrf / trsm); truncation launches: 1 when
+                        they read a temp a dense launch of the same level produces */
+  int32_t level;     /* schedule level: launches of one level are independent */
 } hlu_launch; /* 24 bytes */
 
 /* --- batched kernels (descriptor arrays are device pointers) --- */
@@ -211,6 +212,9 @@ int64_t hlu_schedule_stamps(hlu_schedule *s, unsigned long long *out);
 const char *hlu_version(void);
 int hlu_device_check(void); /* 0 when a sm_100 device is present */
 int64_t hlu_debug_sweeps(int reset); /* total Jacobi sweeps run so far (diagnostics) */
+/* core-kernel phase cycles [K<=32 | K>32][op count, R/combine, core product, QRCP, Jacobi,
+ * rank, W + QRCP apply, combine apply] (16 values; zeros unless built with -DHLU_BPROF) */
+int hlu_debug_bprof(unsigned long long *out, int reset);
 
 #ifdef __cplusplus
 }

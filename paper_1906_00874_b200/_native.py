@@ -11,7 +11,8 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libhlu_b200.so")
+# HLU_LIB selects a diagnostics build of the same library (e.g. libhlu_b200_prof.so)
+LIB_PATH = os.path.join(_HERE, os.environ.get("HLU_LIB", "libhlu_b200.so"))
 
 SYMBOLS = (
     "hlu_getrf_batched_f64",
@@ -30,6 +31,7 @@ SYMBOLS = (
     "hlu_version",
     "hlu_device_check",
     "hlu_debug_sweeps",
+    "hlu_debug_bprof",
 )
 
 
@@ -85,6 +87,8 @@ def lib():
     L.hlu_rkt_ws_doubles.restype = i64
     L.hlu_debug_sweeps.argtypes = [i32]
     L.hlu_debug_sweeps.restype = i64
+    L.hlu_debug_bprof.argtypes = [vp, i32]
+    L.hlu_debug_bprof.restype = ctypes.c_int
     L.hlu_schedule_create.argtypes = [ctypes.POINTER(vp), ctypes.POINTER(HluCtx), vp, i64,
                                       vp, vp, vp, vp, vp, vp, sp, i32, vp]
     L.hlu_schedule_launch.argtypes = [vp, vp]

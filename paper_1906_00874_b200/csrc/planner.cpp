@@ -766,6 +766,7 @@ struct Planner {
   // ---------------------------------------------------------- schedule
   std::vector<int64_t> levels;
   std::vector<int64_t> toffs;
+  std::vector<int64_t> tbirth;  // level of each temp's producer
   int64_t arena = 0;
 
   // Hazard state: slots in segment trees (reads can span whole partitioned
@@ -891,6 +892,7 @@ struct Planner {
       }
       for (int64_t k = o.ti_begin; k < o.ti_end; ++k) death[tids[k]] = std::max(death[tids[k]], lv);
     }
+    tbirth = birth;
     std::vector<int> cls(nt);
     for (int64_t t = 0; t < nt; ++t) {
       const int64_t s = std::max<int64_t>(temp_size[t], 1);
@@ -1060,6 +1062,8 @@ struct Planner {
       int kind;
       int64_t count, first;
       int dim;
+      int64_t lv;
+      bool dep;  // truncation launch reading a temp produced in the same level
     };
     std::vector<Rec> recs;
     int64_t cur_lv = -1;
@@ -1079,7 +1083,7 @@ struct Planner {
           o_terms.insert(o_terms.end(), c.terms.begin(), c.terms.end());
           o_gemm.push_back(d);
         }
-        recs.push_back(Rec{pass == 0 ? HLU_K_GEMM : HLU_K_GEMM_SMALL, (int64_t)st.size(), first, 0});
+        recs.push_back(Rec{pass == 0 ? HLU_K_GEMM : HLU_K_GEMM_SMALL, (int64_t)st.size(), first, 0, pending_lv, false});
         st.clear();
       }
       cur_kind = -1;
@@ -1156,11 +1160,15 @@ struct Planner {
         idx = (int64_t)o_rkt.size() - 1;
         dim = r.kb;
       }
+      bool dep = false;
+      if (kind == HLU_K_RKT32)
+        for (int64_t k = o.ti_begin; k < o.ti_end; ++k) dep = dep || tbirth[tids[k]] == lv;
       if (!recs.empty() && cur_lv == lv && cur_kind == kind) {
         recs.back().count += 1 + extra;
         recs.back().dim = std::max(recs.back().dim, dim);
+        recs.back().dep = recs.back().dep || dep;
       } else {
-        recs.push_back(Rec{kind, 1 + extra, idx, dim});
+        recs.push_back(Rec{kind, 1 + extra, idx, dim, lv, dep});
         cur_lv = lv;
         cur_kind = kind;
       }
@@ -1171,9 +1179,9 @@ struct Planner {
       L.kind = r.kind;
       L.count = (int32_t)r.count;
       L.first = r.first;
-      L.pad = 0;
+      L.level = (int32_t)r.lv;
       if (r.kind == HLU_K_RKT32) {
-        L.smem_dim = 0;
+        L.smem_dim = r.dep ? 1 : 0;
         o_launch.push_back(L);
       } else {
         L.smem_dim = r.dim;

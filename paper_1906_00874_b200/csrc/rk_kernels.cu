@@ -398,6 +398,135 @@ __device__ void qrcp(double *G, int p, int q, double *tau, int *cm, double *nrm)
   }
 }
 
+// Same factorization as qrcp (same storage contract: cm, tau, reflector j
+// below row j of column cm[j], R row j in row j), one barrier per step: every
+// warp selects the pivot (largest remaining norm, smallest column on ties)
+// and builds the reflector itself from the raw pivot column, applies it to
+// its own columns (c = w mod NW) and recomputes their norms; the pivot
+// column's owner writes the reflector back after the barrier, when no warp
+// reads that column any more.  p <= 64 (two rows per lane), q <= 64.
+template <int KM, int NT>
+__device__ void qrcp_fast(double *G, int p, int q, double *tau, int *cm, double *nrm) {
+  constexpr int NW = NT / 32;
+  constexpr int NB = (KM + NW - 1) / NW;
+  const int tid = threadIdx.x, w = tid >> 5, l = tid & 31;
+  for (int c = w; c < q; c += NW) {
+    double ss = 0.0;
+    for (int i = l; i < p; i += 32) ss = fma(G[i + c * KM], G[i + c * KM], ss);
+    ss = warp_sum(ss);
+    if (l == 0) nrm[c] = ss;
+  }
+  __syncthreads();
+  unsigned long long done = 0ull;
+  int prev = -1, prev_j = 0;
+  double pv0 = 0.0, pv1 = 0.0, pbeta = 0.0;
+  for (int j = 0; j < q; ++j) {
+    if (prev >= 0 && prev % NW == w) {  // deferred write-back of the previous reflector
+      if (l > prev_j && l < p) G[l + prev * KM] = pv0;
+      if (l + 32 > prev_j && l + 32 < p) G[l + 32 + prev * KM] = pv1;
+      if (l == 0) G[prev_j + prev * KM] = pbeta;
+    }
+    double best = -1.0;
+    int bi = 64;
+    for (int c = l; c < q; c += 32) {
+      if ((done >> c) & 1ull) continue;
+      const double v = nrm[c];
+      if (v > best || (v == best && c < bi)) {
+        best = v;
+        bi = c;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ob > best || (ob == best && oi < bi)) {
+        best = ob;
+        bi = oi;
+      }
+    }
+    done |= 1ull << bi;
+    const double *x = G + bi * KM;
+    const double x0 = (l > j && l < p) ? x[l] : 0.0;
+    const double x1 = (l + 32 > j && l + 32 < p) ? x[l + 32] : 0.0;
+    const double ss = warp_sum(fma(x0, x0, x1 * x1));
+    const double alpha = x[j];
+    double tj = 0.0, beta = alpha, sc = 0.0;
+    if (ss != 0.0) {
+      const double n2 = fma(alpha, alpha, ss);
+      const double rn = fast_rsqrt(n2);
+      beta = -copysign(n2 * rn, alpha);
+      tj = fma(fabs(alpha), rn, 1.0);
+      sc = fast_rcp(alpha - beta);
+    }
+    const double v0 = x0 * sc, v1 = x1 * sc;
+    int pc[NB];
+    bool act[NB];
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      pc[b] = w + b * NW;
+      act[b] = pc[b] < q && !((done >> pc[b]) & 1ull);
+    }
+    double acc[NB];
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      acc[b] = 0.0;
+      if (act[b] && tj != 0.0) {
+        const double *g = G + pc[b] * KM;
+        acc[b] = fma(v0, (l < p) ? g[l] : 0.0, (l + 32 < p) ? v1 * g[l + 32] : 0.0);
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+      for (int b = 0; b < NB; ++b) acc[b] += __shfl_xor_sync(0xffffffffu, acc[b], o);
+    }
+    double ns[NB];
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      ns[b] = 0.0;
+      if (!act[b]) continue;
+      double *g = G + pc[b] * KM;
+      if (tj != 0.0) {
+        const double f = tj * (acc[b] + g[j]);
+        if (l > j && l < p) g[l] = fma(-f, v0, g[l]);
+        if (l + 32 > j && l + 32 < p) g[l + 32] = fma(-f, v1, g[l + 32]);
+        __syncwarp();
+        if (l == 0) g[j] -= f;
+      }
+      const double a0 = (l > j && l < p) ? g[l] : 0.0;
+      const double a1 = (l + 32 > j && l + 32 < p) ? g[l + 32] : 0.0;
+      ns[b] = fma(a0, a0, a1 * a1);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+      for (int b = 0; b < NB; ++b) ns[b] += __shfl_xor_sync(0xffffffffu, ns[b], o);
+    }
+    if (l == 0) {
+#pragma unroll
+      for (int b = 0; b < NB; ++b)
+        if (act[b]) nrm[pc[b]] = ns[b];
+    }
+    if (tid == 0) {
+      cm[j] = bi;
+      tau[j] = tj;
+    }
+    prev = bi;
+    prev_j = j;
+    pv0 = v0;
+    pv1 = v1;
+    pbeta = beta;
+    __syncthreads();
+  }
+  if (prev >= 0 && prev % NW == w) {
+    if (l > prev_j && l < p) G[l + prev * KM] = pv0;
+    if (l + 32 > prev_j && l + 32 < p) G[l + 32 + prev * KM] = pv1;
+    if (l == 0) G[prev_j + prev * KM] = pbeta;
+  }
+  __syncthreads();
+}
+
 // z (p rows, stride 1) <- Q [z(0:q); 0] with the qrcp reflectors; one warp.
 template <int KM>
 __device__ void qrcp_apply(const double *G, int p, int q, const double *tau, const int *cm, double *z) {
@@ -1041,6 +1170,17 @@ __global__ void __launch_bounds__(HLU_NT)
 
 // ---------------------------------------------------------------- phase B
 
+// phase profiler of the core kernel (diagnostics build: -DHLU_BPROF): clock64
+// cycles per phase accumulated by thread 0, [KM == 64][phase], slot 0 = op count
+#ifdef HLU_BPROF
+__device__ unsigned long long g_bprof[2][8];
+#define BPROF_START() long long bp_t = clock64(); if (tid == 0) atomicAdd(&g_bprof[KM == 64][0], 1ull)
+#define BPROF(k) do { if (tid == 0) { const long long t_ = clock64(); atomicAdd(&g_bprof[KM == 64][k], (unsigned long long)(t_ - bp_t)); bp_t = t_; } } while (0)
+#else
+#define BPROF_START() do {} while (0)
+#define BPROF(k) do {} while (0)
+#endif
+
 template <int KM>
 struct RkB {
   static constexpr int BUF = KM == 32 ? RK_BUFB32 : RK_BUFB64;
@@ -1108,6 +1248,7 @@ __global__ void __launch_bounds__(RkB<KM>::NT)
     }
     if ((KM == 32) != (K <= 32)) continue;
     if (K <= 16 && m <= RK_BR && n <= RK_BR) continue;  // k_rkt_bw
+    BPROF_START();
     const rk_side_t sa = rk_side(m, K), sb = rk_side(n, K);
     double *wsA = c.pool + o.ws;
     double *wsB = wsA + sa.total;
@@ -1142,6 +1283,7 @@ __global__ void __launch_bounds__(RkB<KM>::NT)
       if (grp.t == 0) (left ? s_ra : s_rb) = r;
     }
     __syncthreads();
+    BPROF(1);
     const int ra = s_ra, rb = s_rb;
     // core M = R_a R_b^T (ra x rb); G = M or M^T so that G has q <= p columns
     const bool tr = rb > ra;
@@ -1155,9 +1297,10 @@ __global__ void __launch_bounds__(RkB<KM>::NT)
       else G[i + j * KM] = acc;
     }
     __syncthreads();
+    BPROF(2);
     // SVD of G via QR with column pivoting + one-sided Jacobi on R^T
     // (G P = Q R, R^T V = W = U S  =>  G = (Q V) S (P U)^T)
-    qrcp<KM, NT>(G, p, q, tau, cmap, sig);
+    qrcp_fast<KM, NT>(G, p, q, tau, cmap, sig);
     for (int e = tid; e < KM * KM; e += NT) {
       const int i = e % KM, j = e / KM;  // XT[i, j] = R[j, i]
       XT[e] = (i < q && j < q && j <= i) ? G[j + cmap[i] * KM] : 0.0;
@@ -1165,6 +1308,7 @@ __global__ void __launch_bounds__(RkB<KM>::NT)
     const int qq = q + (q & 1);
     build_pairs<NT>(pairs_a, pairs_b, qq);
     __syncthreads();
+    BPROF(3);
     jacobi<KM, NT>(XT, V, q, pairs_a, pairs_b);
     // singular values, order, rank
     for (int j = tid; j < q; j += NT) {
@@ -1173,6 +1317,7 @@ __global__ void __launch_bounds__(RkB<KM>::NT)
       sig[j] = sqrt(ss);
     }
     __syncthreads();
+    BPROF(4);
     for (int j = tid; j < q; j += NT) {
       int rk = 0;
       const double sj = sig[j];
@@ -1195,6 +1340,7 @@ __global__ void __launch_bounds__(RkB<KM>::NT)
       s_kk = kk;
     }
     __syncthreads();
+    BPROF(5);
     const int kk = s_kk;
     // W_a (ra x kk) -> RA, W_b (rb x kk) -> RB.
     //   G = M  (!tr): W_a = Q (V S)_sel,  W_b = P W_sel / S
@@ -1214,6 +1360,7 @@ __global__ void __launch_bounds__(RkB<KM>::NT)
     __syncthreads();
     for (int col = wq; col < kk; col += NW) qrcp_apply<KM>(G, p, q, tau, cmap, WQ + col * KM);
     __syncthreads();
+    BPROF(6);
     // Z = combine-level Q [W; 0] (or W itself for a single-block factor)
     {
       const bool left = wq < NW / 2;
@@ -1238,6 +1385,7 @@ __global__ void __launch_bounds__(RkB<KM>::NT)
       c.log[o.log + 2] = kk;
     }
     __syncthreads();
+    BPROF(7);
   }
 }
 
@@ -1519,6 +1667,22 @@ extern "C" int64_t hlu_rkt_items(const hlu_rkt_desc *d, int count, hlu_rkt_item 
     }
   }
   return n;
+}
+
+// diagnostics: core-kernel phase cycles (16 values; zeros unless built with -DHLU_BPROF)
+extern "C" int hlu_debug_bprof(unsigned long long *out, int reset) {
+#ifdef HLU_BPROF
+  cudaDeviceSynchronize();
+  if (cudaMemcpyFromSymbol(out, g_bprof, sizeof(g_bprof)) != cudaSuccess) return -1;
+  if (reset) {
+    static const unsigned long long z[16] = {0};
+    cudaMemcpyToSymbol(g_bprof, z, sizeof(z));
+  }
+#else
+  for (int i = 0; i < 16; ++i) out[i] = 0;
+  (void)reset;
+#endif
+  return 0;
 }
 
 extern "C" int64_t hlu_debug_sweeps(int reset) {

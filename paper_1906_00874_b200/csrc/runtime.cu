@@ -29,6 +29,8 @@ struct hlu_schedule {
   cudaGraphExec_t exec;
   bool use_graph;
   unsigned long long *stamps;  // diagnostics: %globaltimer after every launch (HLU_STAMPS=1)
+  cudaStream_t dense;          // getrf / trsm / gemm launches of a level that also truncates
+  cudaEvent_t fork, join;
 };
 
 __global__ void k_stamp(unsigned long long *slot) {
@@ -37,38 +39,60 @@ __global__ void k_stamp(unsigned long long *slot) {
   *slot = t;
 }
 
+static int launch_one(hlu_schedule *s, const hlu_launch &L, int &slot, cudaStream_t st) {
+  switch (L.kind) {
+    case HLU_K_GETRF: return hlu_getrf_batched_f64(&s->ctx, s->getrf + L.first, L.count, L.smem_dim, st);
+    case HLU_K_TRSM: return hlu_trsm_batched_f64(&s->ctx, s->trsm + L.first, L.count, L.smem_dim, st);
+    case HLU_K_GEMM: return hlu_gemm_batched_f64(&s->ctx, s->gemm + L.first, s->terms, L.count, st);
+    case HLU_K_GEMM_SMALL: return hlu_gemm_small_batched_f64(&s->ctx, s->gemm + L.first, s->terms, L.count, st);
+    case HLU_K_RKT32:
+      return hlu_rkt_phases(&s->ctx, s->rkt, s->parts, L.first, L.count, &s->scratch, slot++, st, &s->aux);
+    case HLU_K_RKT64: return 0;
+    default: return -3;
+  }
+}
+
+// The launches of one level are independent (levels are ASAP by skeleton-slot
+// hazards, temps are never reused inside a level) unless a truncation reads a
+// temp a dense launch of the same level produces (a deferred producer chain;
+// the planner flags that truncation launch with smem_dim = 1).  Otherwise a
+// level that truncates runs its dense launches (getrf / trsm / gemm, in
+// order) on a side stream beside the truncation kernels and joins them at the
+// level's end.  With
+// stamps (diagnostics) every launch runs in order on `st`, so consecutive
+// stamps time one launch each.
 static int run_launches(hlu_schedule *s, cudaStream_t st) {
   const size_t nl = s->launches.size();
   if (s->stamps) k_stamp<<<1, 1, 0, st>>>(s->stamps);
   if (s->nrkt) cudaMemsetAsync(s->scratch.counts, 0, 8 * sizeof(int32_t) * s->nrkt, st);
   int slot = 0;
-  for (size_t i = 0; i < nl; ++i) {
-    const hlu_launch &L = s->launches[i];
-    int rc = 0;
-    switch (L.kind) {
-      case HLU_K_GETRF:
-        rc = hlu_getrf_batched_f64(&s->ctx, s->getrf + L.first, L.count, L.smem_dim, st);
-        break;
-      case HLU_K_TRSM:
-        rc = hlu_trsm_batched_f64(&s->ctx, s->trsm + L.first, L.count, L.smem_dim, st);
-        break;
-      case HLU_K_GEMM:
-        rc = hlu_gemm_batched_f64(&s->ctx, s->gemm + L.first, s->terms, L.count, st);
-        break;
-      case HLU_K_GEMM_SMALL:
-        rc = hlu_gemm_small_batched_f64(&s->ctx, s->gemm + L.first, s->terms, L.count, st);
-        break;
-      case HLU_K_RKT32: {
-        rc = hlu_rkt_phases(&s->ctx, s->rkt, s->parts, L.first, L.count, &s->scratch, slot++, st, &s->aux);
-        break;
-      }
-      case HLU_K_RKT64:
-        break;
-      default:
-        rc = -3;
+  size_t i = 0;
+  while (i < nl) {
+    size_t j = i;
+    bool rk = false, dn = false;
+    bool dep = false;
+    while (j < nl && s->launches[j].level == s->launches[i].level) {
+      (s->launches[j].kind == HLU_K_RKT32 ? rk : dn) = true;
+      dep = dep || (s->launches[j].kind == HLU_K_RKT32 && s->launches[j].smem_dim != 0);
+      ++j;
     }
-    if (rc != 0) return rc;
-    if (s->stamps) k_stamp<<<1, 1, 0, st>>>(s->stamps + i + 1);
+    const bool split = rk && dn && !dep && !s->stamps;
+    if (split) {
+      cudaEventRecord(s->fork, st);
+      cudaStreamWaitEvent(s->dense, s->fork, 0);
+    }
+    for (size_t k = i; k < j; ++k) {
+      const hlu_launch &L = s->launches[k];
+      const bool side = split && L.kind != HLU_K_RKT32;
+      const int rc = launch_one(s, L, slot, side ? s->dense : st);
+      if (rc != 0) return rc;
+      if (s->stamps) k_stamp<<<1, 1, 0, st>>>(s->stamps + k + 1);
+    }
+    if (split) {
+      cudaEventRecord(s->join, s->dense);
+      cudaStreamWaitEvent(st, s->join, 0);
+    }
+    i = j;
   }
   return 0;
 }
@@ -113,6 +137,9 @@ extern "C" int hlu_schedule_create(hlu_schedule **out, const hlu_ctx *ctx, const
   cudaStream_t st = (cudaStream_t)stream;
   for (int i = 0; i < 4; ++i) cudaStreamCreateWithFlags((cudaStream_t *)&s->aux.side[i], cudaStreamNonBlocking);
   for (int i = 0; i < 8; ++i) cudaEventCreateWithFlags((cudaEvent_t *)&s->aux.ev[i], cudaEventDisableTiming);
+  cudaStreamCreateWithFlags(&s->dense, cudaStreamNonBlocking);
+  cudaEventCreateWithFlags(&s->fork, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&s->join, cudaEventDisableTiming);
   if (s->use_graph) {
     // make sure kernel attributes are set outside capture
     hlu_getrf_batched_f64(&s->ctx, s->getrf, 0, 0, st);
@@ -158,6 +185,9 @@ extern "C" int hlu_schedule_destroy(hlu_schedule *s) {
   if (s->stamps) cudaFree(s->stamps);
   for (int i = 0; i < 8; ++i) cudaEventDestroy((cudaEvent_t)s->aux.ev[i]);
   for (int i = 0; i < 4; ++i) cudaStreamDestroy((cudaStream_t)s->aux.side[i]);
+  cudaEventDestroy(s->fork);
+  cudaEventDestroy(s->join);
+  cudaStreamDestroy(s->dense);
   delete s;
   return 0;
 }

@@ -25,7 +25,7 @@ RKT = np.dtype([("mode", "<i4"), ("part_begin", "<i4"), ("part_count", "<i4"), (
                 ("out_a", "<i8"), ("out_b", "<i8"), ("ws", "<i8"), ("reserved", "<i4"), ("pad", "<i4")])
 RKT_ITEM = np.dtype([("op", "<i4"), ("side", "<i2"), ("block", "<i2")])
 LAUNCH = np.dtype([("kind", "<i4"), ("count", "<i4"), ("first", "<i8"), ("smem_dim", "<i4"),
-                   ("pad", "<i4")])
+                   ("level", "<i4")])
 
 assert VIEW.itemsize == 32 and GETRF.itemsize == 40 and TRSM.itemsize == 72
 assert TERM.itemsize == 144 and GEMM.itemsize == 16 and RKPART.itemsize == 80

@@ -151,6 +151,10 @@ def pack(pl: Planner, arena_base: int):
     """Levels, arena and the device descriptor arrays for a planned call."""
     levels = assign_levels(pl)
     toffs, arena = allocate_temps(pl, levels)
+    birth = {}
+    for i, op in enumerate(pl.ops):
+        for t in op.temps_out:
+            birth[t] = min(birth.get(t, int(levels[i])), int(levels[i]))
     mask = (1 << TEMP_SHIFT) - 1
 
     def fix(off):
@@ -195,20 +199,24 @@ def pack(pl: Planner, arena_base: int):
                 parts.append((fv(a), fv(b), sign, roff, coff))
             rkt.append((mode, pb, len(pts), m, n, cap, slot, log, fix(out_a), fix(out_b), fix(ws) if ws else 0, 0, 0))
             kind, idx, dim = ir.K_RKT32, len(rkt) - 1, kb
+        # a truncation reading a temp produced in its own level (deferred producer
+        # chains) must run after that level's dense launches
+        dep = kind == ir.K_RKT32 and any(birth.get(t) == lv for t in op.temps_in)
         key = (lv, kind)
         if cur is not None and cur[0] == key:
             cur[1][1] += 1
             cur[1][3] = max(cur[1][3], dim)
+            cur[1][5] = cur[1][5] or dep
         else:
-            rec = [kind, 1, idx, dim]
+            rec = [kind, 1, idx, dim, lv, dep]
             launches.append(rec)
             cur = (key, rec)
     out = []
-    for kind, count, first, dim in launches:
+    for kind, count, first, dim, lv, dep in launches:
         if kind == ir.K_RKT32:
-            out.append((ir.K_RKT32, count, first, 0, 0))
+            out.append((ir.K_RKT32, count, first, int(dep), lv))
         else:
-            out.append((kind, count, first, dim, 0))
+            out.append((kind, count, first, dim, lv))
 
     def arr(rows, dt):
         a = np.zeros(max(len(rows), 1), dtype=dt)
