@@ -47,6 +47,13 @@ def main():
         tot[k][0] += 1
         tot[k][1] += dt[i]
     print("total us", dt.sum())
+    # per level: dense launches vs truncation launches (overlap potential)
+    lvl = p.launches["level"].astype(np.int64)
+    isr = p.launches["kind"] == ir.K_RKT32
+    D = np.bincount(lvl, weights=np.where(isr, 0.0, dt), minlength=p.nlevels)
+    R = np.bincount(lvl, weights=np.where(isr, dt, 0.0), minlength=p.nlevels)
+    print(f"levels {p.nlevels}: sum dense {D.sum() / 1e3:.1f} ms, sum trunc {R.sum() / 1e3:.1f} ms, "
+          f"sum max(dense, trunc) per level {np.maximum(D, R).sum() / 1e3:.1f} ms")
     for k, (c, t) in tot.items():
         print(f"{k:6s} launches {c:6d} total {t / 1e3:9.1f} ms avg {t / c:8.1f} us")
     # truncation phases inside the graph: starts = previous launch's end stamp
