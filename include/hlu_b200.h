@@ -213,7 +213,8 @@ const char *hlu_version(void);
 int hlu_device_check(void); /* 0 when a sm_100 device is present */
 int64_t hlu_debug_sweeps(int reset); /* total Jacobi sweeps run so far (diagnostics) */
 /* core-kernel phase cycles [K<=32 | K>32][op count, R/combine, core product, QRCP, Jacobi,
- * rank, W + QRCP apply, combine apply] (16 values; zeros unless built with -DHLU_BPROF) */
+ * rank, W + QRCP apply, combine apply], then the Jacobi sweeps and rounds of [K<=32, K>32]
+ * (20 values; zeros unless built with -DHLU_BPROF) */
 int hlu_debug_bprof(unsigned long long *out, int reset);
 
 #ifdef __cplusplus

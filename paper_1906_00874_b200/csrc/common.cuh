@@ -77,6 +77,30 @@ __device__ __forceinline__ double fast_rsqrt(double x) {
   return fma(y, t, y);
 }
 
+// Jacobi rotation helpers.  tan(theta) only steers convergence (any angle is
+// an exact rotation once cos/sin are normalised), so it uses one Newton step
+// (~1e-13 relative); cos = rsqrt(1 + t^2) keeps cos^2 + sin^2 = 1 to rounding
+// with two steps (MUFU ~2^-22 -> 2^-44 -> full precision).
+__device__ __forceinline__ double rcp_nr1(double x) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  return fma(y, fma(-x, y, 1.0), y);
+}
+
+__device__ __forceinline__ double rsqrt_nr1(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  return fma(y, fma(-0.5 * x * y, y, 0.5), y);
+}
+
+__device__ __forceinline__ double rsqrt_nr2(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  const double h = 0.5 * x;
+  y = fma(y, fma(-h * y, y, 0.5), y);
+  return fma(y, fma(-h * y, y, 0.5), y);
+}
+
 // block-wide max over HLU_NT threads; red must hold HLU_NWARP doubles
 __device__ __forceinline__ double block_max(double v, double *red) {
   v = warp_max(v);

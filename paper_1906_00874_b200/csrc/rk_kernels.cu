@@ -250,6 +250,9 @@ __device__ void apply_chain(int total, int K, int ch, int kk, const double *W, i
 }
 
 __device__ unsigned long long g_sweeps = 0;  // total Jacobi sweeps (diagnostics)
+#ifdef HLU_BPROF
+__device__ unsigned long long g_bsweeps[4];  // Jacobi sweeps, then rounds, of the CTA cores [KM == 64]
+#endif
 
 // Round-robin pairing table: round r, slot i -> (a, b); computed once per op.
 template <int NT>
@@ -467,20 +470,23 @@ __device__ void qrcp_fast(double *G, int p, int q, double *tau, int *cm, double 
       pc[b] = w + b * NW;
       act[b] = pc[b] < q && !((done >> pc[b]) & 1ull);
     }
-    double acc[NB];
+    // own columns in registers: rows l, l + 32 and row j
+    double c0[NB], c1[NB], cj[NB], acc[NB];
 #pragma unroll
     for (int b = 0; b < NB; ++b) {
-      acc[b] = 0.0;
-      if (act[b] && tj != 0.0) {
-        const double *g = G + pc[b] * KM;
-        acc[b] = fma(v0, (l < p) ? g[l] : 0.0, (l + 32 < p) ? v1 * g[l + 32] : 0.0);
-      }
+      const double *g = G + pc[b] * KM;
+      c0[b] = (act[b] && l < p) ? g[l] : 0.0;
+      c1[b] = (act[b] && l + 32 < p) ? g[l + 32] : 0.0;
+      cj[b] = act[b] ? g[j] : 0.0;
     }
+#pragma unroll
+    for (int b = 0; b < NB; ++b) acc[b] = (act[b] && tj != 0.0) ? fma(v0, c0[b], v1 * c1[b]) : 0.0;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
 #pragma unroll
       for (int b = 0; b < NB; ++b) acc[b] += __shfl_xor_sync(0xffffffffu, acc[b], o);
     }
+    __syncwarp();  // every lane has read row j before lane 0 rewrites it
     double ns[NB];
 #pragma unroll
     for (int b = 0; b < NB; ++b) {
@@ -488,14 +494,19 @@ __device__ void qrcp_fast(double *G, int p, int q, double *tau, int *cm, double 
       if (!act[b]) continue;
       double *g = G + pc[b] * KM;
       if (tj != 0.0) {
-        const double f = tj * (acc[b] + g[j]);
-        if (l > j && l < p) g[l] = fma(-f, v0, g[l]);
-        if (l + 32 > j && l + 32 < p) g[l + 32] = fma(-f, v1, g[l + 32]);
-        __syncwarp();
-        if (l == 0) g[j] -= f;
+        const double f = tj * (acc[b] + cj[b]);
+        if (l > j && l < p) {
+          c0[b] = fma(-f, v0, c0[b]);
+          g[l] = c0[b];
+        }
+        if (l + 32 > j && l + 32 < p) {
+          c1[b] = fma(-f, v1, c1[b]);
+          g[l + 32] = c1[b];
+        }
+        if (l == 0) g[j] = cj[b] - f;
       }
-      const double a0 = (l > j && l < p) ? g[l] : 0.0;
-      const double a1 = (l + 32 > j && l + 32 < p) ? g[l + 32] : 0.0;
+      const double a0 = (l > j && l < p) ? c0[b] : 0.0;
+      const double a1 = (l + 32 > j && l + 32 < p) ? c1[b] : 0.0;
       ns[b] = fma(a0, a0, a1 * a1);
     }
 #pragma unroll
@@ -566,18 +577,49 @@ __device__ void jacobi_lp(double *X, double *V, int n, const unsigned char *pa, 
   const int grp = tid / LP, l = tid % LP, ngrp = NT / LP;
   const int qq = n + (n & 1);
   const int np = qq / 2;
+  const int n1 = qq - 1;
+  // round-robin pairs computed in registers when every group has at most one
+  // pair slot (always for n <= KM <= 64 here): slot pi, round r pairs
+  // u = pi and v = qq-1-pi at positions 1 + (u-1+r) mod n1 (u = 0 stays 0),
+  // the same sequence as the table (pa, pb)
+  const bool one = np <= ngrp;
   for (int sweep = 0; sweep < 40; ++sweep) {
     int big = 0;
+    int cu = grp - 1 < 0 ? 0 : grp - 1, cv = qq - 2 - grp;  // (u-1) mod n1, (v-1) mod n1 at r = 0
     for (int r = 0; r < qq - 1; ++r) {
       for (int pi = grp; pi < np; pi += ngrp) {
-        const int a = pa[r * np + pi], b = pb[r * np + pi];
+        int a, b;
+        if (one) {
+          a = pi == 0 ? 0 : 1 + cu;
+          b = 1 + cv;
+          if (a > b) {
+            const int x = a;
+            a = b;
+            b = x;
+          }
+        } else {
+          a = pa[r * np + pi];
+          b = pb[r * np + pi];
+        }
         if (b >= n) continue;
+        // the pair's rows of X and V, all loads issued up front (rows l + q LP)
+        constexpr int RPL = (KM + LP - 1) / LP;
+        double xa[RPL], xb[RPL], va[RPL], vb[RPL];
+#pragma unroll
+        for (int q = 0; q < RPL; ++q) {
+          const int i = l + q * LP;
+          const bool ok = i < n;
+          xa[q] = ok ? X[i + a * KM] : 0.0;
+          xb[q] = ok ? X[i + b * KM] : 0.0;
+          va[q] = ok ? V[i + a * KM] : 0.0;
+          vb[q] = ok ? V[i + b * KM] : 0.0;
+        }
         double al = 0.0, be = 0.0, ga = 0.0;
-        for (int i = l; i < n; i += LP) {
-          const double x = X[i + a * KM], y = X[i + b * KM];
-          al = fma(x, x, al);
-          be = fma(y, y, be);
-          ga = fma(x, y, ga);
+#pragma unroll
+        for (int q = 0; q < RPL; ++q) {
+          al = fma(xa[q], xa[q], al);
+          be = fma(xb[q], xb[q], be);
+          ga = fma(xa[q], xb[q], ga);
         }
         al = part_sum<LP>(al);
         be = part_sum<LP>(be);
@@ -588,22 +630,30 @@ __device__ void jacobi_lp(double *X, double *V, int n, const unsigned char *pa, 
         // t = tan(theta) = 2 ga / (d + sign(d) sqrt(d^2 + 4 ga^2)), d = be - al
         const double d = be - al;
         const double q2 = fma(d, d, 4.0 * g2);
-        const double rq = q2 * fast_rsqrt(q2);
-        const double t = 2.0 * ga * fast_rcp(d + copysign(rq, d));
-        const double cs = fast_rsqrt(fma(t, t, 1.0)), sn = cs * t;
-        for (int i = l; i < n; i += LP) {
-          const double x = X[i + a * KM], y = X[i + b * KM];
-          X[i + a * KM] = cs * x - sn * y;
-          X[i + b * KM] = sn * x + cs * y;
-          const double u = V[i + a * KM], vv = V[i + b * KM];
-          V[i + a * KM] = cs * u - sn * vv;
-          V[i + b * KM] = sn * u + cs * vv;
+        const double rq = q2 * rsqrt_nr1(q2);
+        const double t = 2.0 * ga * rcp_nr1(d + copysign(rq, d));
+        const double cs = rsqrt_nr2(fma(t, t, 1.0)), sn = cs * t;
+#pragma unroll
+        for (int q = 0; q < RPL; ++q) {
+          const int i = l + q * LP;
+          if (i < n) {
+            X[i + a * KM] = cs * xa[q] - sn * xb[q];
+            X[i + b * KM] = sn * xa[q] + cs * xb[q];
+            V[i + a * KM] = cs * va[q] - sn * vb[q];
+            V[i + b * KM] = sn * va[q] + cs * vb[q];
+          }
         }
       }
+      cu = cu + 1 == n1 ? 0 : cu + 1;
+      cv = cv + 1 == n1 ? 0 : cv + 1;
       __syncthreads();
     }
     if (__syncthreads_or(big) == 0) {
       if (tid == 0) atomicAdd(&g_sweeps, sweep + 1);
+#ifdef HLU_BPROF
+      if (tid == 0) atomicAdd(&g_bsweeps[KM == 64], (unsigned long long)(sweep + 1));
+      if (tid == 0) atomicAdd(&g_bsweeps[2 + (KM == 64)], (unsigned long long)(sweep + 1) * (qq - 1));
+#endif
       break;
     }
   }
@@ -968,9 +1018,9 @@ __device__ int r_core(const double *Rx, int ldx, const double *Ry, int ldy, int 
             // t = tan(theta) = 2 ga / (d + sign(d) sqrt(d^2 + 4 ga^2)), d = be - al
             const double dd = be - al;
             const double q2 = fma(dd, dd, 4.0 * g2);
-            const double rq = q2 * fast_rsqrt(q2);
-            const double t = 2.0 * ga * fast_rcp(dd + copysign(rq, dd));
-            cs = fast_rsqrt(fma(t, t, 1.0));
+            const double rq = q2 * rsqrt_nr1(q2);
+            const double t = 2.0 * ga * rcp_nr1(dd + copysign(rq, dd));
+            cs = rsqrt_nr2(fma(t, t, 1.0));
             sn = cs * t;
           }
         }
@@ -1674,12 +1724,14 @@ extern "C" int hlu_debug_bprof(unsigned long long *out, int reset) {
 #ifdef HLU_BPROF
   cudaDeviceSynchronize();
   if (cudaMemcpyFromSymbol(out, g_bprof, sizeof(g_bprof)) != cudaSuccess) return -1;
+  if (cudaMemcpyFromSymbol(out + 16, g_bsweeps, sizeof(g_bsweeps)) != cudaSuccess) return -1;
   if (reset) {
     static const unsigned long long z[16] = {0};
     cudaMemcpyToSymbol(g_bprof, z, sizeof(z));
+    cudaMemcpyToSymbol(g_bsweeps, z, sizeof(g_bsweeps));
   }
 #else
-  for (int i = 0; i < 16; ++i) out[i] = 0;
+  for (int i = 0; i < 20; ++i) out[i] = 0;
   (void)reset;
 #endif
   return 0;

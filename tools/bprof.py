@@ -20,7 +20,7 @@ def main():
     L, pl = plan_call([h], [("factor", h)], 32)
     call = DeviceCall(L, pl, TruncationControl(*ctl), use_graph=True)
     lib = _native.lib()
-    buf = (ctypes.c_ulonglong * 16)()
+    buf = (ctypes.c_ulonglong * 20)()
     call.snapshot()
     call.launch()
     call.sync()
@@ -35,7 +35,8 @@ def main():
     for v, tag in ((0, "K<=32"), (1, "K>32")):
         ops = buf[8 * v]
         tot = sum(buf[8 * v + k] for k in range(1, 8))
-        print(f"{tag}: ops {ops}  total {tot / 1.965e9:.3f} s-CTA  per op {tot / max(ops, 1) / 1965:.1f} us")
+        print(f"{tag}: ops {ops}  total {tot / 1.965e9:.3f} s-CTA  per op {tot / max(ops, 1) / 1965:.1f} us  "
+              f"Jacobi sweeps per op {buf[16 + v] / max(ops, 1):.2f} rounds per op {buf[18 + v] / max(ops, 1):.1f}")
         for k in range(1, 8):
             print(f"   {names[k]:14s} {buf[8 * v + k] / 1.965e9:8.3f} s  {buf[8 * v + k] / max(ops, 1) / 1965:8.1f} us/op")
     print("jacobi sweeps (all paths, one run):", lib.hlu_debug_sweeps(0))
