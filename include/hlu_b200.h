@@ -200,6 +200,16 @@ int hlu_schedule_create(hlu_schedule **out, const hlu_ctx *ctx, const hlu_launch
                         const hlu_getrf_desc *getrf, const hlu_trsm_desc *trsm, const hlu_gemm_desc *gemm,
                         const hlu_term *terms, hlu_rkt_desc *rkt, const hlu_rkpart *parts,
                         const hlu_rkt_scratch *scratch, int use_graph, void *stream);
+/* Same, as two chains: the dense launches (getrf / trsm / gemm) of every level
+ * on one stream, the truncation launches on another, each chain in level order,
+ * with cross-chain waits only where the plan has a hazard (hlu_plan_level_waits:
+ * nlevels entries each).  Consecutive levels of the two classes overlap instead
+ * of meeting at a barrier after every level.  Null waits = hlu_schedule_create. */
+int hlu_schedule_create_chains(hlu_schedule **out, const hlu_ctx *ctx, const hlu_launch *launches, int64_t nlaunch,
+                               const hlu_getrf_desc *getrf, const hlu_trsm_desc *trsm, const hlu_gemm_desc *gemm,
+                               const hlu_term *terms, hlu_rkt_desc *rkt, const hlu_rkpart *parts,
+                               const hlu_rkt_scratch *scratch, const int32_t *wait_dense, const int32_t *wait_rkt,
+                               int64_t nlevels, int use_graph, void *stream);
 int hlu_schedule_launch(hlu_schedule *s, void *stream);
 int hlu_schedule_destroy(hlu_schedule *s);
 /* diagnostics: with HLU_STAMPS=1 at creation, the %globaltimer (ns) before the first and

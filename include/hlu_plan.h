@@ -59,6 +59,12 @@ int hlu_plan_sizes(const hlu_plan *p, int64_t *sizes);
 int hlu_plan_copy(const hlu_plan *p, void *getrf, void *trsm, void *gemm, void *terms, void *rkt, void *parts,
                   void *launches, int32_t *flop_formula, double *flop_coef, int64_t *flop_log, int64_t *lu_op_ids,
                   int64_t *lu_nodes, int64_t *op_levels);
+/* Two-chain schedule (hlu_schedule_create's wait arrays), one entry per level:
+ * wait_dense[l] / wait_rkt[l] = last level of the truncation / dense chain that
+ * the dense / truncation launches of level l wait for (-1: none), from the ops'
+ * slot / temp hazards and arena-block reuse.  Returns -1 when the plan has a
+ * hazard the two chains cannot express (the caller keeps level barriers). */
+int hlu_plan_level_waits(const hlu_plan *p, int32_t *wait_dense, int32_t *wait_rkt);
 void hlu_plan_free(hlu_plan *p);
 
 #ifdef __cplusplus

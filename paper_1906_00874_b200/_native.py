@@ -25,6 +25,7 @@ SYMBOLS = (
     "hlu_rkt_items",
     "hlu_rkt_ws_doubles",
     "hlu_schedule_create",
+    "hlu_schedule_create_chains",
     "hlu_schedule_launch",
     "hlu_schedule_destroy",
     "hlu_schedule_stamps",
@@ -91,13 +92,16 @@ def lib():
     L.hlu_debug_bprof.restype = ctypes.c_int
     L.hlu_schedule_create.argtypes = [ctypes.POINTER(vp), ctypes.POINTER(HluCtx), vp, i64,
                                       vp, vp, vp, vp, vp, vp, sp, i32, vp]
+    L.hlu_schedule_create_chains.argtypes = [ctypes.POINTER(vp), ctypes.POINTER(HluCtx), vp, i64,
+                                             vp, vp, vp, vp, vp, vp, sp, vp, vp, i64, i32, vp]
     L.hlu_schedule_launch.argtypes = [vp, vp]
     L.hlu_schedule_destroy.argtypes = [vp]
     L.hlu_schedule_stamps.argtypes = [vp, vp]
     L.hlu_schedule_stamps.restype = i64
     L.hlu_version.restype = ctypes.c_char_p
     for name in ("hlu_getrf_batched_f64", "hlu_trsm_batched_f64", "hlu_gemm_batched_f64", "hlu_gemm_small_batched_f64",
-                 "hlu_rk_update_batched_f64", "hlu_rkt_phases", "hlu_rkt_phase", "hlu_schedule_create", "hlu_schedule_launch",
+                 "hlu_rk_update_batched_f64", "hlu_rkt_phases", "hlu_rkt_phase", "hlu_schedule_create", "hlu_schedule_create_chains",
+                 "hlu_schedule_launch",
                  "hlu_schedule_destroy",
     "hlu_schedule_stamps", "hlu_device_check"):
         getattr(L, name).restype = ctypes.c_int

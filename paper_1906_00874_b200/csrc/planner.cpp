@@ -14,6 +14,7 @@
 #include <limits>
 #include <stdexcept>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include "hlu_b200.h"
@@ -767,6 +768,13 @@ struct Planner {
   std::vector<int64_t> levels;
   std::vector<int64_t> toffs;
   std::vector<int64_t> tbirth;  // level of each temp's producer
+  std::vector<int64_t> reuse_from;  // temp whose arena block a temp takes over (-1: fresh)
+  // Cross-class waits (two-chain schedule): the dense chain (getrf / trsm /
+  // gemm) and the truncation chain each run their levels in order on their own
+  // stream; wait_d[l] / wait_r[l] = the last level of the OTHER chain that the
+  // level-l launches of this chain must wait for (-1: none).
+  std::vector<int32_t> wait_d, wait_r;
+  bool waits_ok = false;
   int64_t arena = 0;
 
   // Hazard state: slots in segment trees (reads can span whole partitioned
@@ -906,6 +914,8 @@ struct Planner {
     std::stable_sort(by_death.begin(), by_death.end(), [&](int64_t a, int64_t b) { return death[a] < death[b]; });
     std::vector<std::vector<int64_t>> freel(64);
     toffs.assign(nt, 0);
+    reuse_from.assign(nt, -1);
+    std::unordered_map<int64_t, int64_t> last_user;  // arena offset -> temp that holds it
     int64_t top = 0;
     int64_t di = 0;
     for (int64_t t : order) {
@@ -919,10 +929,12 @@ struct Planner {
       if (!fl.empty()) {
         toffs[t] = fl.back();
         fl.pop_back();
+        reuse_from[t] = last_user[toffs[t]];
       } else {
         toffs[t] = top;
         top += int64_t(1) << cls[t];
       }
+      last_user[toffs[t]] = t;
     }
     arena = top;
   }
@@ -1189,6 +1201,86 @@ struct Planner {
       }
     }
     nlevels = n ? (*std::max_element(levels.begin(), levels.end()) + 1) : 0;
+    compute_waits();
+  }
+
+  // Every op conflicts (RAW / WAR / WAW on skeleton slots and temps, plus the
+  // arena-block reuse of allocate_temps) only with ops at lower levels (one
+  // exception: a truncation reading a temp a dense op of its own level
+  // produces).  Same-class conflicts are covered by the chain's level order;
+  // for the other class the op waits for the highest conflicting level.
+  void compute_waits() {
+    const int64_t nt = (int64_t)temp_size.size();
+    wait_d.assign(nlevels, -1);
+    wait_r.assign(nlevels, -1);
+    waits_ok = true;
+    auto cls_of = [&](const Op &o) { return o.kind == 3 ? 1 : 0; };
+    // highest level at which each class touches each temp (for block reuse)
+    std::vector<int64_t> touch[2] = {std::vector<int64_t>(nt, -1), std::vector<int64_t>(nt, -1)};
+    for (size_t i = 0; i < ops.size(); ++i) {
+      const Op &o = ops[i];
+      auto &tc = touch[cls_of(o)];
+      const int64_t lv = levels[i];
+      for (int64_t k = o.ti_begin; k < o.to_end; ++k) tc[tids[k]] = std::max(tc[tids[k]], lv);
+      for (int64_t k = o.r_begin; k < o.w_end; ++k)
+        if (ivs[k].lo >= nslots) tc[ivs[k].lo - nslots] = std::max(tc[ivs[k].lo - nslots], lv);
+    }
+    MaxTree lw[2];
+    TagTree lr[2];
+    std::vector<int64_t> lw_s[2], lwT[2], lrT[2];
+    for (int c = 0; c < 2; ++c) {
+      lw[c].init(std::max<int64_t>(nslots, 1));
+      lr[c].init(std::max<int64_t>(nslots, 1));
+      lw_s[c].assign(nslots, -1);
+      lwT[c].assign(nt, -1);
+      lrT[c].assign(nt, -1);
+    }
+    for (size_t i = 0; i < ops.size(); ++i) {
+      const Op &o = ops[i];
+      const int x = cls_of(o), y = 1 - x;
+      const int64_t lv = levels[i];
+      int64_t w = -1;
+      auto temp_w = [&](int64_t t) {
+        w = std::max(w, std::max(lwT[y][t], lrT[y][t]));
+        if (reuse_from[t] >= 0) w = std::max(w, touch[y][reuse_from[t]]);
+      };
+      for (int64_t k = o.r_begin; k < o.r_end; ++k) {
+        const Iv &v = ivs[k];
+        if (v.lo >= nslots) w = std::max(w, lwT[y][v.lo - nslots]);
+        else w = std::max(w, lw[y].query(v.lo, v.hi));
+      }
+      for (int64_t k = o.ti_begin; k < o.ti_end; ++k) w = std::max(w, lwT[y][tids[k]]);
+      for (int64_t k = o.to_begin; k < o.to_end; ++k) temp_w(tids[k]);
+      for (int64_t k = o.w_begin; k < o.w_end; ++k) {
+        const Iv &v = ivs[k];
+        if (v.lo >= nslots) temp_w(v.lo - nslots);
+        else
+          for (int64_t s2 = v.lo; s2 < v.hi; ++s2) w = std::max(w, std::max(lw_s[y][s2], lr[y].get(s2)));
+      }
+      if (w > lv || (w == lv && x == 0)) waits_ok = false;  // only truncations may wait on their own level
+      auto &wl = x == 0 ? wait_d : wait_r;
+      wl[lv] = std::max<int32_t>(wl[lv], (int32_t)w);
+      // commit
+      for (int64_t k = o.r_begin; k < o.r_end; ++k) {
+        const Iv &v = ivs[k];
+        if (v.lo >= nslots) lrT[x][v.lo - nslots] = std::max(lrT[x][v.lo - nslots], lv);
+        else lr[x].chmax(v.lo, v.hi, lv);
+      }
+      for (int64_t k = o.ti_begin; k < o.ti_end; ++k) lrT[x][tids[k]] = std::max(lrT[x][tids[k]], lv);
+      for (int64_t k = o.to_begin; k < o.to_end; ++k) lwT[x][tids[k]] = std::max(lwT[x][tids[k]], lv);
+      for (int64_t k = o.w_begin; k < o.w_end; ++k) {
+        const Iv &v = ivs[k];
+        if (v.lo >= nslots) {
+          lwT[x][v.lo - nslots] = std::max(lwT[x][v.lo - nslots], lv);
+        } else {
+          for (int64_t s2 = v.lo; s2 < v.hi; ++s2)
+            if (lv > lw_s[x][s2]) {
+              lw_s[x][s2] = lv;
+              lw[x].set(s2, lv);
+            }
+        }
+      }
+    }
   }
 };
 
@@ -1285,6 +1377,14 @@ extern "C" int hlu_plan_copy(const hlu_plan *p, void *getrf, void *trsm, void *g
   }
   cp(lu_op_ids, P.lu_ops);
   cp(lu_nodes, P.lu_nodes);
+  return 0;
+}
+
+extern "C" int hlu_plan_level_waits(const hlu_plan *p, int32_t *wait_dense, int32_t *wait_rkt) {
+  const Planner &P = p->P;
+  if (!P.waits_ok) return -1;
+  cp(wait_dense, P.wait_d);
+  cp(wait_rkt, P.wait_r);
   return 0;
 }
 

@@ -31,6 +31,9 @@ struct hlu_schedule {
   unsigned long long *stamps;  // diagnostics: %globaltimer after every launch (HLU_STAMPS=1)
   cudaStream_t dense;          // getrf / trsm / gemm launches of a level that also truncates
   cudaEvent_t fork, join;
+  // two-chain mode: per-level cross-chain waits and the events they wait on
+  std::vector<int32_t> wait_d, wait_r;
+  std::vector<cudaEvent_t> ev_d, ev_r;  // after the dense / truncation launches of a level (needed ones only)
 };
 
 __global__ void k_stamp(unsigned long long *slot) {
@@ -61,7 +64,68 @@ static int launch_one(hlu_schedule *s, const hlu_launch &L, int &slot, cudaStrea
 // level's end.  With
 // stamps (diagnostics) every launch runs in order on `st`, so consecutive
 // stamps time one launch each.
+// Two chains: the truncation launches run in level order on `st`, the dense
+// launches in level order on s->dense; a level's launches of one chain wait
+// for the other chain's last conflicting level (planner waits), and the
+// dense launches of a level go first so a truncation can wait on its own level.
+static int run_chains(hlu_schedule *s, cudaStream_t st) {
+  const size_t nl = s->launches.size();
+  if (s->nrkt) cudaMemsetAsync(s->scratch.counts, 0, 8 * sizeof(int32_t) * s->nrkt, st);
+  cudaEventRecord(s->fork, st);
+  cudaStreamWaitEvent(s->dense, s->fork, 0);
+  int slot = 0;
+  int32_t seen_r = -1, seen_d = -1;  // highest level of the other chain already waited for
+  std::vector<char> rec_d(s->wait_d.size(), 0), rec_r(s->wait_d.size(), 0);
+  size_t i = 0;
+  while (i < nl) {
+    const int32_t lv = s->launches[i].level;
+    size_t j = i;
+    while (j < nl && s->launches[j].level == lv) ++j;
+    bool any_d = false, any_r = false;
+    for (size_t k = i; k < j; ++k) (s->launches[k].kind == HLU_K_RKT32 ? any_r : any_d) = true;
+    if (any_d) {
+      const int32_t w = s->wait_d[lv];
+      if (w > seen_r) {
+        if (!s->ev_r[w] || !rec_r[w]) return -16;  // never recorded: plan / launch mismatch  // never recorded: plan / launch mismatch
+        cudaStreamWaitEvent(s->dense, s->ev_r[w], 0);
+        seen_r = w;
+      }
+      for (size_t k = i; k < j; ++k) {
+        if (s->launches[k].kind == HLU_K_RKT32) continue;
+        const int rc = launch_one(s, s->launches[k], slot, s->dense);
+        if (rc != 0) return rc;
+      }
+      if (s->ev_d[lv]) {
+        cudaEventRecord(s->ev_d[lv], s->dense);
+        rec_d[lv] = 1;
+      }
+    }
+    if (any_r) {
+      const int32_t w = s->wait_r[lv];
+      if (w > seen_d) {
+        if (!s->ev_d[w] || !rec_d[w]) return -16;
+        cudaStreamWaitEvent(st, s->ev_d[w], 0);
+        seen_d = w;
+      }
+      for (size_t k = i; k < j; ++k) {
+        if (s->launches[k].kind != HLU_K_RKT32) continue;
+        const int rc = launch_one(s, s->launches[k], slot, st);
+        if (rc != 0) return rc;
+      }
+      if (s->ev_r[lv]) {
+        cudaEventRecord(s->ev_r[lv], st);
+        rec_r[lv] = 1;
+      }
+    }
+    i = j;
+  }
+  cudaEventRecord(s->join, s->dense);
+  cudaStreamWaitEvent(st, s->join, 0);
+  return 0;
+}
+
 static int run_launches(hlu_schedule *s, cudaStream_t st) {
+  if (!s->wait_d.empty() && !s->stamps) return run_chains(s, st);
   const size_t nl = s->launches.size();
   if (s->stamps) k_stamp<<<1, 1, 0, st>>>(s->stamps);
   if (s->nrkt) cudaMemsetAsync(s->scratch.counts, 0, 8 * sizeof(int32_t) * s->nrkt, st);
@@ -102,7 +166,47 @@ extern "C" int hlu_schedule_create(hlu_schedule **out, const hlu_ctx *ctx, const
                                    const hlu_gemm_desc *gemm, const hlu_term *terms, hlu_rkt_desc *rkt,
                                    const hlu_rkpart *parts, const hlu_rkt_scratch *scratch, int use_graph,
                                    void *stream) {
+  return hlu_schedule_create_chains(out, ctx, launches, nlaunch, getrf, trsm, gemm, terms, rkt, parts, scratch,
+                                    nullptr, nullptr, 0, use_graph, stream);
+}
+
+static void destroy_events(hlu_schedule *s) {
+  for (cudaEvent_t e : s->ev_d)
+    if (e) cudaEventDestroy(e);
+  for (cudaEvent_t e : s->ev_r)
+    if (e) cudaEventDestroy(e);
+  s->ev_d.clear();
+  s->ev_r.clear();
+}
+
+extern "C" int hlu_schedule_create_chains(hlu_schedule **out, const hlu_ctx *ctx, const hlu_launch *launches,
+                                          int64_t nlaunch, const hlu_getrf_desc *getrf, const hlu_trsm_desc *trsm,
+                                          const hlu_gemm_desc *gemm, const hlu_term *terms, hlu_rkt_desc *rkt,
+                                          const hlu_rkpart *parts, const hlu_rkt_scratch *scratch,
+                                          const int32_t *wait_dense, const int32_t *wait_rkt, int64_t nlevels,
+                                          int use_graph, void *stream) {
   hlu_schedule *s = new hlu_schedule();
+  if (wait_dense && wait_rkt && nlevels > 0) {
+    for (int64_t i = 0; i < nlaunch; ++i)
+      if (launches[i].level < 0 || launches[i].level >= nlevels) {
+        delete s;
+        return -15;
+      }
+    s->wait_d.assign(wait_dense, wait_dense + nlevels);
+    s->wait_r.assign(wait_rkt, wait_rkt + nlevels);
+    s->ev_d.assign(nlevels, nullptr);
+    s->ev_r.assign(nlevels, nullptr);
+    for (int64_t l = 0; l < nlevels; ++l) {
+      const int32_t wd = s->wait_d[l], wr = s->wait_r[l];
+      if (wd > l || wr > l || (wd == l)) {  // only a truncation may wait on its own level
+        destroy_events(s);
+        delete s;
+        return -15;
+      }
+      if (wd >= 0 && !s->ev_r[wd]) cudaEventCreateWithFlags(&s->ev_r[wd], cudaEventDisableTiming);
+      if (wr >= 0 && !s->ev_d[wr]) cudaEventCreateWithFlags(&s->ev_d[wr], cudaEventDisableTiming);
+    }
+  }
   s->ctx = *ctx;
   s->launches.assign(launches, launches + nlaunch);
   s->getrf = getrf;
@@ -188,6 +292,7 @@ extern "C" int hlu_schedule_destroy(hlu_schedule *s) {
   cudaEventDestroy(s->fork);
   cudaEventDestroy(s->join);
   cudaStreamDestroy(s->dense);
+  destroy_events(s);
   delete s;
   return 0;
 }

@@ -14,6 +14,7 @@ No CPU fallback exists: without the library or a GPU, construction raises.
 from __future__ import annotations
 
 import ctypes
+import os
 
 import numpy as np
 
@@ -89,11 +90,19 @@ class DeviceCall:
             )
             handle = ctypes.c_void_p()
             launches = np.ascontiguousarray(p.launches)
-            rc = lib.hlu_schedule_create(
+            # two chains (dense / truncation) with the planner's cross-chain
+            # waits; HLU_CHAINS=0 keeps a barrier after every level
+            chains = p.wait_dense is not None and os.environ.get("HLU_CHAINS", "1") != "0"
+            self.chains = chains
+            wd = np.ascontiguousarray(p.wait_dense) if chains else None
+            wr = np.ascontiguousarray(p.wait_rkt) if chains else None
+            rc = lib.hlu_schedule_create_chains(
                 ctypes.byref(handle), ctypes.byref(self.ctx), launches.ctypes.data, len(launches),
                 self.d_getrf.data_ptr(), self.d_trsm.data_ptr(), self.d_gemm.data_ptr(),
                 self.d_terms.data_ptr(), self.d_rkt.data_ptr(), self.d_parts.data_ptr(),
                 ctypes.byref(self.scratch),
+                wd.ctypes.data if chains else None, wr.ctypes.data if chains else None,
+                int(p.nlevels) if chains else 0,
                 1 if use_graph else 0, ctypes.c_void_p(self.stream.cuda_stream),
             )
             _native.check(rc, "hlu_schedule_create")

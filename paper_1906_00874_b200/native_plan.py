@@ -48,6 +48,8 @@ def lib():
         L.hlu_plan_sizes.argtypes = [vp, vp]
         L.hlu_plan_copy.argtypes = [vp] * 14
         L.hlu_plan_free.argtypes = [vp]
+        L.hlu_plan_level_waits.argtypes = [vp, vp, vp]
+        L.hlu_plan_level_waits.restype = ctypes.c_int
         _lib = L
     return _lib
 
@@ -152,6 +154,10 @@ def plan(layout, commands, split_rows=SPLIT_ROWS):
         L.hlu_plan_copy(h, getrf.ctypes.data, trsm.ctypes.data, gemm.ctypes.data, terms.ctypes.data,
                         rkt.ctypes.data, parts.ctypes.data, launches.ctypes.data, ff.ctypes.data,
                         fc.ctypes.data, fl.ctypes.data, lu_ops.ctypes.data, lu_nodes.ctypes.data, lv.ctypes.data)
+        wd = np.full(max(nlev, 1), -1, dtype=np.int32)
+        wr = np.full(max(nlev, 1), -1, dtype=np.int32)
+        if L.hlu_plan_level_waits(h, wd.ctypes.data, wr.ctypes.data) != 0:
+            wd = wr = None
     finally:
         L.hlu_plan_free(h)
     labels = []
@@ -163,4 +169,5 @@ def plan(layout, commands, split_rows=SPLIT_ROWS):
         launches=launches, nlevels=nlev, arena_doubles=arena,
         flop_formula=ff.astype(np.int64), flop_coef=fc, flop_log=fl, nlog=max(nlog, 1),
         nranks=max(nrank, 1), lu_op_ids=lu_ops[:nlu], lu_labels=labels, op_levels=lv,
+        wait_dense=wd, wait_rkt=wr,
     ), nops

@@ -141,6 +141,10 @@ class Packed:
     lu_labels: list
     op_levels: np.ndarray
     desc_op: dict = None  # kind name -> op index of every descriptor (Python planner only)
+    # two-chain schedule (native planner only): per level, the last level of the
+    # other chain the dense / truncation launches wait for; None = level barriers
+    wait_dense: np.ndarray = None
+    wait_rkt: np.ndarray = None
 
 
 def _view_rec(v):
