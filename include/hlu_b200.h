@@ -78,9 +78,13 @@ typedef struct {
 
 enum { HLU_TERM_ZERO = 0, HLU_TERM_GEMM = 1, HLU_TERM_TRIPLE = 2 };
 
+/* assoc of a GEMM term: which part of A enters (triangular matvecs with the
+ * stored factors, reference hlu.py:720-767) */
+enum { HLU_TRI_NONE = 0, HLU_TRI_UPPER = 1, HLU_TRI_UNIT_LOWER = 2 };
+
 /* one term of an ordered accumulation chain:
  *   ZERO:   C = 0
- *   GEMM:   C += alpha * A B
+ *   GEMM:   C += alpha * A B   (A = triu(A) / tril(A,-1)+I per assoc)
  *   TRIPLE: C += alpha * A (M B)   (assoc 0)   or   alpha * (A M) B   (assoc 1) */
 typedef struct {
   hlu_view c, a, m, b;

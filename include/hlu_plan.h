@@ -35,7 +35,13 @@ enum {
   HLU_CMD_SOLVE_UPPER = 2, /* a = b, b = u   : b := b u^-1 */
   HLU_CMD_UPDATE = 3,      /* a = c, b = a, c = b : c := c - a b */
   HLU_CMD_FWD_VEC = 4,     /* a = factored root, vector at vec_off (resource vec_res) */
-  HLU_CMD_BWD_VEC = 5
+  HLU_CMD_BWD_VEC = 5,
+  /* y += op(a) x with x at vec_off (vec_res), y at vec2_off (vec2_res), both
+   * vec_cols wide: the full H-matrix (hmatvec, hmatrix.py:178-200), the unit
+   * lower factor or the upper factor of a factored root (hlu.py:720-767) */
+  HLU_CMD_MATVEC = 6,
+  HLU_CMD_LOWER_MATVEC = 7,
+  HLU_CMD_UPPER_MATVEC = 8
 };
 
 typedef struct {
@@ -43,7 +49,8 @@ typedef struct {
   int64_t vec_off;
   int32_t vec_cols, pad;
   int64_t vec_res;
-} hlu_plan_cmd; /* 40 bytes */
+  int64_t vec2_off, vec2_res;
+} hlu_plan_cmd; /* 56 bytes */
 
 typedef struct hlu_plan hlu_plan;
 

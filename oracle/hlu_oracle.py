@@ -568,3 +568,70 @@ def backward_solve(h, y):
 def hlu_solve(h, rhs):
     """x = U^-1 L^-1 rhs on a factored H-matrix."""
     return backward_solve(h, forward_solve(h, rhs))
+
+
+# -- products with the matrix and its stored factors (residual probes)
+
+
+def _matvec_into(h, x, y):
+    """y += h x by recursion over the blocks (reference hmatrix.py:188-200)."""
+    if h.kind == DENSE:
+        y += h.data @ x
+    elif h.kind == LOWRANK:
+        y += h.data.a @ (h.data.b.T @ x)
+    else:
+        r0, c0 = h.row_range[0], h.col_range[0]
+        for line in h.data:
+            for ch in line:
+                (i0, i1), (j0, j1) = ch.row_range, ch.col_range
+                _matvec_into(ch, x[j0 - c0 : j1 - c0], y[i0 - r0 : i1 - r0])
+
+
+def hmatvec(h, x):
+    x = np.asarray(x, dtype=float)
+    y = np.zeros((h.rows,) + x.shape[1:])
+    _matvec_into(h, x, y)
+    return y
+
+
+def _tri_into(h, x, y, lower):
+    """y += L x (unit lower) or U x with the stored factors (hlu.py:727-767)."""
+    if h.kind == DENSE:
+        y += (np.tril(h.data, -1) @ x + x) if lower else (np.triu(h.data) @ x)
+        return
+    if h.kind != PARTITIONED:
+        raise StructureError("factored matrix has a low-rank diagonal block")
+    r0 = h.row_range[0]
+    for i, line in enumerate(h.data):
+        for j, ch in enumerate(line):
+            (i0, i1), (j0, j1) = ch.row_range, ch.col_range
+            if (j < i) if lower else (j > i):
+                _matvec_into(ch, x[j0 - r0 : j1 - r0], y[i0 - r0 : i1 - r0])
+            elif j == i:
+                _tri_into(ch, x[j0 - r0 : j1 - r0], y[i0 - r0 : i1 - r0], lower)
+
+
+def lower_unit_matvec(h, x):
+    x = np.asarray(x, dtype=float)
+    y = np.zeros_like(x)
+    _tri_into(h, x, y, True)
+    return y
+
+
+def upper_matvec(h, x):
+    x = np.asarray(x, dtype=float)
+    y = np.zeros_like(x)
+    _tri_into(h, x, y, False)
+    return y
+
+
+def residual_probe(original, factored, seed=0, probes=10):
+    """Worst ||A x - L (U x)|| / ||A x|| over random x (reference bench.py:142-152)."""
+    rng = np.random.default_rng(seed)
+    worst = 0.0
+    for _ in range(probes):
+        x = rng.standard_normal(original.cols)
+        ax = hmatvec(original, x)
+        lux = lower_unit_matvec(factored, upper_matvec(factored, x))
+        worst = max(worst, float(np.linalg.norm(ax - lux) / np.linalg.norm(ax)))
+    return worst

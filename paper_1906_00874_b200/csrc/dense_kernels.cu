@@ -153,8 +153,17 @@ __global__ void __launch_bounds__(HLU_NT) k_trsm(hlu_ctx c, const hlu_trsm_desc 
 // C += alpha * A B.  64x64 output tiles, 32-deep k-steps; the next k-tile is
 // prefetched into registers while the current one is consumed from shared
 // memory, so each k-step costs max(load latency, compute) instead of the sum.
+// A operand of a GEMM term read through its triangle (hlu_term.assoc of a GEMM
+// term): HLU_TRI_NONE = A, HLU_TRI_UPPER = triu(A), HLU_TRI_UNIT_LOWER =
+// tril(A, -1) + I (the stored factors of a dense diagonal leaf, hlu.py:720-767)
+__device__ __forceinline__ double tri_get(const Mat &A, int i, int j, int tri) {
+  if (tri == HLU_TRI_UPPER) return j >= i ? A.get(i, j) : 0.0;
+  if (tri == HLU_TRI_UNIT_LOWER) return j < i ? A.get(i, j) : (j == i ? 1.0 : 0.0);
+  return A.get(i, j);
+}
+
 __device__ __noinline__ void tile_gemm(const Mat &C, const Mat &A, const Mat &B, double alpha, double *sA,
-                                       double *sB) {
+                                       double *sB, int tri = HLU_TRI_NONE) {
   const int m = C.rows, n = C.cols, k = A.cols;
   const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
   for (int i0 = 0; i0 < m; i0 += GB) {
@@ -173,7 +182,7 @@ __device__ __noinline__ void tile_gemm(const Mat &C, const Mat &A, const Mat &B,
           const int e = tid + u * HLU_NT;
           const int r = a_rows_fast ? e % GB : e / GK, q = a_rows_fast ? e / GB : e % GK;
           const int gi = i0 + r, gk = k0 + q;
-          pa[u] = (gi < m && gk < k) ? A.get(gi, gk) : 0.0;
+          pa[u] = (gi < m && gk < k) ? tri_get(A, gi, gk, tri) : 0.0;
           const int qq = b_rows_fast ? e % GK : e / GB, cc = b_rows_fast ? e / GK : e % GB;
           const int bj = j0 + cc, bk = k0 + qq;
           pb[u] = (bk < k && bj < n) ? B.get(bk, bj) : 0.0;
@@ -252,7 +261,7 @@ __global__ void __launch_bounds__(HLU_NT, 2)
     const Mat B = resolve(c, tm.b);
     if (C.rows == 0 || C.cols == 0) continue;
     if (tm.kind == HLU_TERM_GEMM) {
-      if (A.cols > 0) tile_gemm(C, A, B, tm.alpha, sA, sB);
+      if (A.cols > 0) tile_gemm(C, A, B, tm.alpha, sA, sB, tm.assoc);
       continue;
     }
     const Mat M = resolve(c, tm.m);
@@ -295,7 +304,8 @@ __global__ void __launch_bounds__(HLU_NT, 2)
 #define RB 16
 
 // C (m x n) += alpha * A (m x k) * B (k x n); one warp.
-__device__ __forceinline__ void warp_gemm(const Mat &C, const Mat &A, const Mat &B, double alpha) {
+__device__ __forceinline__ void warp_gemm(const Mat &C, const Mat &A, const Mat &B, double alpha,
+                                          int tri = HLU_TRI_NONE) {
   const int l = threadIdx.x & 31;
   const int m = C.rows, n = C.cols, k = A.cols;
   for (int c = l; c - l < n; c += 32) {
@@ -309,7 +319,7 @@ __device__ __forceinline__ void warp_gemm(const Mat &C, const Mat &A, const Mat 
         const double b = on ? B.get(t, c) : 0.0;
 #pragma unroll
         for (int i = 0; i < RB; ++i)
-          if (i < rr) acc[i] = fma(A.get(r0 + i, t), b, acc[i]);
+          if (i < rr) acc[i] = fma(tri_get(A, r0 + i, t, tri), b, acc[i]);
       }
       if (on) {
 #pragma unroll
@@ -342,7 +352,7 @@ __global__ void __launch_bounds__(HLU_NT)
     const Mat A = resolve(c, tm.a);
     const Mat B = resolve(c, tm.b);
     if (tm.kind == HLU_TERM_GEMM) {
-      if (A.cols > 0) warp_gemm(C, A, B, tm.alpha);
+      if (A.cols > 0) warp_gemm(C, A, B, tm.alpha, tm.assoc);
       continue;
     }
     const Mat M = resolve(c, tm.m);

@@ -764,6 +764,32 @@ struct Planner {
     }
   }
 
+  // products with the H-matrix or its stored factors: y += op(h) x, one chain
+  // of terms in the reference's recursion order (hmatrix.py:188-200,
+  // hlu.py:720-767); tri = 0 full, 1 unit lower, 2 upper
+  void terms_tri(std::vector<Term> &ts, int h, const View &y, const View &x, int tri) {
+    const auto &H = nd(h);
+    if (H.kind == 0) {
+      ts.push_back(Term{1, y, dense_view(whole(h)), NULLV, x, 1.0, tri == 1 ? 2 : 1});
+      return;
+    }
+    if (H.kind != 2) throw std::runtime_error("factored matrix has a low-rank diagonal block");
+    for (int i = 0; i < H.nr; ++i)
+      for (int j = 0; j < H.nc; ++j) {
+        const int ch = child(h, i, j);
+        const auto &q = nd(ch);
+        const View ys = y.rows_slice(q.r0 - H.r0, q.r1 - H.r0), xs = x.rows_slice(q.c0 - H.c0, q.c1 - H.c0);
+        if (tri == 1 ? j < i : j > i) terms_matmat(ts, ys, whole(ch), xs, 1.0);
+        else if (j == i) terms_tri(ts, ch, ys, xs, tri);
+      }
+  }
+  void matvec(int h, const View &x, const View &y, const Iv &xr, const Iv &yr, int tri) {
+    std::vector<Term> ts;
+    if (tri == 0) terms_matmat(ts, y, whole(h), x, 1.0);
+    else terms_tri(ts, h, y, x, tri);
+    gemm_op(ts, {Iv{nd(h).lo, nd(h).hi}, xr}, {yr}, F_STATIC, 0.0, -1, false, {}, {});
+  }
+
   // ---------------------------------------------------------- schedule
   std::vector<int64_t> levels;
   std::vector<int64_t> toffs;
@@ -1319,6 +1345,17 @@ extern "C" int hlu_plan_build(hlu_plan **out, const hlu_plan_node *nodes, int64_
           const Iv r{c.vec_res, c.vec_res + 1};
           if (c.kind == HLU_CMD_FWD_VEC) P.vec_lower(c.a, v, x.r0, r);
           else P.vec_upper(c.a, v, x.r0, r);
+          break;
+        }
+        case HLU_CMD_MATVEC:
+        case HLU_CMD_LOWER_MATVEC:
+        case HLU_CMD_UPPER_MATVEC: {
+          const auto &h = nodes[c.a];
+          const int nr = h.r1 - h.r0, nc = h.c1 - h.c0;
+          const View xv{c.vec_off, nc, c.vec_cols, 1, nc, -1, -1};
+          const View yv{c.vec2_off, nr, c.vec_cols, 1, nr, -1, -1};
+          P.matvec(c.a, xv, yv, Iv{c.vec_res, c.vec_res + 1}, Iv{c.vec2_res, c.vec2_res + 1},
+                   c.kind == HLU_CMD_MATVEC ? 0 : (c.kind == HLU_CMD_LOWER_MATVEC ? 1 : 2));
           break;
         }
         default: throw std::runtime_error("unknown plan command");

@@ -23,7 +23,7 @@ import numpy as np
 
 from .blocks import INADMISSIBLE, PARTITIONED, BlockNode
 from .clustering import Cluster
-from .hmatrix import DENSE, HMatrix, Skeleton, StructureError, _matvec_into, build_skeleton
+from .hmatrix import DENSE, HMatrix, Skeleton, StructureError, build_skeleton
 from .lowrank import TruncationControl
 from .planner import DEFAULT_CAP, Layout, Planner
 
@@ -88,6 +88,9 @@ def _auto_capacity(roots, ctl):
     return int(cap)
 
 
+_TRI = {"lower_matvec": 1, "upper_matvec": 2}
+
+
 def plan_call(roots, commands, capacity, extras=None, planner="native"):
     """Layout + packed schedule for a list of planner commands, e.g.
     ``[("factor", h)]``; ``planner`` = "native" (C++) or "python" (the
@@ -100,6 +103,9 @@ def plan_call(roots, commands, capacity, extras=None, planner="native"):
         return layout, packed
     pl = Planner(layout)
     for cmd in commands:
+        if cmd[0] in _TRI:
+            pl.matvec(*cmd[1:], tri=_TRI[cmd[0]])
+            continue
         name = {"fwd": "forward_vector", "bwd": "backward_vector"}.get(cmd[0], cmd[0])
         getattr(pl, name)(*cmd[1:])
     from .schedule import pack
@@ -186,38 +192,71 @@ def forward_solve(h: HMatrix, rhs, device=None):
     return y.reshape(rhs.shape)
 
 
-# -- triangular matvec with the stored factors (host utilities, hlu.py:720-767)
+# -- products with the matrix / its stored factors, on the GPU
+#    (hmatrix.py:178-200, hlu.py:720-767, residual probe bench.py:142-152)
 
 
-def lower_unit_matvec(h: HMatrix, x):
+def _products(roots, commands, vectors, outputs, device=None):
+    """Run matvec-type commands over pooled vectors; returns the outputs."""
+    extras = dict(vectors)
+    for name, rows, cols in outputs:
+        extras[name] = np.zeros((rows, cols))
+    call = _run(roots, commands, TruncationControl(), _auto_capacity(roots, None), device, extras=extras,
+                keep=True)
+    try:
+        return [call.extra(name) for name, _, _ in outputs]
+    finally:
+        call.close()
+
+
+def _as_block(h, x, n):
     x = np.asarray(x, dtype=float)
-    y = np.zeros_like(x, dtype=float)
-    _tri_into(h, x, y, lower=True)
-    return y
+    if x.shape[0] != n:
+        raise ValueError(f"length mismatch: {n} columns vs {x.shape[0]}")
+    return x, np.ascontiguousarray(x.reshape(n, -1))
 
 
-def upper_matvec(h: HMatrix, x):
-    x = np.asarray(x, dtype=float)
-    y = np.zeros_like(x, dtype=float)
-    _tri_into(h, x, y, lower=False)
-    return y
+def hmatvec(h: HMatrix, x, device=None):
+    """y = h @ x over the block structure (reference ``hmatvec``,
+    hmatrix.py:178-200): one GPU term chain per block row."""
+    x, xb = _as_block(h, x, h.cols)
+    (y,) = _products([h], [("matvec", h, "x", "y")], {"x": xb}, [("y", h.rows, xb.shape[1])], device)
+    return y.reshape((h.rows,) + x.shape[1:])
 
 
-def _tri_into(h, x, y, lower):
-    if h.kind == DENSE:
-        y += (np.tril(h.data, -1) @ x + x) if lower else (np.triu(h.data) @ x)
-        return
-    if h.kind != PARTITIONED:
-        raise StructureError("factored matrix has a low-rank diagonal block")
-    r0 = h.row_range[0]
-    for i, line in enumerate(h.data):
-        for j, ch in enumerate(line):
-            (i0, i1), (j0, j1) = ch.row_range, ch.col_range
-            xs, ys = x[j0 - r0 : j1 - r0], y[i0 - r0 : i1 - r0]
-            if (j < i) if lower else (j > i):
-                _matvec_into(ch, xs, ys)
-            elif j == i:
-                _tri_into(ch, xs, ys, lower)
+def lower_unit_matvec(h: HMatrix, x, device=None):
+    """y = L x with the unit lower factor stored in a factored h (hlu.py:720-727)."""
+    x, xb = _as_block(h, x, h.rows)
+    (y,) = _products([h], [("lower_matvec", h, "x", "y")], {"x": xb}, [("y", h.rows, xb.shape[1])], device)
+    return y.reshape(x.shape)
+
+
+def upper_matvec(h: HMatrix, x, device=None):
+    """y = U x with the upper factor stored in a factored h (hlu.py:745-767)."""
+    x, xb = _as_block(h, x, h.rows)
+    (y,) = _products([h], [("upper_matvec", h, "x", "y")], {"x": xb}, [("y", h.rows, xb.shape[1])], device)
+    return y.reshape(x.shape)
+
+
+def residual_probe(original: HMatrix, factored: HMatrix, seed=0, probes=10, device=None):
+    """Worst relative residual ||A x - L (U x)|| / ||A x|| over random x
+    (reference ``residual_probe``, bench.py:142-152, same rng draws); all
+    probes run as columns of one GPU call (A x, U x, then L (U x))."""
+    rng = np.random.default_rng(seed)
+    n = original.cols
+    xb = np.stack([rng.standard_normal(n) for _ in range(probes)], axis=1)
+    ax, _, lux = _products(
+        [original, factored],
+        [("matvec", original, "x", "ax"), ("upper_matvec", factored, "x", "ux"),
+         ("lower_matvec", factored, "ux", "lux")],
+        {"x": xb},
+        [("ax", n, probes), ("ux", n, probes), ("lux", n, probes)],
+        device,
+    )
+    worst = 0.0
+    for p in range(probes):
+        worst = max(worst, float(np.linalg.norm(ax[:, p] - lux[:, p]) / np.linalg.norm(ax[:, p])))
+    return worst
 
 
 def emit_task_graph(plan: HluPlan):

@@ -35,6 +35,7 @@ assert RKT.itemsize == 64 and LAUNCH.itemsize == 24 and RKT_ITEM.itemsize == 8
 K_GETRF, K_TRSM, K_GEMM, K_RKT32, K_RKT64, K_GEMM_SMALL = 0, 1, 2, 3, 4, 5
 TRSM_LOWER_UNIT, TRSM_RIGHT_UPPER, TRSM_LEFT_UPPER = 0, 1, 2
 TERM_ZERO, TERM_GEMM, TERM_TRIPLE = 0, 1, 2
+TRI_NONE, TRI_UPPER, TRI_UNIT_LOWER = 0, 1, 2  # assoc of a GEMM term (include/hlu_b200.h)
 RK_ADD, RK_RECOMPRESS = 0, 1
 
 # effective-flop formulas (reference FlopCounter sites, hlu.py:408-637)

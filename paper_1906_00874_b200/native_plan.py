@@ -26,10 +26,13 @@ NODE = np.dtype([("kind", "<i4"), ("r0", "<i4"), ("r1", "<i4"), ("c0", "<i4"), (
                  ("nr", "<i4"), ("nc", "<i4"), ("child0", "<i4"), ("lo", "<i4"), ("hi", "<i4"),
                  ("slot", "<i4"), ("pad", "<i4"), ("off_a", "<i8"), ("off_b", "<i8")])
 CMD = np.dtype([("kind", "<i4"), ("a", "<i4"), ("b", "<i4"), ("c", "<i4"), ("vec_off", "<i8"),
-                ("vec_cols", "<i4"), ("pad", "<i4"), ("vec_res", "<i8")])
-assert NODE.itemsize == 64 and CMD.itemsize == 40
+                ("vec_cols", "<i4"), ("pad", "<i4"), ("vec_res", "<i8"), ("vec2_off", "<i8"),
+                ("vec2_res", "<i8")])
+assert NODE.itemsize == 64 and CMD.itemsize == 56
 
-CMD_FACTOR, CMD_SOLVE_LOWER, CMD_SOLVE_UPPER, CMD_UPDATE, CMD_FWD_VEC, CMD_BWD_VEC = range(6)
+(CMD_FACTOR, CMD_SOLVE_LOWER, CMD_SOLVE_UPPER, CMD_UPDATE, CMD_FWD_VEC, CMD_BWD_VEC, CMD_MATVEC,
+ CMD_LOWER_MATVEC, CMD_UPPER_MATVEC) = range(9)
+_MATVEC_CMDS = {"matvec": CMD_MATVEC, "lower_matvec": CMD_LOWER_MATVEC, "upper_matvec": CMD_UPPER_MATVEC}
 
 _lib = None
 
@@ -107,22 +110,30 @@ SPLIT_ROWS = 64
 def plan(layout, commands, split_rows=SPLIT_ROWS):
     """commands: list of (kind, nodes..., extras) in the planner's terms:
     ("factor", h) | ("solve_lower", l, b) | ("solve_upper", b, u) |
-    ("update", c, a, b) | ("fwd", h, name) | ("bwd", h, name)."""
+    ("update", c, a, b) | ("fwd", h, name) | ("bwd", h, name) |
+    ("matvec" | "lower_matvec" | "upper_matvec", h, x_name, y_name)."""
     nodes, index = flatten_nodes(layout)
     cmds = np.zeros(len(commands), dtype=CMD)
     for i, c in enumerate(commands):
         kind = c[0]
         if kind == "factor":
-            cmds[i] = (CMD_FACTOR, index[id(c[1])], 0, 0, 0, 0, 0, 0)
+            cmds[i] = (CMD_FACTOR, index[id(c[1])], 0, 0, 0, 0, 0, 0, 0, 0)
         elif kind == "solve_lower":
-            cmds[i] = (CMD_SOLVE_LOWER, index[id(c[1])], index[id(c[2])], 0, 0, 0, 0, 0)
+            cmds[i] = (CMD_SOLVE_LOWER, index[id(c[1])], index[id(c[2])], 0, 0, 0, 0, 0, 0, 0)
         elif kind == "solve_upper":
-            cmds[i] = (CMD_SOLVE_UPPER, index[id(c[1])], index[id(c[2])], 0, 0, 0, 0, 0)
+            cmds[i] = (CMD_SOLVE_UPPER, index[id(c[1])], index[id(c[2])], 0, 0, 0, 0, 0, 0, 0)
         elif kind == "update":
-            cmds[i] = (CMD_UPDATE, index[id(c[1])], index[id(c[2])], index[id(c[3])], 0, 0, 0, 0)
+            cmds[i] = (CMD_UPDATE, index[id(c[1])], index[id(c[2])], index[id(c[3])], 0, 0, 0, 0, 0, 0)
         elif kind in ("fwd", "bwd"):
             off, rows, cols, res = layout.extra[c[2]]
-            cmds[i] = (CMD_FWD_VEC if kind == "fwd" else CMD_BWD_VEC, index[id(c[1])], 0, 0, off, cols, 0, res)
+            cmds[i] = (CMD_FWD_VEC if kind == "fwd" else CMD_BWD_VEC, index[id(c[1])], 0, 0, off, cols, 0, res,
+                       0, 0)
+        elif kind in _MATVEC_CMDS:
+            xo, _, cols, xr = layout.extra[c[2]]
+            yo, _, ycols, yr = layout.extra[c[3]]
+            if ycols != cols:
+                raise ValueError("matvec: x and y differ in width")
+            cmds[i] = (_MATVEC_CMDS[kind], index[id(c[1])], 0, 0, xo, cols, 0, xr, yo, yr)
         else:
             raise ValueError(kind)
     L = lib()

@@ -34,7 +34,8 @@ from .blocks import PARTITIONED
 from .hmatrix import DENSE, LOWRANK, HMatrix, StructureError, build_skeleton
 from .ir import (
     F_LIN, F_QUAD, F_RKUPD, F_STATIC, NULL_VIEW, RK_ADD, RK_RECOMPRESS, TERM_GEMM, TERM_TRIPLE,
-    TERM_ZERO, TRSM_LEFT_UPPER, TRSM_LOWER_UNIT, TRSM_RIGHT_UPPER, View, colmajor, rkt_ws_doubles,
+    TERM_ZERO, TRI_UNIT_LOWER, TRI_UPPER, TRSM_LEFT_UPPER, TRSM_LOWER_UNIT, TRSM_RIGHT_UPPER, View, colmajor,
+    rkt_ws_doubles,
 )
 
 TEMP_SHIFT = 36  # virtual address of temp t: (t + 1) << TEMP_SHIFT (2^27 temps, 2^36-double offsets)
@@ -660,6 +661,39 @@ class Planner:
         """x := U^-1 x: block back-substitution (restated; absent in the reference)."""
         off, rows, cols, res = self.L.extra[vec_name]
         self._vec_upper(u, View(off, rows, cols, 1, rows), u.row_range[0], (res, res + 1))
+
+    # ------------------------------------------- products with h / its factors
+    def matvec(self, h, x_name, y_name, tri=0):
+        """y += op(h) x for pooled vectors, one term chain in the reference's
+        recursion order: op = h (``hmatvec``, hmatrix.py:178-200), the unit
+        lower factor (tri=1) or the upper factor (tri=2) of a factored h
+        (``lower_unit_matvec`` / ``upper_matvec``, hlu.py:720-767)."""
+        xo, xrows, cols, xres = self.L.extra[x_name]
+        yo, yrows, _, yres = self.L.extra[y_name]
+        x, y = View(xo, xrows, cols, 1, xrows), View(yo, yrows, cols, 1, yrows)
+        terms = []
+        if tri == 0:
+            self.terms_matmat(terms, y, h, x, 1.0)
+        else:
+            self._terms_tri(terms, h, y, x, tri)
+        self.gemm_op(terms, [self.L.res(h), (xres, xres + 1)], [(yres, yres + 1)])
+
+    def _terms_tri(self, terms, h, y, x, tri):
+        if h.kind == DENSE:
+            terms.append((TERM_GEMM, y, self.dense_view(h), NULL_VIEW, x, 1.0,
+                          TRI_UNIT_LOWER if tri == 1 else TRI_UPPER))
+            return
+        if not _part(h):
+            raise StructureError("factored matrix has a low-rank diagonal block")
+        for i, line in enumerate(h.data):
+            for j, ch in enumerate(line):
+                (i0, i1), (j0, j1) = ch.row_range, ch.col_range
+                r0, c0 = h.row_range[0], h.col_range[0]
+                ys, xs = y.rows_slice(i0 - r0, i1 - r0), x.rows_slice(j0 - c0, j1 - c0)
+                if (j < i) if tri == 1 else (j > i):
+                    self.terms_matmat(terms, ys, ch, xs, 1.0)
+                elif j == i:
+                    self._terms_tri(terms, ch, ys, xs, tri)
 
     def _vec_upper(self, u, x, base, res):
         if u.kind == DENSE:

@@ -83,6 +83,11 @@ class CpuMachine:
                 continue
             a, b = self.v(t["a"]), self.v(t["b"])
             if kind == ir.TERM_GEMM:
+                tri = int(t["assoc"])
+                if tri == ir.TRI_UPPER:
+                    a = np.triu(a)
+                elif tri == ir.TRI_UNIT_LOWER:
+                    a = np.tril(a, -1) + np.eye(a.shape[0], a.shape[1])
                 c += t["alpha"] * (a @ b)
             else:
                 m = self.v(t["m"])
