@@ -105,9 +105,48 @@ def flatten_nodes(layout):
 
 
 SPLIT_ROWS = 64
+PLAN_CACHE_ENV = "HLU_PLAN_CACHE"  # directory of cached plans (unset: no cache)
+_PACKED_ARRAYS = ("getrf", "trsm", "gemm", "terms", "rkt", "parts", "launches", "flop_formula", "flop_coef",
+                  "flop_log", "lu_op_ids", "op_levels", "wait_dense", "wait_rkt")
+_PACKED_INTS = ("nlevels", "arena_doubles", "nlog", "nranks")
 
 
-def plan(layout, commands, split_rows=SPLIT_ROWS):
+def plan_key(nodes, cmds, scalars):
+    """The native planner is a pure function of the node table, the command
+    list and a few scalars; their bytes (plus the planner library's) key a
+    cached plan (the analogue of the reference's save/load_hmatrix for the
+    flattened schedule)."""
+    import hashlib
+
+    d = hashlib.sha256()
+    d.update(nodes.tobytes())
+    d.update(cmds.tobytes())
+    d.update(np.asarray(scalars, dtype=np.int64).tobytes())
+    with open(PLAN_LIB, "rb") as f:
+        d.update(hashlib.sha256(f.read()).digest())
+    return d.hexdigest()
+
+
+def save_packed(path, packed, nops):
+    rec = {f: getattr(packed, f) for f in _PACKED_ARRAYS if getattr(packed, f) is not None}
+    for f in _PACKED_INTS:
+        rec[f] = np.int64(getattr(packed, f))
+    rec["nops"] = np.int64(nops)
+    rec["lu_labels"] = np.array(packed.lu_labels, dtype=object)
+    tmp = f"{path}.{os.getpid()}.tmp.npz"
+    np.savez(tmp, **rec)
+    os.replace(tmp, path)  # atomic: concurrent planners never see a partial file
+
+
+def load_packed(path):
+    with np.load(path, allow_pickle=True) as z:
+        kw = {f: (z[f] if f in z.files else None) for f in _PACKED_ARRAYS}
+        kw.update({f: int(z[f]) for f in _PACKED_INTS})
+        kw["lu_labels"] = [str(x) for x in z["lu_labels"]]
+        return Packed(**kw), int(z["nops"])
+
+
+def plan(layout, commands, split_rows=SPLIT_ROWS, cache_dir=None):
     """commands: list of (kind, nodes..., extras) in the planner's terms:
     ("factor", h) | ("solve_lower", l, b) | ("solve_upper", b, u) |
     ("update", c, a, b) | ("fwd", h, name) | ("bwd", h, name) |
@@ -136,6 +175,22 @@ def plan(layout, commands, split_rows=SPLIT_ROWS):
             cmds[i] = (_MATVEC_CMDS[kind], index[id(c[1])], 0, 0, xo, cols, 0, xr, yo, yr)
         else:
             raise ValueError(kind)
+    cache_dir = cache_dir if cache_dir is not None else os.environ.get(PLAN_CACHE_ENV)
+    path = None
+    if cache_dir:
+        key = plan_key(nodes, cmds, (layout.cap, layout.ident_off, layout.nslots, layout.nrk,
+                                     layout.payload_doubles, split_rows))
+        path = os.path.join(cache_dir, f"plan_{key[:32]}.npz")
+        if os.path.exists(path):
+            return load_packed(path)
+    packed, nops = _build(layout, nodes, cmds, split_rows)
+    if path is not None:
+        os.makedirs(cache_dir, exist_ok=True)
+        save_packed(path, packed, nops)
+    return packed, nops
+
+
+def _build(layout, nodes, cmds, split_rows):
     L = lib()
     h = ctypes.c_void_p()
     rc = L.hlu_plan_build(ctypes.byref(h), nodes.ctypes.data, len(nodes), cmds.ctypes.data, len(cmds),

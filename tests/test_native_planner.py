@@ -156,3 +156,21 @@ def test_two_chain_waits_reproduce_reference(name, dense_first):
     read_pool(L, pool, ranks)
     assert np.array_equal(cases.ranks(h), g["ranks_out"])
     assert abs(effective_flops(p, M.log) - float(g["flops"])) <= 1e-12 * float(g["flops"])
+
+
+def test_plan_cache_round_trip(tmp_path):
+    """A cached plan (keyed by the planner's inputs) loads back identical."""
+    h, _ = cases.CASES["sphere_1024"][0]()
+    L = Layout(h, cap=32)
+    fresh, n0 = native_plan.plan(L, [("factor", h)])
+    first, n1 = native_plan.plan(L, [("factor", h)], cache_dir=str(tmp_path))
+    files = list(tmp_path.iterdir())
+    assert len(files) == 1
+    cached, n2 = native_plan.plan(L, [("factor", h)], cache_dir=str(tmp_path))
+    assert n0 == n1 == n2
+    for p in (first, cached):
+        _compare(fresh, p)
+        assert np.array_equal(fresh.wait_dense, p.wait_dense) and np.array_equal(fresh.wait_rkt, p.wait_rkt)
+    # a different capacity is a different plan
+    native_plan.plan(Layout(h, cap=48), [("factor", h)], cache_dir=str(tmp_path))
+    assert len(list(tmp_path.iterdir())) == 2
