@@ -998,9 +998,12 @@ __device__ int r_core(const double *Rx, int ldx, const double *Ry, int ldy, int 
         double pcol[KB];
 #pragma unroll
         for (int i = 0; i < KB; ++i) pcol[i] = __shfl_sync(0xffffffffu, col[i], src);
+        // both lanes of a pair compute the pair's rotation from the same
+        // operands in the same order (fma(x, y, .) == fma(y, x, .)), so the
+        // b lane needs no hand-off; V lanes take it from their M lane.  No
+        // rotation = (cs, sn) = (1, 0), which leaves a column bit-unchanged.
         double cs = 1.0, sn = 0.0;
-        int rot = 0;
-        if (!isV && act && is_a) {
+        if (!isV && act) {
           double a4[4] = {0.0, 0.0, 0.0, 0.0}, b4[4] = {0.0, 0.0, 0.0, 0.0}, g4[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
           for (int i = 0; i < KB; ++i) {
@@ -1008,12 +1011,12 @@ __device__ int r_core(const double *Rx, int ldx, const double *Ry, int ldy, int 
             b4[i & 3] = fma(pcol[i], pcol[i], b4[i & 3]);
             g4[i & 3] = fma(col[i], pcol[i], g4[i & 3]);
           }
-          const double al = (a4[0] + a4[1]) + (a4[2] + a4[3]);
-          const double be = (b4[0] + b4[1]) + (b4[2] + b4[3]);
+          const double so = (a4[0] + a4[1]) + (a4[2] + a4[3]);
+          const double sp = (b4[0] + b4[1]) + (b4[2] + b4[3]);
+          const double al = is_a ? so : sp, be = is_a ? sp : so;
           const double ga = (g4[0] + g4[1]) + (g4[2] + g4[3]);
           const double g2 = ga * ga, ab = al * be;
           if (ga != 0.0 && g2 > 1e-30 * ab) {
-            rot = 1;
             if (g2 > 1e-16 * ab && fmax(al, be) > cmax) big = 1;
             // t = tan(theta) = 2 ga / (d + sign(d) sqrt(d^2 + 4 ga^2)), d = be - al
             const double dd = be - al;
@@ -1024,15 +1027,9 @@ __device__ int r_core(const double *Rx, int ldx, const double *Ry, int ldy, int 
             sn = cs * t;
           }
         }
-        // b lanes take the rotation of their pair's a lane, V lanes that of their column
-        const int from = (!isV && act && !is_a) ? src : l;
-        cs = __shfl_sync(0xffffffffu, cs, from);
-        sn = __shfl_sync(0xffffffffu, sn, from);
-        rot = __shfl_sync(0xffffffffu, rot, from);
         cs = __shfl_sync(0xffffffffu, cs, hl);
         sn = __shfl_sync(0xffffffffu, sn, hl);
-        rot = __shfl_sync(0xffffffffu, rot, hl);
-        if (rot) {
+        {
           // a: cs x_a - sn y_b ; b: sn x_a + cs y_b  (own, partner)
           const double s2 = is_a ? -sn : sn;
 #pragma unroll
