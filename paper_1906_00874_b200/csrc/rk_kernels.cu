@@ -254,6 +254,21 @@ __device__ unsigned long long g_sweeps = 0;  // total Jacobi sweeps (diagnostics
 __device__ unsigned long long g_bsweeps[4];  // Jacobi sweeps, then rounds, of the CTA cores [KM == 64]
 #endif
 
+// Rotation (cs, sn) that annihilates ga in the pair's Gram [al ga; ga be]:
+// tan = 2 ga / (d + sign(d) r), d = be - al, r = sqrt(d^2 + 4 ga^2).  With
+// w = |d| + r this is cs = w / sqrt(w^2 + 4 ga^2), sn = sign(d) 2 ga /
+// sqrt(w^2 + 4 ga^2): one refined reciprocal square root normalises the pair
+// (cs^2 + sn^2 = 1 to rounding whatever the accuracy of r), no division, one
+// transcendental step less on the round's critical path.
+__device__ __forceinline__ void jacobi_rot(double al, double be, double ga, double g2, double &cs, double &sn) {
+  const double d = be - al;
+  const double q2 = fma(d, d, 4.0 * g2);
+  const double w = fabs(d) + q2 * rsqrt_nr1(q2);
+  const double x = rsqrt_nr2(fma(w, w, 4.0 * g2));
+  cs = w * x;
+  sn = copysign(2.0 * x, d) * ga;
+}
+
 // Round-robin pairing table: round r, slot i -> (a, b); computed once per op.
 template <int NT>
 __device__ __forceinline__ void build_pairs(unsigned char *pa, unsigned char *pb, int qq) {
@@ -627,12 +642,8 @@ __device__ void jacobi_lp(double *X, double *V, int n, const unsigned char *pa, 
         const double g2 = ga * ga, ab = al * be;
         if (ga == 0.0 || !(g2 > 1e-30 * ab)) continue;  // |ga| <= 1e-15 sqrt(al be)
         if (g2 > 1e-16 * ab) big = 1;                    // not yet in the quadratic regime
-        // t = tan(theta) = 2 ga / (d + sign(d) sqrt(d^2 + 4 ga^2)), d = be - al
-        const double d = be - al;
-        const double q2 = fma(d, d, 4.0 * g2);
-        const double rq = q2 * rsqrt_nr1(q2);
-        const double t = 2.0 * ga * rcp_nr1(d + copysign(rq, d));
-        const double cs = rsqrt_nr2(fma(t, t, 1.0)), sn = cs * t;
+        double cs, sn;
+        jacobi_rot(al, be, ga, g2, cs, sn);
 #pragma unroll
         for (int q = 0; q < RPL; ++q) {
           const int i = l + q * LP;
@@ -881,65 +892,6 @@ __device__ __forceinline__ void r_qr_step(double (&x)[RPL][KB], double &tau_j, i
   }
 }
 
-// The same step with a run-time j: the step loop is not unrolled, so one
-// step's code (column j picked out and written back by compile-time selects,
-// columns c <= j skipped by warp-uniform branches) serves every j.  The
-// arithmetic of every column is r_qr_step's, in the same order (bit-identical);
-// the kernel's code shrinks by ~KB x, which is what its instruction-fetch
-// stalls ask for.
-template <int RPL, int KB>
-__device__ __forceinline__ void r_qr_step_rt(double (&x)[RPL][KB], double *tau, int j, int l) {
-  double xj[RPL];
-#pragma unroll
-  for (int q = 0; q < RPL; ++q) {
-    xj[q] = 0.0;
-#pragma unroll
-    for (int c = 0; c < KB; ++c)
-      if (c == j) xj[q] = x[q][c];
-  }
-  const double x0 = xj[0];
-  double ss = l > j ? x0 * x0 : 0.0;
-#pragma unroll
-  for (int q = 1; q < RPL; ++q) ss = fma(xj[q], xj[q], ss);
-  ss = warp_sum(ss);
-  const double alpha = __shfl_sync(0xffffffffu, x0, j);
-  double tj = 0.0, beta = alpha, sc = 0.0;
-  if (ss != 0.0) {
-    const double n2 = fma(alpha, alpha, ss);
-    const double rn = fast_rsqrt(n2);
-    beta = -copysign(n2 * rn, alpha);
-    tj = fma(fabs(alpha), rn, 1.0);
-    sc = fast_rcp(alpha - beta);
-  }
-  double v[RPL];
-  v[0] = l > j ? x0 * sc : (l == j ? 1.0 : 0.0);
-#pragma unroll
-  for (int q = 1; q < RPL; ++q) v[q] = xj[q] * sc;
-  const double nj0 = l > j ? v[0] : (l == j ? beta : x0);
-#pragma unroll
-  for (int c = 0; c < KB; ++c) {
-    if (c == j) {
-      x[0][c] = nj0;
-#pragma unroll
-      for (int q = 1; q < RPL; ++q) x[q][c] = v[q];
-    }
-  }
-  if (l == 0) tau[j] = tj;  // straight to the warp's shared tau (no register array)
-#pragma unroll
-  for (int c = 0; c < KB; ++c) {
-    if (c > j) {
-      double pc = v[0] * x[0][c];
-#pragma unroll
-      for (int q = 1; q < RPL; ++q) pc = fma(v[q], x[q][c], pc);
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) pc += __shfl_xor_sync(0xffffffffu, pc, o);
-      const double f = tj * pc;
-#pragma unroll
-      for (int q = 0; q < RPL; ++q) x[q][c] -= f * v[q];
-    }
-  }
-}
-
 template <int RPL, int KB>
 __device__ __forceinline__ void r_store(const double (&x)[RPL][KB], const double (&ta)[KB], double *S, double *tau,
                                         int l) {
@@ -1077,13 +1029,7 @@ __device__ int r_core(const double *Rx, int ldx, const double *Ry, int ldy, int 
           const double g2 = ga * ga, ab = al * be;
           if (ga != 0.0 && g2 > 1e-30 * ab) {
             if (g2 > 1e-16 * ab && fmax(al, be) > cmax) big = 1;
-            // t = tan(theta) = 2 ga / (d + sign(d) sqrt(d^2 + 4 ga^2)), d = be - al
-            const double dd = be - al;
-            const double q2 = fma(dd, dd, 4.0 * g2);
-            const double rq = q2 * rsqrt_nr1(q2);
-            const double t = 2.0 * ga * rcp_nr1(dd + copysign(rq, dd));
-            cs = rsqrt_nr2(fma(t, t, 1.0));
-            sn = cs * t;
+            jacobi_rot(al, be, ga, g2, cs, sn);
           }
         }
         cs = __shfl_sync(0xffffffffu, cs, hl);
@@ -1171,30 +1117,7 @@ __device__ void r_trunc(const hlu_ctx &c, const hlu_rkt_desc &o, const hlu_rkpar
   bool shortcut;
   const int K = logged_K(c, o, &shortcut);
   const int m = o.m, n = o.n;
-  if (RPL == 2 && KB == 16) {  // X and Y interleaved, run-time step loop
-    double x[RPL][KB], y[RPL][KB];
-    r_load<RPL, KB>(P, np, true, m, K, x, l);
-    r_load<RPL, KB>(P, np, false, n, K, y, l);
-    if (l < KB) {
-      tx[l] = 0.0;
-      ty[l] = 0.0;
-    }
-    __syncwarp();
-#pragma unroll 1
-    for (int j = 0; j < K; ++j) {
-      r_qr_step_rt<RPL, KB>(x, tx, j, l);
-      r_qr_step_rt<RPL, KB>(y, ty, j, l);
-    }
-    constexpr int ROWS_ = 32 * RPL;
-#pragma unroll
-    for (int j = 0; j < KB; ++j) {
-#pragma unroll
-      for (int q = 0; q < RPL; ++q) {
-        Sx[l + 32 * q + ROWS_ * j] = x[q][j];
-        Sy[l + 32 * q + ROWS_ * j] = y[q][j];
-      }
-    }
-  } else if (RPL == 2) {  // X and Y interleaved
+  if (RPL == 2) {  // X and Y interleaved
     double x[RPL][KB], y[RPL][KB], tax[KB], tay[KB];
     r_load<RPL, KB>(P, np, true, m, K, x, l);
     r_load<RPL, KB>(P, np, false, n, K, y, l);
