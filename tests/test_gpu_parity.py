@@ -201,3 +201,32 @@ def test_baseline_config_rank_parity(name):
     y = forward_solve(h, g["rhs"])
     rel = np.linalg.norm(y - g["y_forward"]) / np.linalg.norm(g["y_forward"])
     assert rel <= 1e-8, rel
+
+
+@pytest.mark.parametrize("name", ["sphere_1024"])
+def test_rank_capacity_overflow_replans(name):
+    """Rk capacity below the ranks the LU produces: the kernels flag the
+    overflow, the call re-plans with a doubled capacity, and the result still
+    matches the reference fixtures (ranks and flop counter)."""
+    g = cases.golden(name)
+    build, ctl = cases.CASES[name]
+    h, _ = build()
+    kin = int(g["ranks_in"].max()) if len(g["ranks_in"]) else 1
+    cap = max(kin, 1)
+    assert int(g["ranks_out"].max()) > cap  # the case really overflows
+    plan = make_plan(h, TruncationControl(*ctl), capacity=cap)
+    hlu_factorize(plan)
+    assert np.array_equal(cases.ranks(h), g["ranks_out"])
+    assert abs(plan.flops.total - float(g["flops"])) <= 1e-12 * float(g["flops"])
+
+
+def test_multi_column_solve_matches_columnwise():
+    """hlu_solve with an n x 3 right-hand side equals three vector solves."""
+    build, ctl = cases.CASES["sphere_1024"]
+    h, _ = build()
+    hlu_factorize(make_plan(h, TruncationControl(*ctl)))
+    B = np.random.default_rng(5).standard_normal((h.rows, 3))
+    X = hlu_solve(h, B)
+    for j in range(3):
+        xj = hlu_solve(h, B[:, j])
+        assert np.linalg.norm(X[:, j] - xj) <= 1e-13 * np.linalg.norm(xj)
