@@ -229,7 +229,7 @@ int64_t hlu_debug_sweeps(int reset); /* total Jacobi sweeps run so far (diagnost
 /* core-kernel phase cycles [K<=32 | K>32][op count, R/combine, core product, QRCP, Jacobi,
  * rank, W + QRCP apply, combine apply], then the Jacobi sweeps and rounds of [K<=32, K>32]
  * (20 values; zeros unless built with -DHLU_BPROF) */
-int hlu_debug_bprof(unsigned long long *out, int reset);
+int hlu_debug_bprof(unsigned long long *out, int reset); /* out[32]: phase cycles (diagnostics build) */
 
 #ifdef __cplusplus
 }

@@ -252,6 +252,10 @@ __device__ void apply_chain(int total, int K, int ch, int kk, const double *W, i
 __device__ unsigned long long g_sweeps = 0;  // total Jacobi sweeps (diagnostics)
 #ifdef HLU_BPROF
 __device__ unsigned long long g_bsweeps[4];  // Jacobi sweeps, then rounds, of the CTA cores [KM == 64]
+// register warp path, [KB == 16]: k_rkt_r<2, KB> ops, cycles of load +
+// Householder QRs, core (M, Jacobi, rank), Q applies; then sweeps and calls of
+// the warp core r_core (all callers: k_rkt_r and k_rkt_bw)
+__device__ unsigned long long g_rprof[2][6];
 #endif
 
 // Rotation (cs, sn) that annihilates ga in the pair's Gram [al ga; ga be]:
@@ -1044,6 +1048,12 @@ __device__ int r_core(const double *Rx, int ldx, const double *Ry, int ldy, int 
       }
       if (!__any_sync(0xffffffffu, big)) {
         if (l == 0) atomicAdd(&g_sweeps, sweep + 1);
+#ifdef HLU_BPROF
+        if (l == 0) {
+          atomicAdd(&g_rprof[KB == 16][4], (unsigned long long)(sweep + 1));
+          atomicAdd(&g_rprof[KB == 16][5], 1ull);
+        }
+#endif
         break;
       }
     }
@@ -1117,6 +1127,13 @@ __device__ void r_trunc(const hlu_ctx &c, const hlu_rkt_desc &o, const hlu_rkpar
   bool shortcut;
   const int K = logged_K(c, o, &shortcut);
   const int m = o.m, n = o.n;
+#ifdef HLU_BPROF
+  long long rp_t = clock64();
+  unsigned long long rp_c[3];
+#define RPROF(k) do { const long long t_ = clock64(); rp_c[k] = (unsigned long long)(t_ - rp_t); rp_t = t_; } while (0)
+#else
+#define RPROF(k) do {} while (0)
+#endif
   if (RPL == 2) {  // X and Y interleaved
     double x[RPL][KB], y[RPL][KB], tax[KB], tay[KB];
     r_load<RPL, KB>(P, np, true, m, K, x, l);
@@ -1146,10 +1163,20 @@ __device__ void r_trunc(const hlu_ctx &c, const hlu_rkt_desc &o, const hlu_rkpar
     }
   }
   __syncwarp();
+  RPROF(0);
   const int kk = r_core<KB>(Sx, ROWS, Sy, ROWS, K, c, o.cap, Wx, Wy, perm, l);
+  RPROF(1);
   // B' = Q_y [V_sel; 0], A' = Q_x [(U S)_sel; 0]
   r_apply<RPL, KB>(Sy, ty, Wy, perm, K, kk, n, c.pool + o.out_b, l);
   r_apply<RPL, KB>(Sx, tx, Wx, perm, K, kk, m, c.pool + o.out_a, l);
+  RPROF(2);
+#ifdef HLU_BPROF
+  if (l == 0 && RPL == 2) {
+    atomicAdd(&g_rprof[KB == 16][0], 1ull);
+    for (int k = 0; k < 3; ++k) atomicAdd(&g_rprof[KB == 16][1 + k], rp_c[k]);
+  }
+#endif
+#undef RPROF
   if (l == 0) {
     c.ranks[o.out_slot] = kk;
     c.log[o.log + 2] = kk;
@@ -1721,19 +1748,22 @@ extern "C" int64_t hlu_rkt_items(const hlu_rkt_desc *d, int count, hlu_rkt_item 
   return n;
 }
 
-// diagnostics: core-kernel phase cycles (16 values; zeros unless built with -DHLU_BPROF)
+// diagnostics: core-kernel phase cycles (32 values; zeros unless built with -DHLU_BPROF):
+// [0,16) CTA cores, [16,20) CTA-core sweeps/rounds, [20,32) warp path (g_rprof)
 extern "C" int hlu_debug_bprof(unsigned long long *out, int reset) {
 #ifdef HLU_BPROF
   cudaDeviceSynchronize();
   if (cudaMemcpyFromSymbol(out, g_bprof, sizeof(g_bprof)) != cudaSuccess) return -1;
   if (cudaMemcpyFromSymbol(out + 16, g_bsweeps, sizeof(g_bsweeps)) != cudaSuccess) return -1;
+  if (cudaMemcpyFromSymbol(out + 20, g_rprof, sizeof(g_rprof)) != cudaSuccess) return -1;
   if (reset) {
     static const unsigned long long z[16] = {0};
     cudaMemcpyToSymbol(g_bprof, z, sizeof(z));
     cudaMemcpyToSymbol(g_bsweeps, z, sizeof(g_bsweeps));
+    cudaMemcpyToSymbol(g_rprof, z, sizeof(g_rprof));
   }
 #else
-  for (int i = 0; i < 20; ++i) out[i] = 0;
+  for (int i = 0; i < 32; ++i) out[i] = 0;
   (void)reset;
 #endif
   return 0;

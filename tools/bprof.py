@@ -20,7 +20,7 @@ def main():
     L, pl = plan_call([h], [("factor", h)], 32)
     call = DeviceCall(L, pl, TruncationControl(*ctl), use_graph=True)
     lib = _native.lib()
-    buf = (ctypes.c_ulonglong * 20)()
+    buf = (ctypes.c_ulonglong * 32)()
     call.snapshot()
     call.launch()
     call.sync()
@@ -39,6 +39,14 @@ def main():
               f"Jacobi sweeps per op {buf[16 + v] / max(ops, 1):.2f} rounds per op {buf[18 + v] / max(ops, 1):.1f}")
         for k in range(1, 8):
             print(f"   {names[k]:14s} {buf[8 * v + k] / 1.965e9:8.3f} s  {buf[8 * v + k] / max(ops, 1) / 1965:8.1f} us/op")
+    rn = ["load + QR", "core (M, Jacobi, rank)", "Q apply"]
+    for v, tag in ((0, "warp path KB=8"), (1, "warp path KB=16")):
+        b = 20 + 6 * v
+        ops = buf[b]
+        print(f"{tag}: k_rkt_r<2,{8 << v}> ops {ops}  warp-core calls (r + bw) {buf[b + 5]}  "
+              f"sweeps per call {buf[b + 4] / max(buf[b + 5], 1):.2f}")
+        for k in range(3):
+            print(f"   {rn[k]:24s} {buf[b + 1 + k] / 1.965e9:8.3f} s-warp  {buf[b + 1 + k] / max(ops, 1) / 1965:8.1f} us/op")
     print("jacobi sweeps (all paths, one run):", lib.hlu_debug_sweeps(0))
 
 
