@@ -850,6 +850,111 @@ __device__ __forceinline__ void r_load(const PartInfo *P, int np, bool left, int
   }
 }
 
+constexpr int pow2ceil(int n) { return n <= 1 ? 1 : 2 * pow2ceil((n + 1) / 2); }
+constexpr int ilog2(int n) { return n <= 1 ? 0 : 1 + ilog2(n / 2); }
+
+// Warp sums of N per-lane values (N a power of two <= 32) by reduce-scatter:
+// at each level a lane swaps half of its values with lane ^ o, so the N sums
+// cost N shuffles (plus 5 - log2 N single-value levels) instead of 5 N for N
+// butterflies.  Returns the sum of column tr_col(l); every lane of a group of
+// 32 / N lanes holds the same (bit-identical) value.
+template <int N>
+__device__ __forceinline__ double tr_reduce(double (&v)[N], int l) {
+#pragma unroll
+  for (int h = N / 2, o = 16; h >= 1; h >>= 1, o >>= 1) {
+    const bool up = (l & o) != 0;
+#pragma unroll
+    for (int i = 0; i < h; ++i) {
+      const double send = up ? v[i] : v[i + h];
+      const double keep = up ? v[i + h] : v[i];
+      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+    }
+  }
+  double r = v[0];
+#pragma unroll
+  for (int o = 16 >> ilog2(N); o > 0; o >>= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
+  return r;
+}
+
+// a lane holding column c after tr_reduce<N>
+template <int N>
+__device__ __forceinline__ constexpr int tr_lane(int c) {
+  int l = 0;
+  for (int h = N / 2, o = 16; h >= 1; h >>= 1, o >>= 1)
+    if (c & h) l |= o;
+  return l;
+}
+
+// Householder step J (compile time) on the register-resident factor, as
+// r_qr_step, with the KB-1-J column dots reduced by tr_reduce and broadcast
+// back: ~2.5x fewer shuffles per step (the warp path is shuffle-throughput
+// bound in wide levels).
+template <int RPL, int KB, int J>
+__device__ __forceinline__ void r_qr_step_tr(double (&x)[RPL][KB], double &tau_j, int l) {
+  constexpr int j = J;
+  const double x0 = x[0][j];
+  double ss = l > j ? x0 * x0 : 0.0;
+#pragma unroll
+  for (int q = 1; q < RPL; ++q) ss = fma(x[q][j], x[q][j], ss);
+  ss = warp_sum(ss);
+  const double alpha = __shfl_sync(0xffffffffu, x0, j);
+  double tj = 0.0, beta = alpha, sc = 0.0;
+  if (ss != 0.0) {
+    const double n2 = fma(alpha, alpha, ss);
+    const double rn = fast_rsqrt(n2);
+    beta = -copysign(n2 * rn, alpha);
+    tj = fma(fabs(alpha), rn, 1.0);
+    sc = fast_rcp(alpha - beta);
+  }
+  double v[RPL];
+  v[0] = l > j ? x0 * sc : (l == j ? 1.0 : 0.0);
+#pragma unroll
+  for (int q = 1; q < RPL; ++q) v[q] = x[q][j] * sc;
+  x[0][j] = l > j ? v[0] : (l == j ? beta : x0);
+#pragma unroll
+  for (int q = 1; q < RPL; ++q) x[q][j] = v[q];
+  tau_j = tj;
+  constexpr int NA = KB - 1 - J;  // columns j+1 .. KB-1
+  if constexpr (NA > 0) {
+    constexpr int N = pow2ceil(NA);
+    double w[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      if (i < NA) {
+        const int c = j + 1 + i;
+        w[i] = v[0] * x[0][c];
+#pragma unroll
+        for (int q = 1; q < RPL; ++q) w[i] = fma(v[q], x[q][c], w[i]);
+      } else {
+        w[i] = 0.0;
+      }
+    }
+    const double sum = tr_reduce<N>(w, l);
+#pragma unroll
+    for (int i = 0; i < NA; ++i) {
+      const int c = j + 1 + i;
+      const double f = tj * __shfl_sync(0xffffffffu, sum, tr_lane<N>(i));
+#pragma unroll
+      for (int q = 0; q < RPL; ++q) x[q][c] -= f * v[q];
+    }
+  }
+}
+
+// steps J, J+1, .. while J < K (X and Y interleaved when Y is given)
+template <int RPL, int KB, int J>
+struct RQrSteps {
+  static __device__ __forceinline__ void run(double (&x)[RPL][KB], double (&y)[RPL][KB], double (&tx)[KB],
+                                             double (&ty)[KB], int K, int l) {
+    if constexpr (J < KB) {
+      if (J < K) {
+        r_qr_step_tr<RPL, KB, J>(x, tx[J], l);
+        r_qr_step_tr<RPL, KB, J>(y, ty[J], l);
+        RQrSteps<RPL, KB, J + 1>::run(x, y, tx, ty, K, l);
+      }
+    }
+  }
+};
+
 // Householder step j (dlarfg conventions) on the register-resident factor;
 // columns >= K are zero and stay zero
 template <int RPL, int KB>
@@ -1142,11 +1247,8 @@ __device__ void r_trunc(const hlu_ctx &c, const hlu_rkt_desc &o, const hlu_rkpar
     for (int j = 0; j < KB; ++j) {
       tax[j] = 0.0;
       tay[j] = 0.0;
-      if (j < K) {
-        r_qr_step<RPL, KB>(x, tax[j], j, l);
-        r_qr_step<RPL, KB>(y, tay[j], j, l);
-      }
     }
+    RQrSteps<RPL, KB, 0>::run(x, y, tax, tay, K, l);
     r_store<RPL, KB>(x, tax, Sx, tx, l);
     r_store<RPL, KB>(y, tay, Sy, ty, l);
   } else {
