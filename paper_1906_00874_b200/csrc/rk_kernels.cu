@@ -97,6 +97,41 @@ __device__ __forceinline__ void make_reflector(double *S, int ld, int rows, int 
 // Apply the reflector H = I - tj [1; v] [1; v]^T (v = v[j+1 .. rows), unit at
 // row j) to nc <= NB columns T[:, c0 + b*cstep] (ld ldt); one warp, the nc
 // reductions interleaved.
+constexpr int pow2ceil(int n) { return n <= 1 ? 1 : 2 * pow2ceil((n + 1) / 2); }
+constexpr int ilog2(int n) { return n <= 1 ? 0 : 1 + ilog2(n / 2); }
+
+// Warp sums of N per-lane values (N a power of two <= 32) by reduce-scatter:
+// at each level a lane swaps half of its values with lane ^ o, so the N sums
+// cost N shuffles (plus 5 - log2 N single-value levels) instead of 5 N for N
+// butterflies.  Returns the sum of column tr_col(l); every lane of a group of
+// 32 / N lanes holds the same (bit-identical) value.
+template <int N>
+__device__ __forceinline__ double tr_reduce(double (&v)[N], int l) {
+#pragma unroll
+  for (int h = N / 2, o = 16; h >= 1; h >>= 1, o >>= 1) {
+    const bool up = (l & o) != 0;
+#pragma unroll
+    for (int i = 0; i < h; ++i) {
+      const double send = up ? v[i] : v[i + h];
+      const double keep = up ? v[i + h] : v[i];
+      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+    }
+  }
+  double r = v[0];
+#pragma unroll
+  for (int o = 16 >> ilog2(N); o > 0; o >>= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
+  return r;
+}
+
+// a lane holding column c after tr_reduce<N>
+template <int N>
+__device__ __forceinline__ constexpr int tr_lane(int c) {
+  int l = 0;
+  for (int h = N / 2, o = 16; h >= 1; h >>= 1, o >>= 1)
+    if (c & h) l |= o;
+  return l;
+}
+
 template <int NB>
 __device__ __forceinline__ void refl_cols(const double *v, int rows, int j, double tj, double *T, int ldt, int c0,
                                           int cstep, int nc, int l) {
@@ -109,14 +144,18 @@ __device__ __forceinline__ void refl_cols(const double *v, int rows, int j, doub
     for (int b = 0; b < NB; ++b)
       if (b < nc) acc[b] = fma(x, T[i + (c0 + b * cstep) * ldt], acc[b]);
   }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-#pragma unroll
-    for (int b = 0; b < NB; ++b) acc[b] += __shfl_xor_sync(0xffffffffu, acc[b], o);
-  }
   double f[NB];
+  if constexpr (NB == 1) {
+    acc[0] = warp_sum(acc[0]);
+    f[0] = (0 < nc) ? tj * (acc[0] + T[j + c0 * ldt]) : 0.0;
+  } else {
+    const double sum = tr_reduce<NB>(acc, l);  // NB dots: reduce-scatter, then broadcast
 #pragma unroll
-  for (int b = 0; b < NB; ++b) f[b] = (b < nc) ? tj * (acc[b] + T[j + (c0 + b * cstep) * ldt]) : 0.0;
+    for (int b = 0; b < NB; ++b) {
+      const double s_b = __shfl_sync(0xffffffffu, sum, tr_lane<NB>(b));
+      f[b] = (b < nc) ? tj * (s_b + T[j + (c0 + b * cstep) * ldt]) : 0.0;
+    }
+  }
   for (int i = j + 1 + l; i < rows; i += 32) {
     const double x = v[i];
 #pragma unroll
@@ -850,41 +889,6 @@ __device__ __forceinline__ void r_load(const PartInfo *P, int np, bool left, int
   }
 }
 
-constexpr int pow2ceil(int n) { return n <= 1 ? 1 : 2 * pow2ceil((n + 1) / 2); }
-constexpr int ilog2(int n) { return n <= 1 ? 0 : 1 + ilog2(n / 2); }
-
-// Warp sums of N per-lane values (N a power of two <= 32) by reduce-scatter:
-// at each level a lane swaps half of its values with lane ^ o, so the N sums
-// cost N shuffles (plus 5 - log2 N single-value levels) instead of 5 N for N
-// butterflies.  Returns the sum of column tr_col(l); every lane of a group of
-// 32 / N lanes holds the same (bit-identical) value.
-template <int N>
-__device__ __forceinline__ double tr_reduce(double (&v)[N], int l) {
-#pragma unroll
-  for (int h = N / 2, o = 16; h >= 1; h >>= 1, o >>= 1) {
-    const bool up = (l & o) != 0;
-#pragma unroll
-    for (int i = 0; i < h; ++i) {
-      const double send = up ? v[i] : v[i + h];
-      const double keep = up ? v[i + h] : v[i];
-      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
-    }
-  }
-  double r = v[0];
-#pragma unroll
-  for (int o = 16 >> ilog2(N); o > 0; o >>= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
-  return r;
-}
-
-// a lane holding column c after tr_reduce<N>
-template <int N>
-__device__ __forceinline__ constexpr int tr_lane(int c) {
-  int l = 0;
-  for (int h = N / 2, o = 16; h >= 1; h >>= 1, o >>= 1)
-    if (c & h) l |= o;
-  return l;
-}
-
 // Householder step J (compile time) on the register-resident factor, as
 // r_qr_step, with the KB-1-J column dots reduced by tr_reduce and broadcast
 // back: ~2.5x fewer shuffles per step (the warp path is shuffle-throughput
@@ -1043,14 +1047,10 @@ __device__ __forceinline__ void r_apply(const double *S, const double *tau, cons
 #pragma unroll
         for (int r = 1; r < RPL; ++r) p[q] = fma(v[r], a[r][q], p[q]);
       }
-#pragma unroll
-      for (int o2 = 16; o2 > 0; o2 >>= 1) {
-#pragma unroll
-        for (int q = 0; q < RK_NB; ++q) p[q] += __shfl_xor_sync(0xffffffffu, p[q], o2);
-      }
+      const double sum = tr_reduce<RK_NB>(p, l);  // RK_NB dots: reduce-scatter, then broadcast
 #pragma unroll
       for (int q = 0; q < RK_NB; ++q) {
-        const double f = tj * p[q];
+        const double f = tj * __shfl_sync(0xffffffffu, sum, tr_lane<RK_NB>(q));
 #pragma unroll
         for (int r = 0; r < RPL; ++r) a[r][q] -= f * v[r];
       }
