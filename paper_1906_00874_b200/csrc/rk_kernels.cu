@@ -539,10 +539,10 @@ __device__ void qrcp_fast(double *G, int p, int q, double *tau, int *cm, double 
     }
 #pragma unroll
     for (int b = 0; b < NB; ++b) acc[b] = (act[b] && tj != 0.0) ? fma(v0, c0[b], v1 * c1[b]) : 0.0;
+    {
+      const double sum = tr_reduce<NB>(acc, l);  // NB dots: reduce-scatter, then broadcast
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-#pragma unroll
-      for (int b = 0; b < NB; ++b) acc[b] += __shfl_xor_sync(0xffffffffu, acc[b], o);
+      for (int b = 0; b < NB; ++b) acc[b] = __shfl_sync(0xffffffffu, sum, tr_lane<NB>(b));
     }
     __syncwarp();  // every lane has read row j before lane 0 rewrites it
     double ns[NB];
@@ -567,15 +567,12 @@ __device__ void qrcp_fast(double *G, int p, int q, double *tau, int *cm, double 
       const double a1 = (l + 32 > j && l + 32 < p) ? c1[b] : 0.0;
       ns[b] = fma(a0, a0, a1 * a1);
     }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-#pragma unroll
-      for (int b = 0; b < NB; ++b) ns[b] += __shfl_xor_sync(0xffffffffu, ns[b], o);
-    }
-    if (l == 0) {
+    {
+      // NB norms by reduce-scatter; the lane holding column b writes it
+      const double sum = tr_reduce<NB>(ns, l);
 #pragma unroll
       for (int b = 0; b < NB; ++b)
-        if (act[b]) nrm[pc[b]] = ns[b];
+        if (l == tr_lane<NB>(b) && act[b]) nrm[pc[b]] = sum;
     }
     if (tid == 0) {
       cm[j] = bi;
