@@ -152,8 +152,8 @@ __device__ __forceinline__ void refl_cols(const double *v, int rows, int j, doub
     const double sum = tr_reduce<NB>(acc, l);  // NB dots: reduce-scatter, then broadcast
 #pragma unroll
     for (int b = 0; b < NB; ++b) {
-      const double s_b = __shfl_sync(0xffffffffu, sum, tr_lane<NB>(b));
-      f[b] = (b < nc) ? tj * (s_b + T[j + (c0 + b * cstep) * ldt]) : 0.0;
+      f[b] = 0.0;
+      if (b < nc) f[b] = tj * (__shfl_sync(0xffffffffu, sum, tr_lane<NB>(b)) + T[j + (c0 + b * cstep) * ldt]);
     }
   }
   for (int i = j + 1 + l; i < rows; i += 32) {
@@ -332,140 +332,13 @@ __device__ __forceinline__ void build_pairs(unsigned char *pa, unsigned char *pb
 
 // QR with column pivoting of G (p x q, p >= q, ld KM), in place, without
 // moving data: cm[j] is the physical column holding logical column j (the
-// pivot order), reflector j lives below row j of column cm[j], tau[j].
-// Each warp updates its columns (and recomputes their norms) together.
-template <int KM, int NT>
-__device__ void qrcp(double *G, int p, int q, double *tau, int *cm, double *nrm) {
-  const int tid = threadIdx.x, w = tid >> 5, l = tid & 31;
-  __shared__ double s_beta;
-  for (int c = tid; c < q; c += NT) cm[c] = c;
-  for (int c = w; c < q; c += (NT / 32)) {
-    double ss = 0.0;
-    for (int i = l; i < p; i += 32) ss += G[i + c * KM] * G[i + c * KM];
-    ss = warp_sum(ss);
-    if (l == 0) nrm[c] = ss;
-  }
-  __syncthreads();
-  constexpr int NB = (KM + (NT / 32) - 1) / (NT / 32);
-  for (int j = 0; j < q; ++j) {
-    if (w == 0) {
-      // pivot: largest remaining norm (first on ties), then the reflector
-      double best = -1.0;
-      int bi = j;
-      for (int c = j + l; c < q; c += 32) {
-        const double v = nrm[cm[c]];
-        if (v > best) {
-          best = v;
-          bi = c;
-        }
-      }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
-        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-        if (ob > best || (ob == best && oi < bi)) {
-          best = ob;
-          bi = oi;
-        }
-      }
-      const int cj = cm[bi];
-      __syncwarp();
-      if (l == 0 && bi != j) {
-        cm[bi] = cm[j];
-        cm[j] = cj;
-      }
-      double ss = 0.0;
-      for (int i = j + 1 + l; i < p; i += 32) ss += G[i + cj * KM] * G[i + cj * KM];
-      ss = warp_sum(ss);
-      const double alpha = G[j + cj * KM];
-      double tj = 0.0, beta = alpha;
-      if (ss != 0.0) {
-        const double n2 = fma(alpha, alpha, ss);
-        const double rn = fast_rsqrt(n2);
-        beta = -copysign(n2 * rn, alpha);
-        tj = fma(fabs(alpha), rn, 1.0);
-        const double sc = fast_rcp(alpha - beta);
-        for (int i = j + 1 + l; i < p; i += 32) G[i + cj * KM] *= sc;
-      }
-      if (l == 0) {
-        tau[j] = tj;
-        s_beta = beta;
-      }
-    }
-    __syncthreads();
-    const double tj = tau[j];
-    const double *v = G + cm[j] * KM;
-    int pc[NB];
-    int nc = 0;
-#pragma unroll
-    for (int b = 0; b < NB; ++b) {
-      const int c = j + 1 + w + b * (NT / 32);
-      pc[b] = c < q ? cm[c] : 0;
-      nc += c < q;
-    }
-    if (nc > 0) {
-      double acc[NB];
-#pragma unroll
-      for (int b = 0; b < NB; ++b) acc[b] = 0.0;
-      if (tj != 0.0) {
-        for (int i = j + 1 + l; i < p; i += 32) {
-          const double x = v[i];
-#pragma unroll
-          for (int b = 0; b < NB; ++b)
-            if (b < nc) acc[b] += x * G[i + pc[b] * KM];
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-#pragma unroll
-          for (int b = 0; b < NB; ++b) acc[b] += __shfl_xor_sync(0xffffffffu, acc[b], o);
-        }
-        double f[NB];
-#pragma unroll
-        for (int b = 0; b < NB; ++b) f[b] = (b < nc) ? tj * (acc[b] + G[j + pc[b] * KM]) : 0.0;
-        for (int i = j + 1 + l; i < p; i += 32) {
-          const double x = v[i];
-#pragma unroll
-          for (int b = 0; b < NB; ++b)
-            if (b < nc) G[i + pc[b] * KM] -= f[b] * x;
-        }
-        __syncwarp();
-        if (l == 0) {
-#pragma unroll
-          for (int b = 0; b < NB; ++b)
-            if (b < nc) G[j + pc[b] * KM] -= f[b];
-        }
-      }
-      double ss[NB];
-#pragma unroll
-      for (int b = 0; b < NB; ++b) ss[b] = 0.0;
-      for (int i = j + 1 + l; i < p; i += 32) {
-#pragma unroll
-        for (int b = 0; b < NB; ++b)
-          if (b < nc) ss[b] += G[i + pc[b] * KM] * G[i + pc[b] * KM];
-      }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-#pragma unroll
-        for (int b = 0; b < NB; ++b) ss[b] += __shfl_xor_sync(0xffffffffu, ss[b], o);
-      }
-      if (l == 0) {
-#pragma unroll
-        for (int b = 0; b < NB; ++b)
-          if (b < nc) nrm[pc[b]] = ss[b];
-      }
-    }
-    if (tid == 0) G[j + cm[j] * KM] = s_beta;
-    __syncthreads();
-  }
-}
-
-// Same factorization as qrcp (same storage contract: cm, tau, reflector j
-// below row j of column cm[j], R row j in row j), one barrier per step: every
-// warp selects the pivot (largest remaining norm, smallest column on ties)
-// and builds the reflector itself from the raw pivot column, applies it to
-// its own columns (c = w mod NW) and recomputes their norms; the pivot
-// column's owner writes the reflector back after the barrier, when no warp
-// reads that column any more.  p <= 64 (two rows per lane), q <= 64.
+// pivot order), reflector j lives below row j of column cm[j], tau[j], R row
+// j in row j.  One barrier per step: every warp selects the pivot (largest
+// remaining norm, smallest column on ties) and builds the reflector itself
+// from the raw pivot column, applies it to its own columns (c = w mod NW)
+// and recomputes their norms; the pivot column's owner writes the reflector
+// back after the barrier, when no warp reads that column any more.
+// p <= 64 (two rows per lane), q <= 64.
 template <int KM, int NT>
 __device__ void qrcp_fast(double *G, int p, int q, double *tau, int *cm, double *nrm) {
   constexpr int NW = NT / 32;
