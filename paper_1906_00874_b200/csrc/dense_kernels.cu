@@ -388,15 +388,24 @@ __global__ void __launch_bounds__(HLU_NT)
 
 using namespace hlu;
 
+// dynamic shared-memory opt-ins are per device: one bit per device ordinal and kernel
+static bool first_on_device(unsigned long long &mask) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev >= 64) return true;
+  if ((mask >> dev) & 1ull) return false;
+  mask |= 1ull << dev;
+  return true;
+}
+
 static size_t getrf_smem(int n) { return (size_t)n * (n + 1) * sizeof(double); }
 static size_t trsm_smem(int n) { return (size_t)n * (n + 1) * sizeof(double) + (size_t)(n + 1) * TRSM_CHUNK * sizeof(double); }
 
 extern "C" int hlu_getrf_batched_f64(const hlu_ctx *ctx, const hlu_getrf_desc *d, int count, int max_n,
                                      void *stream) {
-  static bool init = false;
-  if (!init) {
+  static unsigned long long init = 0ull;
+  if (first_on_device(init)) {
     cudaFuncSetAttribute(k_getrf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)getrf_smem(128));
-    init = true;
   }
   if (max_n > 128) return -2;
   if (count <= 0) return 0;
@@ -406,10 +415,9 @@ extern "C" int hlu_getrf_batched_f64(const hlu_ctx *ctx, const hlu_getrf_desc *d
 
 extern "C" int hlu_trsm_batched_f64(const hlu_ctx *ctx, const hlu_trsm_desc *d, int count, int max_n,
                                     void *stream) {
-  static bool init = false;
-  if (!init) {
+  static unsigned long long init = 0ull;
+  if (first_on_device(init)) {
     cudaFuncSetAttribute(k_trsm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)trsm_smem(128));
-    init = true;
   }
   if (max_n > 128) return -2;
   if (count <= 0) return 0;
@@ -420,10 +428,9 @@ extern "C" int hlu_trsm_batched_f64(const hlu_ctx *ctx, const hlu_trsm_desc *d, 
 extern "C" int hlu_gemm_batched_f64(const hlu_ctx *ctx, const hlu_gemm_desc *d, const hlu_term *terms,
                                     int count, void *stream) {
   const size_t smem = (size_t)(2 * GLD * GK + GB * GB) * sizeof(double);
-  static bool init = false;
-  if (!init) {
+  static unsigned long long init = 0ull;
+  if (first_on_device(init)) {
     cudaFuncSetAttribute(k_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    init = true;
   }
   if (count <= 0) return 0;
   k_gemm<<<count, HLU_NT, smem, (cudaStream_t)stream>>>(*ctx, d, terms);
@@ -433,10 +440,9 @@ extern "C" int hlu_gemm_batched_f64(const hlu_ctx *ctx, const hlu_gemm_desc *d, 
 extern "C" int hlu_gemm_small_batched_f64(const hlu_ctx *ctx, const hlu_gemm_desc *d, const hlu_term *terms,
                                           int count, void *stream) {
   const size_t smem = (size_t)HLU_NWARP * WSMALL * sizeof(double);
-  static bool init = false;
-  if (!init) {
+  static unsigned long long init = 0ull;
+  if (first_on_device(init)) {
     cudaFuncSetAttribute(k_gemm_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    init = true;
   }
   if (count <= 0) return 0;
   k_gemm_warp<<<(count + HLU_NWARP - 1) / HLU_NWARP, HLU_NT, smem, (cudaStream_t)stream>>>(*ctx, d, terms, count);

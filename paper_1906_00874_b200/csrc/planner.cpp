@@ -8,7 +8,11 @@
 // arrays.  The Python planner takes ~75 s per 5.6M reference tasks (cfg3);
 // this one takes a few seconds.
 #include <algorithm>
+#include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <initializer_list>
 #include <cstdint>
 #include <cstring>
 #include <limits>
@@ -69,6 +73,22 @@ struct Opnd {  // an H-node or a window of a leaf, in global coordinates
 
 struct Iv {
   int64_t lo, hi;
+};
+
+// read-only view of a vector or a braced list (no allocation for the short
+// read / write / temp lists every op passes)
+template <class T>
+struct Span {
+  const T *p = nullptr;
+  size_t n = 0;
+  Span() = default;
+  Span(const std::vector<T> &v) : p(v.data()), n(v.size()) {}
+  Span(std::initializer_list<T> l) : p(l.begin()), n(l.size()) {}
+  const T *begin() const { return p; }
+  const T *end() const { return p + n; }
+  size_t size() const { return n; }
+  bool empty() const { return n == 0; }
+  const T &operator[](size_t i) const { return p[i]; }
 };
 
 struct Term {
@@ -181,8 +201,8 @@ struct Planner {
     *b = View{x.off_b + (o.c0 - x.c0), o.c1 - o.c0, cap, 1, cols, -1, x.slot};
   }
 
-  int64_t emit(int kind, bool defer, int64_t payload, const std::vector<Iv> &reads, const std::vector<Iv> &writes,
-               const std::vector<int64_t> &tin, const std::vector<int64_t> &tout, int ff, double fc, int64_t fl) {
+  int64_t emit(int kind, bool defer, int64_t payload, Span<Iv> reads, Span<Iv> writes, Span<int64_t> tin,
+               Span<int64_t> tout, int ff, double fc, int64_t fl) {
     Op o;
     o.kind = kind;
     o.defer = defer;
@@ -257,9 +277,8 @@ struct Planner {
     }
   }
 
-  int64_t gemm_op(const std::vector<Term> &ts, const std::vector<Iv> &reads, const std::vector<Iv> &writes, int ff,
-                  double fc, int log_slot, bool defer, const std::vector<int64_t> &tout,
-                  const std::vector<int64_t> &tin, bool splittable = true) {
+  int64_t gemm_op(const std::vector<Term> &ts, Span<Iv> reads, Span<Iv> writes, int ff, double fc, int log_slot,
+                  bool defer, Span<int64_t> tout, Span<int64_t> tin, bool splittable = true) {
     int64_t lg = -1;
     if (ff == F_LIN || ff == F_QUAD) lg = log();
     GemmP g{(int64_t)terms.size(), (int64_t)ts.size(), (int)lg, log_slot, splittable};
@@ -269,8 +288,8 @@ struct Planner {
   }
 
   // ---------------------------------------------------------- truncation
-  bool rkt_op(int mode, const std::vector<Pair> &ps, int m, int n, int out_node, const std::vector<Iv> &reads,
-              const std::vector<int64_t> &tin, bool defer, bool has_flop, double flop_mn, Pair *res) {
+  bool rkt_op(int mode, const std::vector<Pair> &ps, int m, int n, int out_node, Span<Iv> reads, Span<int64_t> tin,
+              bool defer, bool has_flop, double flop_mn, Pair *res) {
     int kb = 0;
     for (const auto &p : ps) kb += p.a.cols;
     std::vector<int64_t> tout;
@@ -560,7 +579,7 @@ struct Planner {
   }
 
   // ---------------------------------------------------------- trsm
-  void trsm_op(const View &t, const View &x, int mode, const std::vector<Iv> &reads, const std::vector<Iv> &writes,
+  void trsm_op(const View &t, const View &x, int mode, Span<Iv> reads, Span<Iv> writes,
                double coef, bool dyn) {
     const int64_t lg = dyn ? log() : -1;
     trsm.push_back(TrsmP{t, x, mode, (int)lg});
@@ -1025,7 +1044,10 @@ struct Planner {
   // into independent sub-chains over disjoint row groups (>= split_rows rows
   // each); every sub-chain keeps the original term order on its rows.
   // appends the op's chain(s) to (large, small) staging lists
-  void emit_gemm(const GemmP &g, int64_t ab, std::vector<std::vector<hlu_term>> &chains) {
+  // output: chain c = terms [cb[c], cb[c+1]) of ct (both cleared first)
+  void emit_gemm(const GemmP &g, int64_t ab, std::vector<hlu_term> &ct, std::vector<int64_t> &cb) {
+    ct.clear();
+    cb.assign(1, 0);
     bool ok = split_rows > 0 && g.split && g.tn > 1;
     int64_t base = 0, ld = 0, cols = 0;
     if (ok) {
@@ -1060,13 +1082,12 @@ struct Planner {
       if (cuts.size() <= 2) ok = false;
     }
     if (!ok) {
-      chains.emplace_back();
-      for (int64_t k = g.tb; k < g.tb + g.tn; ++k) push_term(chains.back(), terms[k], ab);
+      for (int64_t k = g.tb; k < g.tb + g.tn; ++k) push_term(ct, terms[k], ab);
+      cb.push_back((int64_t)ct.size());
       return;
     }
     for (size_t q = 0; q + 1 < cuts.size(); ++q) {
       const int64_t g0 = cuts[q], g1 = cuts[q + 1];
-      chains.emplace_back();
       for (int64_t k = g.tb; k < g.tb + g.tn; ++k) {
         const Term &t = terms[k];
         const int64_t r0 = t.c.off - base, r1 = r0 + t.c.rows;
@@ -1075,27 +1096,56 @@ struct Planner {
         Term p = t;
         p.c = t.c.rows_slice((int)(lo - r0), (int)(hi - r0));
         if (t.kind != 0) p.a = t.a.rows_slice((int)(lo - r0), (int)(hi - r0));
-        push_term(chains.back(), p, ab);
+        push_term(ct, p, ab);
       }
+      cb.push_back((int64_t)ct.size());
     }
   }
 
-  struct StagedChain {
-    int log, log_slot;
+  // gemm chains of the pending level, flat: chain i = terms [tb[i], tb[i+1])
+  struct Stage {
     std::vector<hlu_term> terms;
+    std::vector<int64_t> tb{0};
+    std::vector<int> log, log_slot;
+    size_t size() const { return log.size(); }
+    bool empty() const { return log.empty(); }
+    void clear() {
+      terms.clear();
+      tb.assign(1, 0);
+      log.clear();
+      log_slot.clear();
+    }
+    void add(const hlu_term *t, int64_t n, int lg, int ls) {
+      terms.insert(terms.end(), t, t + n);
+      tb.push_back((int64_t)terms.size());
+      log.push_back(lg);
+      log_slot.push_back(ls);
+    }
   };
-  std::vector<StagedChain> stage_large, stage_small;
+  Stage stage_large, stage_small;
+  std::vector<hlu_term> chain_terms;
+  std::vector<int64_t> chain_bounds;
 
+  static double now_s() {
+    return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+  }
   void pack(int64_t arena_base) {
+    const bool timing = std::getenv("HLU_PLAN_TIMING") != nullptr;
+    double t0 = now_s();
     assign_levels();
+    if (timing) std::fprintf(stderr, "plan: levels %.2fs\n", now_s() - t0), t0 = now_s();
     allocate_temps();
+    if (timing) std::fprintf(stderr, "plan: temps %.2fs\n", now_s() - t0), t0 = now_s();
     const size_t n = ops.size();
+    // ops ordered by (level, kind), program order inside: a stable counting sort
     std::vector<int64_t> order(n);
-    for (size_t i = 0; i < n; ++i) order[i] = (int64_t)i;
-    std::stable_sort(order.begin(), order.end(), [&](int64_t a, int64_t b) {
-      if (levels[a] != levels[b]) return levels[a] < levels[b];
-      return ops[a].kind < ops[b].kind;
-    });
+    {
+      const int64_t nlv = n ? (*std::max_element(levels.begin(), levels.end()) + 1) : 0;
+      std::vector<int64_t> start(nlv * 4 + 1, 0);
+      for (size_t i = 0; i < n; ++i) ++start[levels[i] * 4 + ops[i].kind + 1];
+      for (size_t b = 1; b < start.size(); ++b) start[b] += start[b - 1];
+      for (size_t i = 0; i < n; ++i) order[start[levels[i] * 4 + ops[i].kind]++] = (int64_t)i;
+    }
     struct Rec {
       int kind;
       int64_t count, first;
@@ -1112,15 +1162,16 @@ struct Planner {
         auto &st = pass == 0 ? stage_large : stage_small;
         if (st.empty()) continue;
         const int64_t first = (int64_t)o_gemm.size();
-        for (auto &c : st) {
+        const int64_t tbase = (int64_t)o_terms.size();
+        for (size_t c = 0; c < st.size(); ++c) {
           hlu_gemm_desc d;
-          d.term_begin = (int32_t)o_terms.size();
-          d.term_count = (int32_t)c.terms.size();
-          d.log = c.log;
-          d.log_slot = c.log_slot;
-          o_terms.insert(o_terms.end(), c.terms.begin(), c.terms.end());
+          d.term_begin = (int32_t)(tbase + st.tb[c]);
+          d.term_count = (int32_t)(st.tb[c + 1] - st.tb[c]);
+          d.log = st.log[c];
+          d.log_slot = st.log_slot[c];
           o_gemm.push_back(d);
         }
+        o_terms.insert(o_terms.end(), st.terms.begin(), st.terms.end());
         recs.push_back(Rec{pass == 0 ? HLU_K_GEMM : HLU_K_GEMM_SMALL, (int64_t)st.size(), first, 0, pending_lv, false});
         st.clear();
       }
@@ -1158,12 +1209,12 @@ struct Planner {
         dim = t.t.rows;
       } else if (o.kind == 2) {
         const GemmP &g = gemm[o.payload];
-        std::vector<std::vector<hlu_term>> chains;
-        emit_gemm(g, arena_base, chains);
-        for (auto &ch : chains) {
-          const bool sm = small_gemm && small_chain(ch.data(), (int)ch.size());
-          auto &dst = sm ? stage_small : stage_large;
-          dst.push_back({g.log, g.log_slot, std::move(ch)});
+        emit_gemm(g, arena_base, chain_terms, chain_bounds);
+        for (size_t c = 0; c + 1 < chain_bounds.size(); ++c) {
+          const hlu_term *t = chain_terms.data() + chain_bounds[c];
+          const int64_t nt_ = chain_bounds[c + 1] - chain_bounds[c];
+          const bool sm = small_gemm && small_chain(t, (int)nt_);
+          (sm ? stage_small : stage_large).add(t, nt_, g.log, g.log_slot);
         }
         pending_lv = lv;
         continue;
@@ -1227,7 +1278,9 @@ struct Planner {
       }
     }
     nlevels = n ? (*std::max_element(levels.begin(), levels.end()) + 1) : 0;
+    if (timing) std::fprintf(stderr, "plan: pack %.2fs\n", now_s() - t0), t0 = now_s();
     compute_waits();
+    if (timing) std::fprintf(stderr, "plan: waits %.2fs\n", now_s() - t0);
   }
 
   // Every op conflicts (RAW / WAR / WAW on skeleton slots and temps, plus the
@@ -1331,6 +1384,7 @@ extern "C" int hlu_plan_build(hlu_plan **out, const hlu_plan_node *nodes, int64_
   P.nrank = nrk;
   P.split_rows = split_rows;
   try {
+    const double t0 = Planner::now_s();
     for (int64_t i = 0; i < ncmds; ++i) {
       const hlu_plan_cmd &c = cmds[i];
       switch (c.kind) {
@@ -1361,7 +1415,10 @@ extern "C" int hlu_plan_build(hlu_plan **out, const hlu_plan_node *nodes, int64_
         default: throw std::runtime_error("unknown plan command");
       }
     }
+    if (std::getenv("HLU_PLAN_TIMING"))
+      std::fprintf(stderr, "plan: recursion %.2fs (%zu ops)\n", Planner::now_s() - t0, P.ops.size());
     P.pack(arena_base);
+    if (std::getenv("HLU_PLAN_TIMING")) std::fprintf(stderr, "plan: total %.2fs\n", Planner::now_s() - t0);
   } catch (const std::exception &e) {
     p->error = e.what();
     return -1;

@@ -654,18 +654,14 @@ struct StackedR {  // the blocks' R factors stacked: block b at R + b K K (ld K)
 #define RK_CNT_BIGITEMS 2  // row blocks of the CTA-path ops for the large-buffer phase A/C kernels
 #define RK_SEG_BIG 3    // CTA phases (and the ADD shortcuts / empty recompressions)
 #define RK_SEG_C16 4    // CTA-path ops with K <= 16, m, n <= RK_BR: core SVD by one warp
-#define RK_SEG_Q8 5     // max(m,n) <= 128, K <= 8: register warp kernel, 4 rows per lane
-#define RK_SEG_Q16 6    // max(m,n) <= 128, K <= 16: register warp kernel, 4 rows per lane
+// segments 5, 6: unused (the scratch keeps RK_NSEG op-list segments)
 #define RK_NSEG 7
-// largest factor height of the register warp kernels (64: 2 rows per lane only;
-// the 4-rows-per-lane variant breaks rank parity at cfg2, under investigation)
-#define RK_RMAX 64
 #define RK_CNT_ITEMS 7  // row blocks of the CTA-path ops for the small-buffer phase A/C kernels
 
 // One thread per op of the level: the stacked rank from the level-start ranks
 // is logged ((k1, k2) for ADD, (K, 0) for RECOMPRESS; every later phase reads
 // the log, because the op overwrites its destination's rank), and the op is
-// routed: small ops (max(m, n) <= 64, K <= 32) to the warp kernels, the rest
+// routed: small ops (max(m, n) <= 64, K <= 16) to the warp kernels, the rest
 // (and the ADD shortcuts / empty recompressions) to the CTA phases, whose row
 // blocks become work items.
 __global__ void k_rkt_classify(hlu_ctx c, const hlu_rkt_desc *__restrict__ d, const hlu_rkpart *__restrict__ parts,
@@ -694,9 +690,8 @@ __global__ void k_rkt_classify(hlu_ctx c, const hlu_rkt_desc *__restrict__ d, co
     atomicAdd(&c.err[2], 1);
     return;
   }
-  if (max(o.m, o.n) <= RK_RMAX && K <= 16) {
-    const bool r2 = max(o.m, o.n) <= 64;
-    const int w = K <= 8 ? (r2 ? RK_SEG_R8 : RK_SEG_Q8) : (r2 ? RK_SEG_R16 : RK_SEG_Q16);
+  if (max(o.m, o.n) <= 64 && K <= 16) {
+    const int w = K <= 8 ? RK_SEG_R8 : RK_SEG_R16;
     s.list[w * s.max_ops + atomicAdd(&cnt[w], 1)] = op;
     return;
   }
@@ -731,10 +726,10 @@ __global__ void k_rkt_classify(hlu_ctx c, const hlu_rkt_desc *__restrict__ d, co
 
 // ---------------------------------------------------------------- register warp path
 //
-// One warp per small truncation (max(m, n) <= 32 RPL, K <= KB), every loop
+// One warp per small truncation (max(m, n) <= 64, K <= KB), every loop
 // unrolled at compile time so a factor lives in registers: lane l owns rows
-// l + 32 q (q < RPL).  With RPL = 2 the Householder QRs of X and Y run
-// interleaved (two independent chains); with RPL = 4 one after the other.
+// l + 32 q (q < RPL = 2).  The Householder QRs of X and Y run interleaved
+// (two independent chains).
 // Reflectors are parked in warp-private shared memory (ld 32 RPL).  The core
 // SVD (r_core) holds M one column per lane in lanes 0..15 and V in lanes
 // 16..31; Q [W; 0] is applied RK_NB columns at a time.
@@ -759,10 +754,11 @@ __device__ __forceinline__ void r_load(const PartInfo *P, int np, bool left, int
   }
 }
 
-// Householder step J (compile time) on the register-resident factor, as
-// r_qr_step, with the KB-1-J column dots reduced by tr_reduce and broadcast
-// back: ~2.5x fewer shuffles per step (the warp path is shuffle-throughput
-// bound in wide levels).
+// Householder step J (compile time, dlarfg conventions) on the
+// register-resident factor; columns >= K are zero and stay zero.  The KB-1-J
+// column dots are reduced by tr_reduce and broadcast back: ~2.5x fewer
+// shuffles than butterflies (the warp path is shuffle-throughput bound in
+// wide levels).
 template <int RPL, int KB, int J>
 __device__ __forceinline__ void r_qr_step_tr(double (&x)[RPL][KB], double &tau_j, int l) {
   constexpr int j = J;
@@ -828,52 +824,6 @@ struct RQrSteps {
     }
   }
 };
-
-// Householder step j (dlarfg conventions) on the register-resident factor;
-// columns >= K are zero and stay zero
-template <int RPL, int KB>
-__device__ __forceinline__ void r_qr_step(double (&x)[RPL][KB], double &tau_j, int j, int l) {
-  const double x0 = x[0][j];
-  double ss = l > j ? x0 * x0 : 0.0;
-#pragma unroll
-  for (int q = 1; q < RPL; ++q) ss = fma(x[q][j], x[q][j], ss);
-  ss = warp_sum(ss);
-  const double alpha = __shfl_sync(0xffffffffu, x0, j);
-  double tj = 0.0, beta = alpha, sc = 0.0;
-  if (ss != 0.0) {
-    const double n2 = fma(alpha, alpha, ss);
-    const double rn = fast_rsqrt(n2);
-    beta = -copysign(n2 * rn, alpha);
-    tj = fma(fabs(alpha), rn, 1.0);
-    sc = fast_rcp(alpha - beta);
-  }
-  double v[RPL];
-  v[0] = l > j ? x0 * sc : (l == j ? 1.0 : 0.0);
-#pragma unroll
-  for (int q = 1; q < RPL; ++q) v[q] = x[q][j] * sc;
-  x[0][j] = l > j ? v[0] : (l == j ? beta : x0);
-#pragma unroll
-  for (int q = 1; q < RPL; ++q) x[q][j] = v[q];
-  tau_j = tj;
-  double p[KB];
-#pragma unroll
-  for (int c = j + 1; c < KB; ++c) {
-    p[c] = v[0] * x[0][c];
-#pragma unroll
-    for (int q = 1; q < RPL; ++q) p[c] = fma(v[q], x[q][c], p[c]);
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-#pragma unroll
-    for (int c = j + 1; c < KB; ++c) p[c] += __shfl_xor_sync(0xffffffffu, p[c], o);
-  }
-#pragma unroll
-  for (int c = j + 1; c < KB; ++c) {
-    const double f = tj * p[c];
-#pragma unroll
-    for (int q = 0; q < RPL; ++q) x[q][c] -= f * v[q];
-  }
-}
 
 template <int RPL, int KB>
 __device__ __forceinline__ void r_store(const double (&x)[RPL][KB], const double (&ta)[KB], double *S, double *tau,
@@ -1109,7 +1059,8 @@ __device__ void r_trunc(const hlu_ctx &c, const hlu_rkt_desc &o, const hlu_rkpar
 #else
 #define RPROF(k) do {} while (0)
 #endif
-  if (RPL == 2) {  // X and Y interleaved
+  static_assert(RPL == 2, "register warp path: two rows per lane");
+  {  // X and Y interleaved
     double x[RPL][KB], y[RPL][KB], tax[KB], tay[KB];
     r_load<RPL, KB>(P, np, true, m, K, x, l);
     r_load<RPL, KB>(P, np, false, n, K, y, l);
@@ -1121,18 +1072,6 @@ __device__ void r_trunc(const hlu_ctx &c, const hlu_rkt_desc &o, const hlu_rkpar
     RQrSteps<RPL, KB, 0>::run(x, y, tax, tay, K, l);
     r_store<RPL, KB>(x, tax, Sx, tx, l);
     r_store<RPL, KB>(y, tay, Sy, ty, l);
-  } else {
-#pragma unroll 1
-    for (int side = 0; side < 2; ++side) {
-      double x[RPL][KB], ta[KB];
-      r_load<RPL, KB>(P, np, side == 0, side == 0 ? m : n, K, x, l);
-#pragma unroll
-      for (int j = 0; j < KB; ++j) {
-        ta[j] = 0.0;
-        if (j < K) r_qr_step<RPL, KB>(x, ta[j], j, l);
-      }
-      r_store<RPL, KB>(x, ta, side == 0 ? Sx : Sy, side == 0 ? tx : ty, l);
-    }
   }
   __syncwarp();
   RPROF(0);
@@ -1143,7 +1082,7 @@ __device__ void r_trunc(const hlu_ctx &c, const hlu_rkt_desc &o, const hlu_rkpar
   r_apply<RPL, KB>(Sx, tx, Wx, perm, K, kk, m, c.pool + o.out_a, l);
   RPROF(2);
 #ifdef HLU_BPROF
-  if (l == 0 && RPL == 2) {
+  if (l == 0) {
     atomicAdd(&g_rprof[KB == 16][0], 1ull);
     for (int k = 0; k < 3; ++k) atomicAdd(&g_rprof[KB == 16][1 + k], rp_c[k]);
   }
@@ -1161,7 +1100,7 @@ __global__ void __launch_bounds__(RCfg<RPL, KB>::WPC * 32)
             int slot) {
   using Cfg = RCfg<RPL, KB>;
   constexpr int WPC = Cfg::WPC;
-  constexpr int SEG = RPL == 2 ? (KB == 8 ? RK_SEG_R8 : RK_SEG_R16) : (KB == 8 ? RK_SEG_Q8 : RK_SEG_Q16);
+  constexpr int SEG = KB == 8 ? RK_SEG_R8 : RK_SEG_R16;
   extern __shared__ double sm[];
   __shared__ PartInfo P[WPC][RK_MAXP];
   __shared__ int perm[WPC][KB];
@@ -1543,9 +1482,12 @@ static size_t smem_c(bool big) {
   return (size_t)(big ? RK_TBUF + RK_BUFA + RK_KMAX : 2 * RK_BUFS + RK_KMAX) * sizeof(double);
 }
 
+// dynamic shared-memory opt-ins are per device: one bit per device ordinal
 static void rkt_init() {
-  static bool init = false;
-  if (init) return;
+  static unsigned long long done = 0ull;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 64 && ((done >> dev) & 1ull)) return;
   cudaFuncSetAttribute(k_rkt_a<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_a(false));
   cudaFuncSetAttribute(k_rkt_a<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_a(true));
   cudaFuncSetAttribute(k_rkt_b<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RkB<32>::smem());
@@ -1554,10 +1496,8 @@ static void rkt_init() {
   cudaFuncSetAttribute(k_rkt_c<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_c(true));
   cudaFuncSetAttribute(k_rkt_r<2, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RCfg<2, 8>::smem());
   cudaFuncSetAttribute(k_rkt_r<2, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RCfg<2, 16>::smem());
-  cudaFuncSetAttribute(k_rkt_r<4, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RCfg<4, 8>::smem());
-  cudaFuncSetAttribute(k_rkt_r<4, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RCfg<4, 16>::smem());
   cudaFuncSetAttribute(k_rkt_bw<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)BwCfg<16>::smem());
-  init = true;
+  if (dev < 64) done |= 1ull << dev;
 }
 
 // persistent grid of the register warp kernel: as many CTAs as fit on the GPU
@@ -1584,15 +1524,9 @@ static int rkt_launch(int which, const hlu_ctx *ctx, hlu_rkt_desc *d, const hlu_
     case 0:
       k_rkt_classify<<<(count + 127) / 128, 128, 0, st>>>(*ctx, d, parts, first, count, s, slot);
       break;
-    case 1:
-      launch_r<2, 8>(ctx, d, parts, count, s, slot, st);
-      launch_r<4, 8>(ctx, d, parts, count, s, slot, st);
-      break;
-    case 2:
-      launch_r<2, 16>(ctx, d, parts, count, s, slot, st);
-      launch_r<4, 16>(ctx, d, parts, count, s, slot, st);
-      break;
-    case 3: break;  // (slot of a retired kernel)
+    case 1: launch_r<2, 8>(ctx, d, parts, count, s, slot, st); break;
+    case 2: launch_r<2, 16>(ctx, d, parts, count, s, slot, st); break;
+    case 3: break;  // no kernel (kept so the stamp slots stay stable)
     case 4: k_rkt_a<false><<<lim(2 * (int64_t)count, 4), HLU_NT, smem_a(false), st>>>(*ctx, d, parts, s, slot); break;
     case 9: k_rkt_a<true><<<lim(2 * (int64_t)count, 1), HLU_NT, smem_a(true), st>>>(*ctx, d, parts, s, slot); break;
     case 5:

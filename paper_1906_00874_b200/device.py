@@ -110,10 +110,15 @@ class DeviceCall:
         self.nkernels = int(p.launches["count"].astype(bool).sum()) if len(p.launches) else 0
 
     # -- data movement
+    def refill(self, extras=None):
+        """Re-pack the current host payloads of the layout's H-matrices into the
+        pinned staging buffers (same structure; the next ``upload`` sends them)."""
+        fill_pool(self.L, self.host_pool.numpy(), self.host_ranks.numpy(), extras)
+
     def upload(self):
         """Host (pinned) -> device copy of payloads and ranks; resets error words."""
         n = self.L.payload_doubles
-        with self.torch.cuda.stream(self.stream):
+        with self.torch.cuda.device(self.device), self.torch.cuda.stream(self.stream):
             self.pool[:n].copy_(self.host_pool, non_blocking=True)
             self.ranks.copy_(self.host_ranks, non_blocking=True)
             self.err[0] = 0
@@ -173,11 +178,13 @@ class DeviceCall:
         return np.diff(st[: nl + 1].astype(np.int64)) * 1e-9
 
     def launch(self):
-        rc = self.lib.hlu_schedule_launch(self.handle, ctypes.c_void_p(self.stream.cuda_stream))
+        with self.torch.cuda.device(self.device):
+            rc = self.lib.hlu_schedule_launch(self.handle, ctypes.c_void_p(self.stream.cuda_stream))
         _native.check(rc, "hlu_schedule_launch")
 
     def sync(self):
-        self.stream.synchronize()
+        with self.torch.cuda.device(self.device):
+            self.stream.synchronize()
 
     def check_errors(self):
         self.sync()
@@ -214,7 +221,8 @@ class DeviceCall:
 
     def close(self):
         if getattr(self, "handle", None):
-            self.lib.hlu_schedule_destroy(self.handle)
+            with self.torch.cuda.device(self.device):
+                self.lib.hlu_schedule_destroy(self.handle)
             self.handle = None
 
     def __del__(self):

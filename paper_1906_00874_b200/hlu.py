@@ -25,7 +25,7 @@ from .blocks import INADMISSIBLE, PARTITIONED, BlockNode
 from .clustering import Cluster
 from .hmatrix import DENSE, HMatrix, Skeleton, StructureError, build_skeleton
 from .lowrank import TruncationControl
-from .planner import DEFAULT_CAP, Layout, Planner
+from .planner import DEFAULT_CAP, MAX_CAP, Layout, Planner
 
 SEQUENTIAL = "sequential"
 PARALLEL = "parallel"
@@ -58,11 +58,16 @@ class HluPlan:
     device: object = None
     use_graph: bool = True
     last_call: object = None
+    keep_schedule: bool = False
 
 
 def make_plan(h: HMatrix, truncation: TruncationControl | None = None, mode: str = SEQUENTIAL,
               workers: int = 1, wd_er: bool = True, seed: int = 0, capacity: int | None = None,
-              device=None, use_graph: bool = True) -> HluPlan:
+              device=None, use_graph: bool = True, keep_schedule: bool = False) -> HluPlan:
+    """Reference ``make_plan`` (hlu.py:72-90).  ``keep_schedule=True`` keeps the
+    planned device schedule (pools, descriptors, CUDA graph) on the plan, so
+    later ``hlu_factorize(plan)`` calls on the same structure only re-pack the
+    host payloads, upload, replay and download (plan once, factorize many)."""
     if mode not in (SEQUENTIAL, PARALLEL):
         raise ValueError(f"unknown mode {mode!r}")
     return HluPlan(
@@ -70,7 +75,7 @@ def make_plan(h: HMatrix, truncation: TruncationControl | None = None, mode: str
         truncation=truncation if truncation is not None else TruncationControl(),
         mode=mode, workers=workers, wd_er=wd_er, seed=seed,
         capacity=_auto_capacity([h], truncation) if capacity is None else int(capacity),
-        device=device, use_graph=use_graph,
+        device=device, use_graph=use_graph, keep_schedule=keep_schedule,
     )
 
 
@@ -115,7 +120,8 @@ def plan_call(roots, commands, capacity, extras=None, planner="native"):
 
 def _run(roots, commands, ctl, capacity, device=None, use_graph=True, extras=None, keep=False):
     """Plan + run one H-arithmetic call on the GPU, re-planning with a doubled
-    capacity if any Rk result overflows.  Returns the DeviceCall."""
+    capacity (clamped to MAX_CAP) if any Rk result overflows.  Returns the
+    DeviceCall; ``call.capacity`` is the capacity that succeeded."""
     from .device import DeviceCall, RankOverflow
 
     cap = capacity
@@ -127,10 +133,11 @@ def _run(roots, commands, ctl, capacity, device=None, use_graph=True, extras=Non
             call.check_errors()
         except RankOverflow:
             call.close()
-            cap *= 2
-            if cap > 64:
+            if cap >= MAX_CAP:
                 raise
+            cap = min(2 * cap, MAX_CAP)
             continue
+        call.capacity = cap
         call.download()
         if not keep:
             call.close()
@@ -143,7 +150,24 @@ def hlu_factorize(plan: HluPlan):
     h = plan.matrix
     if h.rows != h.cols:
         raise StructureError("H-LU requires a square matrix")
-    call = _run([h], [("factor", h)], plan.truncation, plan.capacity, plan.device, plan.use_graph)
+    call = plan.last_call if plan.keep_schedule else None
+    if call is not None and getattr(call, "handle", None) and call.L.roots[0] is h:
+        from .device import RankOverflow
+
+        call.refill()  # the structure is unchanged: new payloads through the kept schedule
+        call.upload()
+        call.launch()
+        try:
+            call.check_errors()
+            call.download()
+            plan.flops.add(call.flops())
+            return None
+        except RankOverflow:
+            call.close()
+            plan.capacity = min(2 * plan.capacity, MAX_CAP)
+    call = _run([h], [("factor", h)], plan.truncation, plan.capacity, plan.device, plan.use_graph,
+                keep=plan.keep_schedule)
+    plan.capacity = call.capacity  # later calls start from the capacity that fitted
     plan.flops.add(call.flops())
     plan.last_call = call
     return None

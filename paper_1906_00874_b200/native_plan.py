@@ -105,10 +105,21 @@ def flatten_nodes(layout):
 
 
 SPLIT_ROWS = 64
-PLAN_CACHE_ENV = "HLU_PLAN_CACHE"  # directory of cached plans (unset: no cache)
+PLAN_CACHE_ENV = "HLU_PLAN_CACHE"  # directory of cached plans ("" or "0": no cache)
+DEFAULT_CACHE = os.path.join(os.path.expanduser("~"), ".cache", "paper_1906_00874_b200", "plans")
+
+
+def cache_dir_default():
+    """Plan cache directory: $HLU_PLAN_CACHE, else ~/.cache/paper_1906_00874_b200/plans;
+    "" or "0" disables caching."""
+    d = os.environ.get(PLAN_CACHE_ENV)
+    if d is None:
+        return DEFAULT_CACHE
+    return None if d in ("", "0") else d
 _PACKED_ARRAYS = ("getrf", "trsm", "gemm", "terms", "rkt", "parts", "launches", "flop_formula", "flop_coef",
                   "flop_log", "lu_op_ids", "op_levels", "wait_dense", "wait_rkt")
 _PACKED_INTS = ("nlevels", "arena_doubles", "nlog", "nranks")
+PLAN_FORMAT = 2  # bump when the packing (Python side) or the npz layout changes
 
 
 def plan_key(nodes, cmds, scalars):
@@ -119,12 +130,28 @@ def plan_key(nodes, cmds, scalars):
     import hashlib
 
     d = hashlib.sha256()
+    d.update(f"hlu-plan-v{PLAN_FORMAT}".encode())
     d.update(nodes.tobytes())
     d.update(cmds.tobytes())
     d.update(np.asarray(scalars, dtype=np.int64).tobytes())
-    with open(PLAN_LIB, "rb") as f:
-        d.update(hashlib.sha256(f.read()).digest())
+    d.update(_lib_digest())
     return d.hexdigest()
+
+
+_LIB_DIGEST = None
+
+
+def _lib_digest():
+    global _LIB_DIGEST
+    if _LIB_DIGEST is None:
+        import hashlib
+
+        with open(PLAN_LIB, "rb") as f:
+            _LIB_DIGEST = hashlib.sha256(f.read()).digest()
+    return _LIB_DIGEST
+
+
+CACHE_MIN_OPS = 100_000  # the default cache keeps big plans only (planning cfg3 takes ~25 s)
 
 
 def save_packed(path, packed, nops):
@@ -132,14 +159,14 @@ def save_packed(path, packed, nops):
     for f in _PACKED_INTS:
         rec[f] = np.int64(getattr(packed, f))
     rec["nops"] = np.int64(nops)
-    rec["lu_labels"] = np.array(packed.lu_labels, dtype=object)
+    rec["lu_labels"] = np.array(packed.lu_labels, dtype=str)  # no pickled objects in the cache
     tmp = f"{path}.{os.getpid()}.tmp.npz"
     np.savez(tmp, **rec)
     os.replace(tmp, path)  # atomic: concurrent planners never see a partial file
 
 
 def load_packed(path):
-    with np.load(path, allow_pickle=True) as z:
+    with np.load(path, allow_pickle=False) as z:
         kw = {f: (z[f] if f in z.files else None) for f in _PACKED_ARRAYS}
         kw.update({f: int(z[f]) for f in _PACKED_INTS})
         kw["lu_labels"] = [str(x) for x in z["lu_labels"]]
@@ -175,7 +202,8 @@ def plan(layout, commands, split_rows=SPLIT_ROWS, cache_dir=None):
             cmds[i] = (_MATVEC_CMDS[kind], index[id(c[1])], 0, 0, xo, cols, 0, xr, yo, yr)
         else:
             raise ValueError(kind)
-    cache_dir = cache_dir if cache_dir is not None else os.environ.get(PLAN_CACHE_ENV)
+    explicit = cache_dir is not None
+    cache_dir = cache_dir if explicit else cache_dir_default()
     path = None
     if cache_dir:
         key = plan_key(nodes, cmds, (layout.cap, layout.ident_off, layout.nslots, layout.nrk,
@@ -184,7 +212,7 @@ def plan(layout, commands, split_rows=SPLIT_ROWS, cache_dir=None):
         if os.path.exists(path):
             return load_packed(path)
     packed, nops = _build(layout, nodes, cmds, split_rows)
-    if path is not None:
+    if path is not None and (explicit or nops >= CACHE_MIN_OPS):
         os.makedirs(cache_dir, exist_ok=True)
         save_packed(path, packed, nops)
     return packed, nops

@@ -42,6 +42,7 @@ TEMP_SHIFT = 36  # virtual address of temp t: (t + 1) << TEMP_SHIFT (2^27 temps,
 DEFAULT_CAP = 32
 IDENT = 64     # identity block edge kept in the pool
 KMAX_STACK = 64  # largest stacked rank the truncation kernel handles
+MAX_CAP = 64     # largest per-block Rk capacity (= the stacked-rank limit of the kernels)
 
 
 def _label(kind, rows, cols):

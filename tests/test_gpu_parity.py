@@ -130,11 +130,30 @@ def test_recompress_tall(rng):
 # ---- whole factorizations vs the reference fixtures ------------------------------
 
 
+def _check_solve_fixture(name, h, original):
+    """x = U^-1 L^-1 b on the GPU factors against x_ref computed on the REAL
+    reference's own factors (tests/golden/make_golden_solve.py), and the GPU
+    residual probe against the reference's residual_probe (bench.py:142-152)."""
+    s = cases.golden(f"solve_{name}")
+    if s is None:
+        return None
+    from paper_1906_00874_b200 import residual_probe
+
+    x = hlu_solve(h, s["rhs"])
+    rel = np.linalg.norm(x - s["x"]) / np.linalg.norm(s["x"])
+    assert rel <= 1e-8, f"x differs from the reference-factor solve by {rel:.2e}"
+    r = residual_probe(original, h)
+    rr = float(s["residual"])
+    assert abs(r - rr) <= 1e-3 * rr, f"residual {r:.6e} vs reference {rr:.6e}"
+    return rel, r, rr
+
+
 @pytest.mark.parametrize("name", GOLDEN_CASES)
 def test_factorization_parity(name):
     g = cases.golden(name)
     build, ctl = cases.CASES[name]
     h, _ = build()
+    original = h.copy()
     plan = make_plan(h, TruncationControl(*ctl))
     hlu_factorize(plan)
     ranks = cases.ranks(h)
@@ -149,6 +168,7 @@ def test_factorization_parity(name):
     y = forward_solve(h, g["rhs"])
     rel = np.linalg.norm(y - g["y_forward"]) / np.linalg.norm(g["y_forward"])
     assert rel <= 1e-8, rel
+    _check_solve_fixture(name, h, original)
 
 
 @pytest.mark.parametrize("name", ["sphere_1024", "bem1d_1024", "mixed_192"])
@@ -191,6 +211,7 @@ def test_baseline_config_rank_parity(name):
     h, _ = cases.bem(d, n, eta, leaf, eps, kmax, workers=os.cpu_count())
     assert hashlib.sha256(hmatrix.structure_dump(h).encode()).hexdigest() == str(g["structure_sha"])
     assert cases.payload_sha(h) == str(g["payload_sha"])
+    original = h.copy()
     ctl = cases.CASES[name][1]
     plan = make_plan(h, TruncationControl(*ctl))
     hlu_factorize(plan)
@@ -201,6 +222,9 @@ def test_baseline_config_rank_parity(name):
     y = forward_solve(h, g["rhs"])
     rel = np.linalg.norm(y - g["y_forward"]) / np.linalg.norm(g["y_forward"])
     assert rel <= 1e-8, rel
+    out = _check_solve_fixture(name, h, original)
+    if out is not None:
+        print(f"{name}: x rel diff {out[0]:.2e}, residual {out[1]:.6e} (reference {out[2]:.6e})")
 
 
 @pytest.mark.parametrize("name", ["sphere_1024"])
