@@ -21,8 +21,8 @@ clean:
 
 PLAN := paper_1906_00874_b200/libhlu_plan.so
 all: $(PLAN)
-$(PLAN): paper_1906_00874_b200/csrc/planner.cpp paper_1906_00874_b200/csrc/rk_layout.h include/hlu_plan.h include/hlu_b200.h
-	g++ -O3 -std=c++17 -fPIC -shared -Iinclude paper_1906_00874_b200/csrc/planner.cpp -o $@
+$(PLAN): paper_1906_00874_b200/csrc/planner.cpp paper_1906_00874_b200/csrc/hostpack.cpp paper_1906_00874_b200/csrc/rk_layout.h include/hlu_plan.h include/hlu_b200.h
+	g++ -O3 -std=c++17 -fPIC -shared -pthread -Iinclude paper_1906_00874_b200/csrc/planner.cpp paper_1906_00874_b200/csrc/hostpack.cpp -o $@
 
 # diagnostics build (core-kernel phase profiler), loaded with HLU_LIB=libhlu_b200_prof.so
 prof: paper_1906_00874_b200/libhlu_b200_prof.so

@@ -74,6 +74,22 @@ int hlu_plan_copy(const hlu_plan *p, void *getrf, void *trsm, void *gemm, void *
 int hlu_plan_level_waits(const hlu_plan *p, int32_t *wait_dense, int32_t *wait_rkt);
 void hlu_plan_free(hlu_plan *p);
 
+/* --- host payload staging (the upload / download of hlu_factorize) ---
+ * One leaf payload: a row-major host array (numpy C order, rows x cols, row
+ * stride host_stride doubles) <-> a column-major slab of the pool at off with
+ * leading dimension ld.  Replaces the per-leaf numpy copies around the
+ * reference's in-place leaf updates (lowrank.py:50-51 keeps factors C-contiguous). */
+typedef struct {
+  void *host;
+  int64_t off;
+  int32_t rows, cols;
+  int32_t ld, host_stride;
+} hlu_pack_rec; /* 32 bytes */
+
+/* threads <= 0: one per hardware thread */
+int hlu_host_pack(const hlu_pack_rec *recs, int64_t n, double *pool, int threads);
+int hlu_host_unpack(const hlu_pack_rec *recs, int64_t n, const double *pool, int threads);
+
 #ifdef __cplusplus
 }
 #endif

@@ -8,6 +8,7 @@
 //   gemm   <- gemm_update and the H-operand products _op_matmat,
 //             _op_t_matmat, _op_gemm_into, _op_t_gemm_into, _op_rgemm_into
 //             (lowrank.py:250-261, hlu.py:160-255), as ordered chains.
+#include <algorithm>
 #include <climits>
 
 #include "common.cuh"
@@ -15,72 +16,283 @@
 namespace hlu {
 
 // ---------------------------------------------------------------------------
-// GETRF: in-place unpivoted LU in shared memory (n <= 128).
-// Pivot test |p| <= 1e-12 * max|A_input| as lowrank.py:194-212; the first
-// failing op (program order) is reported through ctx.err[1].
+// GEMM chains on the fp64 tensor cores (DMMA, mma.sync.m16n8k8.f64).
+// C += alpha * A B with 64x64 output tiles and 32-deep k-tiles staged in
+// shared memory; 8 warps in a 4 (M) x 2 (N) grid, each warp a 16 x 32 block
+// = 4 m16n8 accumulator fragments (16 fp64 registers per lane).
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(HLU_NT) k_getrf(hlu_ctx c, const hlu_getrf_desc *__restrict__ d) {
-  extern __shared__ double sm[];
-  __shared__ double red[HLU_NWARP];
-  const hlu_getrf_desc o = d[blockIdx.x];
-  const Mat A = resolve(c, o.a);
-  const int n = A.rows;
-  const int ld = n + 1;
-  const int tid = threadIdx.x;
-  double mx = 0.0;
-  for (int e = tid; e < n * n; e += HLU_NT) {
-    const int i = e % n, j = e / n;
-    const double v = A.get(i, j);
-    sm[i + j * ld] = v;
-    mx = fmax(mx, fabs(v));
-  }
-  const double tol = 1e-12 * block_max(mx, red);  // includes a __syncthreads
-  for (int j = 0; j < n; ++j) {
-    const double p = sm[j + j * ld];
-    if (fabs(p) <= tol) {
-      if (tid == 0) {
-        atomicMin(&c.err[1], o.op_id);
-        c.dlog[2 * o.lu_index] = p;
-        c.dlog[2 * o.lu_index + 1] = tol;
+#define GB 64
+#define GK 32
+#define GPF (GB * GK / HLU_NT)  // tile elements each thread stages per operand (8)
+// Shared tile layouts, chosen per operand orientation so that both the
+// coalesced staging stores and the fragment loads are bank-conflict free:
+//   the operand's unit-stride dimension fastest in the tile -> ld 68 (k-major
+//   A / n-major B, "GL64") or ld 36 (m-major A / k-fastest B, "GL32").
+#define GL64 68
+#define GL32 36
+#define GTILE (GB * GL32)  // doubles per staged operand tile (>= GK * GL64)
+
+// A operand of a GEMM term read through its triangle (hlu_term.assoc of a GEMM
+// term): HLU_TRI_NONE = A, HLU_TRI_UPPER = triu(A), HLU_TRI_UNIT_LOWER =
+// tril(A, -1) + I (the stored factors of a dense diagonal leaf, hlu.py:720-767)
+__device__ __forceinline__ double tri_get(const Mat &A, int i, int j, int tri) {
+  if (tri == HLU_TRI_UPPER) return j >= i ? A.get(i, j) : 0.0;
+  if (tri == HLU_TRI_UNIT_LOWER) return j < i ? A.get(i, j) : (j == i ? 1.0 : 0.0);
+  return A.get(i, j);
+}
+
+// D = A(16x8, row) * B(8x8, col) + D, fp64 tensor core.  Fragments (lane =
+// 4 g + t): a = {A[g][t], A[g+8][t], A[g][t+4], A[g+8][t+4]},
+// b = {B[t][g], B[t+4][g]}, d = {D[g][2t], D[g][2t+1], D[g+8][2t], D[g+8][2t+1]}.
+__device__ __forceinline__ void dmma16884(double (&d)[4], const double (&a)[4], const double (&b)[2]) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k8.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};\n"
+      : "+d"(d[0]), "+d"(d[1]), "+d"(d[2]), "+d"(d[3])
+      : "d"(a[0]), "d"(a[1]), "d"(a[2]), "d"(a[3]), "d"(b[0]), "d"(b[1]));
+}
+
+// 8-byte global -> shared copy that bypasses the registers (LDGSTS);
+// ok == false writes a zero (src-size 0: nothing is read)
+__device__ __forceinline__ void cp_async8(double *sdst, const double *gsrc, bool ok) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(sdst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gsrc), "r"(ok ? 8 : 0) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+
+// C += alpha * A B.  Double-buffered k-tiles: the next tile streams into the
+// other shared buffers by cp.async while the tensor cores consume this one.
+// sA / sB hold two GTILE buffers each.
+__device__ __noinline__ void tile_gemm(const Mat &C, const Mat &A, const Mat &B, double alpha, double *sA,
+                                       double *sB, int tri = HLU_TRI_NONE) {
+  const int m = C.rows, n = C.cols, k = A.cols;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int wm = (wid & 3) * 16, wn = (wid >> 2) * 32;
+  // coalescing: walk each operand's unit-stride dimension fastest
+  const bool a_rf = A.rs == 1, b_rf = B.rs == 1;
+  // element (row r, depth q) of the A tile / (depth q, col c) of the B tile
+  const int am = a_rf ? 1 : GL32, ak = a_rf ? GL64 : 1;
+  const int bk = b_rf ? 1 : GL64, bn = b_rf ? GL32 : 1;
+  for (int i0 = 0; i0 < m; i0 += GB) {
+    for (int j0 = 0; j0 < n; j0 += GB) {
+      double acc[4][4];
+#pragma unroll
+      for (int f = 0; f < 4; ++f)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) acc[f][v] = 0.0;
+      auto issue = [&](int k0, int buf) {
+        double *ta = sA + buf * GTILE, *tb = sB + buf * GTILE;
+#pragma unroll 1
+        for (int u = 0; u < GPF; ++u) {
+          const int e = tid + u * HLU_NT;
+          const int r = a_rf ? e % GB : e / GK, q = a_rf ? e / GB : e % GK;
+          const int gi = i0 + r, gk = k0 + q;
+          const bool oka = gi < m && gk < k;
+          cp_async8(ta + r * am + q * ak, oka ? &A.at(gi, gk) : A.p, oka);
+          const int qq = b_rf ? e % GK : e / GB, cc = b_rf ? e / GK : e % GB;
+          const int bj = j0 + cc, bkk = k0 + qq;
+          const bool okb = bkk < k && bj < n;
+          cp_async8(tb + qq * bk + cc * bn, okb ? &B.at(bkk, bj) : B.p, okb);
+        }
+        cp_async_commit();
+      };
+      // triangular read of A (factor matvecs): fix this thread's staged elements
+      auto mask = [&](int k0, int buf) {
+        double *ta = sA + buf * GTILE;
+#pragma unroll
+        for (int u = 0; u < GPF; ++u) {
+          const int e = tid + u * HLU_NT;
+          const int r = a_rf ? e % GB : e / GK, q = a_rf ? e / GB : e % GK;
+          const int gi = i0 + r, gk = k0 + q;
+          if (gi < m && gk < k) {
+            double &x = ta[r * am + q * ak];
+            if (tri == HLU_TRI_UPPER && gk < gi) x = 0.0;
+            if (tri == HLU_TRI_UNIT_LOWER && gk >= gi) x = gk == gi ? 1.0 : 0.0;
+          }
+        }
+      };
+      issue(0, 0);
+      int buf = 0;
+      for (int k0 = 0; k0 < k; k0 += GK, buf ^= 1) {
+        if (k0 + GK < k) {
+          issue(k0 + GK, buf ^ 1);  // the other buffer was released by the barrier below
+          cp_async_wait<1>();
+        } else {
+          cp_async_wait<0>();
+        }
+        if (tri != HLU_TRI_NONE) mask(k0, buf);
+        __syncthreads();
+        const double *ta = sA + buf * GTILE, *tb = sB + buf * GTILE;
+        const int ksteps = (min(GK, k - k0) + 7) >> 3;  // zero-padded past k
+        for (int s = 0; s < ksteps; ++s) {
+          const int q0 = s * 8 + t;
+          double af[4];
+          af[0] = ta[(wm + g) * am + q0 * ak];
+          af[1] = ta[(wm + g + 8) * am + q0 * ak];
+          af[2] = ta[(wm + g) * am + (q0 + 4) * ak];
+          af[3] = ta[(wm + g + 8) * am + (q0 + 4) * ak];
+#pragma unroll
+          for (int f = 0; f < 4; ++f) {
+            const int c = wn + f * 8 + g;
+            double bf[2];
+            bf[0] = tb[q0 * bk + c * bn];
+            bf[1] = tb[(q0 + 4) * bk + c * bn];
+            dmma16884(acc[f], af, bf);
+          }
+        }
+        __syncthreads();
       }
-      break;  // p is read from shared memory by every thread: uniform exit
+#pragma unroll
+      for (int f = 0; f < 4; ++f) {
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          const int gi = i0 + wm + g + 8 * (v >> 1), gj = j0 + wn + f * 8 + 2 * t + (v & 1);
+          if (gi < m && gj < n) C.at(gi, gj) += alpha * acc[f][v];
+        }
+      }
     }
-    const int r = n - j - 1;
-    for (int i = j + 1 + tid; i < n; i += HLU_NT) sm[i + j * ld] /= p;
-    __syncthreads();
-    for (int e = tid; e < r * r; e += HLU_NT) {
-      const int i = j + 1 + e % r, l = j + 1 + e / r;
-      sm[i + l * ld] -= sm[i + j * ld] * sm[j + l * ld];
-    }
-    __syncthreads();
-  }
-  __syncthreads();
-  for (int e = tid; e < n * n; e += HLU_NT) {
-    const int i = e % n, j = e / n;
-    A.at(i, j) = sm[i + j * ld];
   }
 }
 
+__device__ __forceinline__ Mat sub(const Mat &x, int i0, int j0, int rows, int cols) {
+  Mat r = x;
+  r.p = x.p + i0 * x.rs + j0 * x.cs;
+  r.rows = rows;
+  r.cols = cols;
+  return r;
+}
+
+__device__ void zero_mat(const Mat &C) {
+  for (int e = threadIdx.x; e < C.rows * C.cols; e += HLU_NT) C.at(e % C.rows, e / C.rows) = 0.0;
+  __syncthreads();
+}
+
 // ---------------------------------------------------------------------------
-// TRSM (n <= 128): T in shared memory, right-hand sides in chunks of 64.
+// GETRF: in-place unpivoted LU, right-looking with 8-column panels; the
+// trailing updates A22 -= L21 U12 run on the fp64 tensor cores (one
+// m16n8k8 DMMA per 16 x 8 tile and panel).  n <= 128: the whole block in
+// shared memory; n > 128 (HODLR leaves): 64-blocked in place in HBM, the
+// diagonal blocks through the shared-memory kernel, L21 / U12 by the
+// shared-memory triangular solves and A22 by tile_gemm.
+// Pivot test |p| <= 1e-12 * max|A_input| over the whole block, as
+// lowrank.py:194-212; the first failing op (program order) is reported
+// through ctx.err[1].
+// ---------------------------------------------------------------------------
+#define LU_PW 8      // panel width
+#define SMALL_N 128  // largest block held whole in shared memory
+#define BLK 64       // block edge of the n > SMALL_N paths
+
+__host__ __device__ __forceinline__ int lu_npad(int n) { return (n + 15) & ~15; }
+__host__ __device__ __forceinline__ int lu_ld(int n) { return lu_npad(n) + 4; }  // conflict-free DMMA fragments
+// rows of the shared tile: npad + 16, so 16-row tiles starting at any multiple
+// of 8 stay inside the (zero) padding
+__host__ __device__ __forceinline__ size_t lu_smem_doubles(int n) { return (size_t)lu_ld(n) * (lu_npad(n) + 16); }
+
+// LU of the n x n block in shared memory (column-major, ld, zero padding);
+// returns the first column whose pivot fails the test (its value in *piv), or -1
+__device__ int lu_shared(double *sm, int ld, int n, double tol, double *piv) {
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int npad = lu_npad(n);
+  for (int j0 = 0; j0 < n; j0 += LU_PW) {
+    const int j1 = min(j0 + LU_PW, n);
+    // panel: rank-1 steps on columns j0 .. j1-1 (all rows below the diagonal)
+    for (int j = j0; j < j1; ++j) {
+      const double p = sm[j + j * ld];
+      if (fabs(p) <= tol) {
+        if (tid == 0) *piv = p;
+        __syncthreads();
+        return j;  // p is read from shared memory by every thread: uniform exit
+      }
+      for (int i = j + 1 + tid; i < n; i += HLU_NT) sm[i + j * ld] /= p;
+      __syncthreads();
+      const int r = n - j - 1, w = j1 - j - 1;
+      for (int e = tid; e < r * w; e += HLU_NT) {
+        const int i = j + 1 + e % r, l = j + 1 + e / r;
+        sm[i + l * ld] -= sm[i + j * ld] * sm[j + l * ld];
+      }
+      __syncthreads();
+    }
+    if (j1 >= n) break;
+    // U12 = L11^-1 A12: rows j0 .. j1-1 of the trailing columns, one column per thread
+    for (int col = j1 + tid; col < n; col += HLU_NT) {
+      double u[LU_PW];
+#pragma unroll
+      for (int r = 0; r < LU_PW; ++r) u[r] = (j0 + r < j1) ? sm[j0 + r + col * ld] : 0.0;
+#pragma unroll
+      for (int r = 1; r < LU_PW; ++r)
+#pragma unroll
+        for (int q = 0; q < r; ++q) u[r] -= sm[j0 + r + (j0 + q) * ld] * u[q];
+#pragma unroll
+      for (int r = 1; r < LU_PW; ++r)
+        if (j0 + r < j1) sm[j0 + r + col * ld] = u[r];
+    }
+    __syncthreads();
+    // A22 -= L21 U12: 16 x 8 tiles, one DMMA each (padding rows / columns are zero)
+    const int tr = (npad - j1 + 15) >> 4, tc = (npad - j1 + 7) >> 3;
+    for (int tile = wid; tile < tr * tc; tile += HLU_NWARP) {
+      const int r0 = j1 + (tile % tr) * 16, c0 = j1 + (tile / tr) * 8;
+      double a[4], b[2], d[4];
+      a[0] = -sm[r0 + g + (j0 + t) * ld];
+      a[1] = -sm[r0 + g + 8 + (j0 + t) * ld];
+      a[2] = -sm[r0 + g + (j0 + t + 4) * ld];
+      a[3] = -sm[r0 + g + 8 + (j0 + t + 4) * ld];
+      b[0] = sm[j0 + t + (c0 + g) * ld];
+      b[1] = sm[j0 + t + 4 + (c0 + g) * ld];
+      d[0] = sm[r0 + g + (c0 + 2 * t) * ld];
+      d[1] = sm[r0 + g + (c0 + 2 * t + 1) * ld];
+      d[2] = sm[r0 + g + 8 + (c0 + 2 * t) * ld];
+      d[3] = sm[r0 + g + 8 + (c0 + 2 * t + 1) * ld];
+      dmma16884(d, a, b);
+      sm[r0 + g + (c0 + 2 * t) * ld] = d[0];
+      sm[r0 + g + (c0 + 2 * t + 1) * ld] = d[1];
+      sm[r0 + g + 8 + (c0 + 2 * t) * ld] = d[2];
+      sm[r0 + g + 8 + (c0 + 2 * t + 1) * ld] = d[3];
+    }
+    __syncthreads();
+  }
+  return -1;
+}
+
+// global block -> shared (column-major, ld), zero padding up to rows x cols
+__device__ void load_padded(double *sm, int ld, int rows, int cols, const Mat &A) {
+  for (int e = threadIdx.x; e < rows * cols; e += HLU_NT) {
+    const int i = e % rows, j = e / rows;
+    sm[i + j * ld] = (i < A.rows && j < A.cols) ? A.get(i, j) : 0.0;
+  }
+  __syncthreads();
+}
+
+__device__ void store_block(const double *sm, int ld, const Mat &A) {
+  for (int e = threadIdx.x; e < A.rows * A.cols; e += HLU_NT) {
+    const int i = e % A.rows, j = e / A.rows;
+    A.at(i, j) = sm[i + j * ld];
+  }
+  __syncthreads();
+}
+
+// ---------------------------------------------------------------------------
+// TRSM core (n <= SMALL_N): T in shared memory, right-hand sides in chunks of 64.
 //   mode 0: X <- L^-1 X  (unit lower, X n x r)
 //   mode 1: X <- X U^-1  (upper,      X r x n)
 //   mode 2: X <- U^-1 X  (upper,      X n x r)
 // Solve dimension index i, rhs index v; xs[i + v*ld].
 // ---------------------------------------------------------------------------
 #define TRSM_CHUNK 64
-__global__ void __launch_bounds__(HLU_NT) k_trsm(hlu_ctx c, const hlu_trsm_desc *__restrict__ d) {
-  extern __shared__ double sm[];
-  const hlu_trsm_desc o = d[blockIdx.x];
-  const Mat T = resolve(c, o.t);
-  const Mat X = resolve(c, o.x);
+__host__ __device__ __forceinline__ size_t trsm_smem_doubles(int n) {
+  return (size_t)n * (n + 1) + (size_t)(n + 1) * TRSM_CHUNK;
+}
+
+__device__ void trsm_shared(double *sm, const Mat &T, const Mat &X, int mode) {
   const int n = T.rows;
   const int ld = n + 1;
   double *ts = sm;
   double *xs = sm + n * ld;
   const int tid = threadIdx.x;
-  const int nrhs = (o.mode == 1) ? X.rows : X.cols;
-  if (o.log >= 0 && tid == 0) c.log[o.log] = nrhs;
+  const int nrhs = (mode == 1) ? X.rows : X.cols;
   for (int e = tid; e < n * n; e += HLU_NT) {
     const int i = e % n, j = e / n;
     ts[i + j * ld] = T.get(i, j);
@@ -90,11 +302,11 @@ __global__ void __launch_bounds__(HLU_NT) k_trsm(hlu_ctx c, const hlu_trsm_desc 
     __syncthreads();
     for (int e = tid; e < n * nv; e += HLU_NT) {
       int i, v;
-      if (o.mode == 1) { v = e % nv; i = e / nv; } else { i = e % n; v = e / n; }
-      xs[i + v * ld] = (o.mode == 1) ? X.get(v0 + v, i) : X.get(i, v0 + v);
+      if (mode == 1) { v = e % nv; i = e / nv; } else { i = e % n; v = e / n; }
+      xs[i + v * ld] = (mode == 1) ? X.get(v0 + v, i) : X.get(i, v0 + v);
     }
     __syncthreads();
-    if (o.mode == 0) {
+    if (mode == 0) {
       for (int j = 0; j < n - 1; ++j) {
         const int r = n - j - 1;
         for (int e = tid; e < r * nv; e += HLU_NT) {
@@ -103,7 +315,7 @@ __global__ void __launch_bounds__(HLU_NT) k_trsm(hlu_ctx c, const hlu_trsm_desc 
         }
         __syncthreads();
       }
-    } else if (o.mode == 1) {
+    } else if (mode == 1) {
       for (int j = 0; j < n; ++j) {
         const double ujj = ts[j + j * ld];
         const int r = n - j - 1;
@@ -134,120 +346,102 @@ __global__ void __launch_bounds__(HLU_NT) k_trsm(hlu_ctx c, const hlu_trsm_desc 
     __syncthreads();
     for (int e = tid; e < n * nv; e += HLU_NT) {
       int i, v;
-      if (o.mode == 1) { v = e % nv; i = e / nv; } else { i = e % n; v = e / n; }
-      if (o.mode == 1) X.at(v0 + v, i) = xs[i + v * ld];
+      if (mode == 1) { v = e % nv; i = e / nv; } else { i = e % n; v = e / n; }
+      if (mode == 1) X.at(v0 + v, i) = xs[i + v * ld];
       else X.at(i, v0 + v) = xs[i + v * ld];
     }
   }
+  __syncthreads();
 }
 
-// ---------------------------------------------------------------------------
-// GEMM chains.  C += alpha * A B with 64x64 output tiles, k-steps of 16,
-// each thread a 4x4 register tile (rows ty+16q, cols tx+16q).
-// ---------------------------------------------------------------------------
-#define GB 64
-#define GK 32
-#define GPF (GB * GK / HLU_NT)  // tile elements each thread stages per operand (8)
-#define GLD (GB + 1)            // padded tile row: transposed stores stay conflict-free
-
-// C += alpha * A B.  64x64 output tiles, 32-deep k-steps; the next k-tile is
-// prefetched into registers while the current one is consumed from shared
-// memory, so each k-step costs max(load latency, compute) instead of the sum.
-// A operand of a GEMM term read through its triangle (hlu_term.assoc of a GEMM
-// term): HLU_TRI_NONE = A, HLU_TRI_UPPER = triu(A), HLU_TRI_UNIT_LOWER =
-// tril(A, -1) + I (the stored factors of a dense diagonal leaf, hlu.py:720-767)
-__device__ __forceinline__ double tri_get(const Mat &A, int i, int j, int tri) {
-  if (tri == HLU_TRI_UPPER) return j >= i ? A.get(i, j) : 0.0;
-  if (tri == HLU_TRI_UNIT_LOWER) return j < i ? A.get(i, j) : (j == i ? 1.0 : 0.0);
-  return A.get(i, j);
+// n > SMALL_N: 64-blocked substitution in place; off-diagonal block updates by
+// tile_gemm (DMMA), diagonal blocks by trsm_shared.
+__device__ void trsm_blocked(double *sm, const Mat &T, const Mat &X, int mode) {
+  const int n = T.rows;
+  const int nb = (n + BLK - 1) / BLK;
+  double *sA = sm, *sB = sm + 2 * GTILE;
+  for (int s = 0; s < nb; ++s) {
+    const int bi = mode == 2 ? nb - 1 - s : s;
+    const int i0 = bi * BLK, ni = min(BLK, n - i0), i1 = i0 + ni;
+    if (mode == 0) {  // X_i -= L_i,<i X_<i ; X_i <- L_ii^-1 X_i
+      const Mat Xi = sub(X, i0, 0, ni, X.cols);
+      if (i0 > 0) tile_gemm(Xi, sub(T, i0, 0, ni, i0), sub(X, 0, 0, i0, X.cols), -1.0, sA, sB);
+      __syncthreads();
+      trsm_shared(sm, sub(T, i0, i0, ni, ni), Xi, 0);
+    } else if (mode == 2) {  // X_i -= U_i,>i X_>i ; X_i <- U_ii^-1 X_i
+      const Mat Xi = sub(X, i0, 0, ni, X.cols);
+      if (i1 < n) tile_gemm(Xi, sub(T, i0, i1, ni, n - i1), sub(X, i1, 0, n - i1, X.cols), -1.0, sA, sB);
+      __syncthreads();
+      trsm_shared(sm, sub(T, i0, i0, ni, ni), Xi, 2);
+    } else {  // X_:,j -= X_:,<j U_<j,j ; X_:,j <- X_:,j U_jj^-1
+      const Mat Xj = sub(X, 0, i0, X.rows, ni);
+      if (i0 > 0) tile_gemm(Xj, sub(X, 0, 0, X.rows, i0), sub(T, 0, i0, i0, ni), -1.0, sA, sB);
+      __syncthreads();
+      trsm_shared(sm, sub(T, i0, i0, ni, ni), Xj, 1);
+    }
+    __syncthreads();
+  }
 }
 
-__device__ __noinline__ void tile_gemm(const Mat &C, const Mat &A, const Mat &B, double alpha, double *sA,
-                                       double *sB, int tri = HLU_TRI_NONE) {
-  const int m = C.rows, n = C.cols, k = A.cols;
-  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
-  for (int i0 = 0; i0 < m; i0 += GB) {
-    for (int j0 = 0; j0 < n; j0 += GB) {
-      double acc[4][4];
-#pragma unroll
-      for (int a = 0; a < 4; ++a)
-#pragma unroll
-        for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
-      double pa[GPF], pb[GPF];
-      // coalescing: walk the operand's unit-stride dimension fastest
-      const bool a_rows_fast = A.rs == 1, b_rows_fast = B.rs == 1;
-      auto fetch = [&](int k0) {
-#pragma unroll
-        for (int u = 0; u < GPF; ++u) {
-          const int e = tid + u * HLU_NT;
-          const int r = a_rows_fast ? e % GB : e / GK, q = a_rows_fast ? e / GB : e % GK;
-          const int gi = i0 + r, gk = k0 + q;
-          pa[u] = (gi < m && gk < k) ? tri_get(A, gi, gk, tri) : 0.0;
-          const int qq = b_rows_fast ? e % GK : e / GB, cc = b_rows_fast ? e / GK : e % GB;
-          const int bj = j0 + cc, bk = k0 + qq;
-          pb[u] = (bk < k && bj < n) ? B.get(bk, bj) : 0.0;
-        }
-      };
-      fetch(0);
-      for (int k0 = 0; k0 < k; k0 += GK) {
+__global__ void __launch_bounds__(HLU_NT) k_getrf(hlu_ctx c, const hlu_getrf_desc *__restrict__ d) {
+  extern __shared__ double sm[];
+  __shared__ double red[HLU_NWARP];
+  __shared__ double s_piv;
+  const hlu_getrf_desc o = d[blockIdx.x];
+  const Mat A = resolve(c, o.a);
+  const int n = A.rows;
+  double mx = 0.0;
+  for (int e = threadIdx.x; e < n * n; e += HLU_NT) mx = fmax(mx, fabs(A.get(e % n, e / n)));
+  const double tol = 1e-12 * block_max(mx, red);  // includes a __syncthreads
+  int bad = -1;
+  if (n <= SMALL_N) {
+    const int ld = lu_ld(n), npad = lu_npad(n);
+    load_padded(sm, ld, npad + 16, npad, A);
+    bad = lu_shared(sm, ld, n, tol, &s_piv);
+    if (bad < 0) store_block(sm, ld, A);
+  } else {
+    // 64-blocked right-looking LU in place: A11 = L11 U11 (shared memory),
+    // A21 <- A21 U11^-1, A12 <- L11^-1 A12, A22 -= A21 A12 (DMMA)
+    for (int k0 = 0; k0 < n; k0 += BLK) {
+      const int nk = min(BLK, n - k0), k1 = k0 + nk;
+      const Mat A11 = sub(A, k0, k0, nk, nk);
+      const int ld = lu_ld(nk), npad = lu_npad(nk);
+      load_padded(sm, ld, npad + 16, npad, A11);
+      bad = lu_shared(sm, ld, nk, tol, &s_piv);
+      if (bad >= 0) break;
+      store_block(sm, ld, A11);
+      if (k1 < n) {
+        trsm_shared(sm, A11, sub(A, k1, k0, n - k1, nk), 1);
+        trsm_shared(sm, A11, sub(A, k0, k1, nk, n - k1), 0);
+        tile_gemm(sub(A, k1, k1, n - k1, n - k1), sub(A, k1, k0, n - k1, nk), sub(A, k0, k1, nk, n - k1), -1.0,
+                  sm, sm + 2 * GTILE);
         __syncthreads();
-#pragma unroll
-        for (int u = 0; u < GPF; ++u) {
-          const int e = tid + u * HLU_NT;
-          const int r = a_rows_fast ? e % GB : e / GK, q = a_rows_fast ? e / GB : e % GK;
-          sA[q * GLD + r] = pa[u];
-          const int qq = b_rows_fast ? e % GK : e / GB, cc = b_rows_fast ? e / GK : e % GB;
-          sB[qq * GLD + cc] = pb[u];
-        }
-        __syncthreads();
-        if (k0 + GK < k) fetch(k0 + GK);  // in flight during the FMAs below
-        const int kk = min(GK, k - k0);
-        for (int q = 0; q < kk; ++q) {
-          double av[4], bv[4];
-#pragma unroll
-          for (int a = 0; a < 4; ++a) av[a] = sA[q * GLD + ty + 16 * a];
-#pragma unroll
-          for (int b = 0; b < 4; ++b) bv[b] = sB[q * GLD + tx + 16 * b];
-#pragma unroll
-          for (int a = 0; a < 4; ++a)
-#pragma unroll
-            for (int b = 0; b < 4; ++b) acc[a][b] = fma(av[a], bv[b], acc[a][b]);
-        }
-      }
-#pragma unroll
-      for (int a = 0; a < 4; ++a) {
-        const int gi = i0 + ty + 16 * a;
-        if (gi >= m) continue;
-#pragma unroll
-        for (int b = 0; b < 4; ++b) {
-          const int gj = j0 + tx + 16 * b;
-          if (gj < n) C.at(gi, gj) += alpha * acc[a][b];
-        }
       }
     }
   }
-  __syncthreads();
+  if (bad >= 0 && threadIdx.x == 0) {
+    atomicMin(&c.err[1], o.op_id);
+    c.dlog[2 * o.lu_index] = s_piv;
+    c.dlog[2 * o.lu_index + 1] = tol;
+  }
 }
 
-__device__ __forceinline__ Mat sub(const Mat &x, int i0, int j0, int rows, int cols) {
-  Mat r = x;
-  r.p = x.p + i0 * x.rs + j0 * x.cs;
-  r.rows = rows;
-  r.cols = cols;
-  return r;
-}
-
-__device__ void zero_mat(const Mat &C) {
-  for (int e = threadIdx.x; e < C.rows * C.cols; e += HLU_NT) C.at(e % C.rows, e / C.rows) = 0.0;
-  __syncthreads();
+__global__ void __launch_bounds__(HLU_NT) k_trsm(hlu_ctx c, const hlu_trsm_desc *__restrict__ d) {
+  extern __shared__ double sm[];
+  const hlu_trsm_desc o = d[blockIdx.x];
+  const Mat T = resolve(c, o.t);
+  const Mat X = resolve(c, o.x);
+  if (o.log >= 0 && threadIdx.x == 0) c.log[o.log] = (o.mode == 1) ? X.rows : X.cols;
+  if (T.rows <= SMALL_N) trsm_shared(sm, T, X, o.mode);
+  else trsm_blocked(sm, T, X, o.mode);
 }
 
 __global__ void __launch_bounds__(HLU_NT, 2)
     k_gemm(hlu_ctx c, const hlu_gemm_desc *__restrict__ d, const hlu_term *__restrict__ terms) {
   extern __shared__ double gsm[];
-  double *sA = gsm;
-  double *sB = sA + GLD * GK;
-  double *sW = sB + GLD * GK;
+  double *sA = gsm;             // two k-tile buffers
+  double *sB = sA + 2 * GTILE;  // two k-tile buffers
+  double *sW = sB + 2 * GTILE;
   const hlu_gemm_desc o = d[blockIdx.x];
   if (o.log >= 0 && threadIdx.x == 0) c.log[o.log] = c.ranks[o.log_slot];
   for (int t = 0; t < o.term_count; ++t) {
@@ -398,16 +592,26 @@ static bool first_on_device(unsigned long long &mask) {
   return true;
 }
 
-static size_t getrf_smem(int n) { return (size_t)n * (n + 1) * sizeof(double); }
-static size_t trsm_smem(int n) { return (size_t)n * (n + 1) * sizeof(double) + (size_t)(n + 1) * TRSM_CHUNK * sizeof(double); }
+// dynamic shared memory (bytes) of the LU / TRSM kernels for blocks up to n
+static size_t getrf_smem(int n) {
+  if (n <= SMALL_N) return lu_smem_doubles(n) * sizeof(double);
+  const size_t d = std::max(std::max(lu_smem_doubles(BLK), trsm_smem_doubles(BLK)), (size_t)4 * GTILE);
+  return d * sizeof(double);
+}
+static size_t trsm_smem(int n) {
+  if (n <= SMALL_N) return trsm_smem_doubles(n) * sizeof(double);
+  return std::max(trsm_smem_doubles(BLK), (size_t)4 * GTILE) * sizeof(double);
+}
+#define DENSE_NMAX 256  // largest dense leaf of the LU / TRSM kernels
 
 extern "C" int hlu_getrf_batched_f64(const hlu_ctx *ctx, const hlu_getrf_desc *d, int count, int max_n,
                                      void *stream) {
   static unsigned long long init = 0ull;
   if (first_on_device(init)) {
-    cudaFuncSetAttribute(k_getrf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)getrf_smem(128));
+    cudaFuncSetAttribute(k_getrf, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)std::max(getrf_smem(SMALL_N), getrf_smem(DENSE_NMAX)));
   }
-  if (max_n > 128) return -2;
+  if (max_n > DENSE_NMAX) return -2;
   if (count <= 0) return 0;
   k_getrf<<<count, HLU_NT, getrf_smem(max_n), (cudaStream_t)stream>>>(*ctx, d);
   return cudaGetLastError() == cudaSuccess ? 0 : -1;
@@ -417,9 +621,10 @@ extern "C" int hlu_trsm_batched_f64(const hlu_ctx *ctx, const hlu_trsm_desc *d, 
                                     void *stream) {
   static unsigned long long init = 0ull;
   if (first_on_device(init)) {
-    cudaFuncSetAttribute(k_trsm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)trsm_smem(128));
+    cudaFuncSetAttribute(k_trsm, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)std::max(trsm_smem(SMALL_N), trsm_smem(DENSE_NMAX)));
   }
-  if (max_n > 128) return -2;
+  if (max_n > DENSE_NMAX) return -2;
   if (count <= 0) return 0;
   k_trsm<<<count, HLU_NT, trsm_smem(max_n), (cudaStream_t)stream>>>(*ctx, d);
   return cudaGetLastError() == cudaSuccess ? 0 : -1;
@@ -427,7 +632,7 @@ extern "C" int hlu_trsm_batched_f64(const hlu_ctx *ctx, const hlu_trsm_desc *d, 
 
 extern "C" int hlu_gemm_batched_f64(const hlu_ctx *ctx, const hlu_gemm_desc *d, const hlu_term *terms,
                                     int count, void *stream) {
-  const size_t smem = (size_t)(2 * GLD * GK + GB * GB) * sizeof(double);
+  const size_t smem = (size_t)(4 * GTILE + GB * GB) * sizeof(double);
   static unsigned long long init = 0ull;
   if (first_on_device(init)) {
     cudaFuncSetAttribute(k_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -77,6 +77,7 @@ struct Iv {
 
 // read-only view of a vector or a braced list (no allocation for the short
 // read / write / temp lists every op passes)
+#pragma GCC diagnostic ignored "-Winit-list-lifetime"  // Spans only ever bind call arguments
 template <class T>
 struct Span {
   const T *p = nullptr;

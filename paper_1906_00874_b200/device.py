@@ -60,17 +60,16 @@ class DeviceCall:
         self.packed: Packed = packed
         p = self.packed
         self.total = layout.payload_doubles + p.arena_doubles
-        host_pool = np.zeros(layout.payload_doubles, dtype=np.float64)
-        host_ranks = np.zeros(p.nranks, dtype=np.int32)
-        fill_pool(layout, host_pool, host_ranks, extras)
-        self.h2d_bytes = host_pool.nbytes + host_ranks.nbytes
+        self.h2d_bytes = layout.payload_doubles * 8 + p.nranks * 4
         with torch.cuda.device(self.device):
             # a dedicated stream: the legacy default stream cannot be graph-captured
             self.stream = torch.cuda.Stream(self.device)
         with torch.cuda.device(self.device), torch.cuda.stream(self.stream):
             self.pool = torch.empty(self.total, dtype=torch.float64, device=self.device)
-            self.host_pool = torch.from_numpy(host_pool).pin_memory()
-            self.host_ranks = torch.from_numpy(host_ranks).pin_memory()
+            # pinned staging buffers (payloads packed natively, hlu_host_pack)
+            self.host_pool = torch.zeros(layout.payload_doubles, dtype=torch.float64, pin_memory=True)
+            self.host_ranks = torch.zeros(p.nranks, dtype=torch.int32, pin_memory=True)
+            fill_pool(layout, self.host_pool.numpy(), self.host_ranks.numpy(), extras)
             self.ranks = torch.empty(p.nranks, dtype=torch.int32, device=self.device)
             self.log = torch.zeros(p.nlog, dtype=torch.int32, device=self.device)
             self.err = torch.tensor([0, INT32_MAX, 0, 0], dtype=torch.int32, device=self.device)
@@ -203,11 +202,15 @@ class DeviceCall:
             raise RankOverflow(f"{int(err[0])} Rk results exceeded capacity {self.L.cap}")
 
     def download(self):
-        """Device -> host: install results into the H-matrix; returns d2h bytes."""
+        """Device -> host (into the pinned staging buffers): install results
+        into the H-matrix; returns d2h bytes."""
         n = self.L.payload_doubles
+        with self.torch.cuda.device(self.device), self.torch.cuda.stream(self.stream):
+            self.host_pool.copy_(self.pool[:n], non_blocking=True)
+            self.host_ranks.copy_(self.ranks, non_blocking=True)
         self.sync()
-        pool = self.pool[:n].cpu().numpy()
-        ranks = self.ranks.cpu().numpy()
+        pool = self.host_pool.numpy()
+        ranks = self.host_ranks.numpy()
         read_pool(self.L, pool, ranks)
         self._last_pool = pool
         return pool.nbytes + ranks.nbytes

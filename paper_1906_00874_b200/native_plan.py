@@ -53,6 +53,8 @@ def lib():
         L.hlu_plan_free.argtypes = [vp]
         L.hlu_plan_level_waits.argtypes = [vp, vp, vp]
         L.hlu_plan_level_waits.restype = ctypes.c_int
+        L.hlu_host_pack.argtypes = [vp, i64, vp, ctypes.c_int]
+        L.hlu_host_unpack.argtypes = [vp, i64, vp, ctypes.c_int]
         _lib = L
     return _lib
 

@@ -19,8 +19,84 @@ def max_rank(layout):
     return max((lf.data.k for lf in layout.leaves if lf.kind != DENSE), default=0)
 
 
+PACK_REC = np.dtype([("host", "<u8"), ("off", "<i8"), ("rows", "<i4"), ("cols", "<i4"), ("ld", "<i4"),
+                     ("host_stride", "<i4")])
+assert PACK_REC.itemsize == 32
+
+
+def _addr(a):
+    return a.__array_interface__["data"][0]
+
+
+def _c_order(a):
+    return a if a.flags.c_contiguous and a.dtype == np.float64 else np.ascontiguousarray(a, dtype=np.float64)
+
+
+def _native():
+    from . import native_plan
+
+    return native_plan.lib()
+
+
+def _records(host, off, rows, cols):
+    """Pack records (row-major host arrays -> column-major slabs, ld = rows)."""
+    recs = np.empty(len(host), dtype=PACK_REC)
+    recs["host"] = host
+    recs["off"] = off
+    recs["rows"] = rows
+    recs["cols"] = cols
+    recs["ld"] = rows
+    recs["host_stride"] = cols
+    return recs
+
+
 def fill_pool(layout, pool, ranks, extras=None):
-    """Write every leaf payload into ``pool`` (float64) and ranks (int32)."""
+    """Write every leaf payload into ``pool`` (float64, column-major slabs) and
+    the ranks (int32): one threaded native transpose-copy pass
+    (``hlu_host_pack``, include/hlu_plan.h)."""
+    cap = layout.cap
+    host, off, rows, cols, keep = [], [], [], [], []
+    slots, ks = [], []
+    dense_off, rk = layout.dense_off, layout.rk
+    for lf in layout.leaves:
+        if lf.kind == DENSE:
+            d = _c_order(lf.data)
+            keep.append(d)
+            host.append(_addr(d))
+            off.append(dense_off[id(lf)])
+            rows.append(lf.rows)
+            cols.append(lf.cols)
+        else:
+            a_off, b_off, slot = rk[id(lf)]
+            k = lf.data.k
+            if k > cap:
+                raise ValueError(f"rank {k} exceeds the Rk capacity {cap}")
+            slots.append(slot)
+            ks.append(k)
+            if k == 0:
+                continue
+            a, b = _c_order(lf.data.a), _c_order(lf.data.b)
+            keep.extend((a, b))
+            host.extend((_addr(a), _addr(b)))
+            off.extend((a_off, b_off))
+            rows.extend((lf.rows, lf.cols))
+            cols.extend((k, k))
+    if slots:
+        ranks[np.asarray(slots)] = np.asarray(ks, dtype=np.int32)
+    recs = _records(host, off, rows, cols)
+    assert pool.dtype == np.float64 and pool.flags.c_contiguous
+    _native().hlu_host_pack(recs.ctypes.data, len(recs), pool.ctypes.data, 0)
+    del keep
+    from .planner import IDENT
+
+    pool[layout.ident_off : layout.ident_off + IDENT * IDENT] = np.eye(IDENT).ravel()
+    for name, arr in (extras or {}).items():
+        off, rows, cols, _ = layout.extra[name]
+        pool[off : off + rows * cols] = np.asarray(arr, dtype=float).reshape(rows, cols).ravel(order="F")
+
+
+def fill_pool_numpy(layout, pool, ranks, extras=None):
+    """Reference implementation of fill_pool (per-leaf numpy copies; tests)."""
     cap = layout.cap
     for lf in layout.leaves:
         if lf.kind == DENSE:
@@ -44,7 +120,40 @@ def fill_pool(layout, pool, ranks, extras=None):
 
 
 def read_pool(layout, pool, ranks):
-    """Install the pool contents back into the layout's H-matrix."""
+    """Install the pool contents back into the layout's H-matrix: dense
+    payloads in place, fresh LowRank factors for Rk leaves (one threaded native
+    transpose-copy pass, ``hlu_host_unpack``)."""
+    host, off, rows, cols = [], [], [], []
+    dense_off, rk = layout.dense_off, layout.rk
+    ranks = np.asarray(ranks).tolist()
+    empty = np.empty
+    for lf in layout.leaves:
+        if lf.kind == DENSE:
+            d = lf.data
+            if not (d.flags.c_contiguous and d.dtype == np.float64 and d.flags.writeable):
+                lf.data = d = np.array(d, dtype=np.float64, order="C")
+            host.append(_addr(d))
+            off.append(dense_off[id(lf)])
+            rows.append(lf.rows)
+            cols.append(lf.cols)
+        else:
+            a_off, b_off, slot = rk[id(lf)]
+            k = ranks[slot]
+            a = empty((lf.rows, k))
+            b = empty((lf.cols, k))
+            lf.data = LowRank(a, b)
+            if k:
+                host.extend((_addr(a), _addr(b)))
+                off.extend((a_off, b_off))
+                rows.extend((lf.rows, lf.cols))
+                cols.extend((k, k))
+    recs = _records(host, off, rows, cols)
+    pool = np.ascontiguousarray(pool, dtype=np.float64)
+    _native().hlu_host_unpack(recs.ctypes.data, len(recs), pool.ctypes.data, 0)
+
+
+def read_pool_numpy(layout, pool, ranks):
+    """Reference implementation of read_pool (per-leaf numpy copies; tests)."""
     for lf in layout.leaves:
         if lf.kind == DENSE:
             off = layout.dense_off[id(lf)]

@@ -39,8 +39,10 @@ def test_lu_known_answers():
     assert err.value.block_path == "diag"
 
 
-@pytest.mark.parametrize("n", [15, 32, 48, 64, 96, 128])
+@pytest.mark.parametrize("n", [15, 17, 32, 33, 48, 64, 96, 128, 129, 200, 256])
 def test_lu_vs_oracle(rng, n):
+    """DMMA-panel LU (n <= 128 in shared memory) and the 64-blocked in-place LU
+    (128 < n <= 256, the HODLR leaves) against the oracle's lu_nopivot."""
     a = rng.standard_normal((n, n)) + n * np.eye(n)
     want = orc.lu_nopivot(a.copy())
     got = device_ops.lu_nopivot(a.copy())
@@ -48,7 +50,7 @@ def test_lu_vs_oracle(rng, n):
 
 
 def test_trsm_vs_oracle(rng):
-    for n, r in [(16, 7), (64, 64), (64, 130), (33, 1)]:
+    for n, r in [(16, 7), (64, 64), (64, 130), (33, 1), (128, 32), (129, 5), (200, 70), (256, 256)]:
         l = np.tril(rng.standard_normal((n, n)), -1) + np.eye(n)
         b = rng.standard_normal((n, r))
         want = orc.trsm_lower_unit(l, b.copy())
@@ -65,7 +67,8 @@ def test_trsm_vs_oracle(rng):
 
 
 def test_gemm_update_vs_oracle(rng):
-    for m, n, k in [(6, 5, 4), (64, 64, 64), (130, 70, 33), (1, 200, 3)]:
+    for m, n, k in [(6, 5, 4), (64, 64, 64), (130, 70, 33), (1, 200, 3), (64, 64, 16), (17, 9, 100),
+                    (256, 256, 256)]:
         c, a, b = rng.standard_normal((m, n)), rng.standard_normal((m, k)), rng.standard_normal((k, n))
         want = c - a @ b
         got = device_ops.gemm_update(c.copy(), a, b)
