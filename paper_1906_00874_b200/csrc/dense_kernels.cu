@@ -186,10 +186,14 @@ __device__ void zero_mat(const Mat &C) {
 #define BLK 64       // block edge of the n > SMALL_N paths
 
 __host__ __device__ __forceinline__ int lu_npad(int n) { return (n + 15) & ~15; }
-__host__ __device__ __forceinline__ int lu_ld(int n) { return lu_npad(n) + 4; }  // conflict-free DMMA fragments
-// rows of the shared tile: npad + 16, so 16-row tiles starting at any multiple
-// of 8 stay inside the (zero) padding
-__host__ __device__ __forceinline__ size_t lu_smem_doubles(int n) { return (size_t)lu_ld(n) * (lu_npad(n) + 16); }
+// The DMMA tiles of a panel step start at row / column j1 (a multiple of 8)
+// and run in 16-row x 8-column steps, so they reach up to row npad + 15 and
+// column npad + 7: the shared tile is (npad + 16) rows (ld npad + 20, which
+// keeps the fragment loads bank-conflict free) by npad + 8 columns, zero
+// outside the block.
+__host__ __device__ __forceinline__ int lu_ld(int n) { return lu_npad(n) + 20; }
+__host__ __device__ __forceinline__ int lu_cols(int n) { return lu_npad(n) + 8; }
+__host__ __device__ __forceinline__ size_t lu_smem_doubles(int n) { return (size_t)lu_ld(n) * lu_cols(n); }
 
 // LU of the n x n block in shared memory (column-major, ld, zero padding);
 // returns the first column whose pivot fails the test (its value in *piv), or -1
@@ -395,8 +399,8 @@ __global__ void __launch_bounds__(HLU_NT) k_getrf(hlu_ctx c, const hlu_getrf_des
   const double tol = 1e-12 * block_max(mx, red);  // includes a __syncthreads
   int bad = -1;
   if (n <= SMALL_N) {
-    const int ld = lu_ld(n), npad = lu_npad(n);
-    load_padded(sm, ld, npad + 16, npad, A);
+    const int ld = lu_ld(n);
+    load_padded(sm, ld, ld, lu_cols(n), A);
     bad = lu_shared(sm, ld, n, tol, &s_piv);
     if (bad < 0) store_block(sm, ld, A);
   } else {
@@ -405,8 +409,8 @@ __global__ void __launch_bounds__(HLU_NT) k_getrf(hlu_ctx c, const hlu_getrf_des
     for (int k0 = 0; k0 < n; k0 += BLK) {
       const int nk = min(BLK, n - k0), k1 = k0 + nk;
       const Mat A11 = sub(A, k0, k0, nk, nk);
-      const int ld = lu_ld(nk), npad = lu_npad(nk);
-      load_padded(sm, ld, npad + 16, npad, A11);
+      const int ld = lu_ld(nk);
+      load_padded(sm, ld, ld, lu_cols(nk), A11);
       bad = lu_shared(sm, ld, nk, tol, &s_piv);
       if (bad >= 0) break;
       store_block(sm, ld, A11);

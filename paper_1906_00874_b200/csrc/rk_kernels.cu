@@ -654,7 +654,7 @@ struct StackedR {  // the blocks' R factors stacked: block b at R + b K K (ld K)
 #define RK_CNT_BIGITEMS 2  // row blocks of the CTA-path ops for the large-buffer phase A/C kernels
 #define RK_SEG_BIG 3    // CTA phases (and the ADD shortcuts / empty recompressions)
 #define RK_SEG_C16 4    // CTA-path ops with K <= 16, m, n <= RK_BR: core SVD by one warp
-// segments 5, 6: unused (the scratch keeps RK_NSEG op-list segments)
+#define RK_SEG_D0 5    // eps == 0 dense-fallback ops (k_rkt_d0); segment 6: unused
 #define RK_NSEG 7
 #define RK_CNT_ITEMS 7  // row blocks of the CTA-path ops for the small-buffer phase A/C kernels
 
@@ -688,6 +688,14 @@ __global__ void k_rkt_classify(hlu_ctx c, const hlu_rkt_desc *__restrict__ d, co
   }
   if (K > RK_KMAX || o.part_count > RK_MAXP) {
     atomicAdd(&c.err[2], 1);
+    return;
+  }
+  if (add && c.eps == 0.0 && 2.0 * K >= (double)min(o.m, o.n)) {  // lowrank.py:164: k1 + k2 >= min(m, n) / 2
+    if (max(o.m, o.n) > 64) {
+      atomicAdd(&c.err[2], 1);
+      return;
+    }
+    s.list[RK_SEG_D0 * s.max_ops + atomicAdd(&cnt[RK_SEG_D0], 1)] = op;
     return;
   }
   if (max(o.m, o.n) <= 64 && K <= 16) {
@@ -1434,6 +1442,119 @@ __global__ void __launch_bounds__(BwCfg<KB>::WPC * 32)
   }
 }
 
+// ---------------------------------------------------------------- eps == 0 dense fallback
+//
+// add_truncated's dense route (lowrank.py:164-165 -> compress_dense,
+// lowrank.py:171-175) when eps == 0: the reference keeps every singular value
+// of the DENSE sum x1 + x2 that is not exactly zero, and the trailing ones of a
+// rank-K dense matrix are rounding noise, nonzero in floating point, so the
+// rank comes out as min(m, n) (or kmax) -- not K.  The factor route would cap
+// it at K, so these ops take the reference's route: form the dense m x n sum in
+// shared memory and take its SVD (QR with column pivoting + one-sided Jacobi,
+// as the CTA core), keep sigma_i > 0, cap at kmax.  One CTA per op, m, n <= 64
+// (larger blocks are reported as unsupported through ctx.err[2]).
+#define D0_KM 64
+#define D0_NT 256
+static size_t smem_d0() { return (size_t)(3 * D0_KM * D0_KM + 3 * D0_KM) * sizeof(double); }
+
+__global__ void __launch_bounds__(D0_NT)
+    k_rkt_d0(hlu_ctx c, const hlu_rkt_desc *__restrict__ d, const hlu_rkpart *__restrict__ parts, hlu_rkt_scratch sc,
+             int slot) {
+  constexpr int KM = D0_KM, NT = D0_NT, NW = NT / 32;
+  extern __shared__ double sm[];
+  double *G = sm;              // p x q (the dense sum or its transpose), later reflectors
+  double *V = G + KM * KM;     // Jacobi rotations
+  double *XT = V + KM * KM;    // R^T, later W = U S
+  double *tau = XT + KM * KM;  // KM
+  double *sig = tau + KM;      // KM (norms in the QRCP, then singular values)
+  __shared__ PartInfo P[RK_MAXP];
+  __shared__ int perm[KM];
+  __shared__ int cmap[KM];
+  __shared__ unsigned char pairs_a[(KM - 1) * (KM / 2)], pairs_b[(KM - 1) * (KM / 2)];
+  __shared__ int s_kk;
+  const int tid = threadIdx.x, wq = tid >> 5;
+  const int nops = sc.counts[RK_CNT * slot + RK_SEG_D0];
+  const int32_t *lst = sc.list + RK_SEG_D0 * sc.max_ops;
+  for (int idx = blockIdx.x; idx < nops; idx += gridDim.x) {
+    const hlu_rkt_desc o = d[lst[idx]];
+    const int np = load_parts(c, o, parts, P);
+    const int m = o.m, n = o.n;
+    const bool tr = n > m;  // G = D (m >= n) or D^T, so that G has q <= p columns
+    const int p = tr ? n : m, q = tr ? m : n;
+    int K = 0;
+    for (int t = 0; t < np; ++t) K += P[t].k;
+    // dense sum D(i, j) = sum over the stacked columns of X(i, t) Y(j, t)
+    for (int e = tid; e < m * n; e += NT) {
+      const int i = e % m, j = e / m;
+      double acc = 0.0;
+      for (int t = 0; t < K; ++t) acc = fma(stacked(P, np, true, i, t), stacked(P, np, false, j, t), acc);
+      if (tr) G[j + i * KM] = acc;
+      else G[i + j * KM] = acc;
+    }
+    __syncthreads();
+    qrcp_fast<KM, NT>(G, p, q, tau, cmap, sig);
+    for (int e = tid; e < KM * KM; e += NT) {
+      const int i = e % KM, j = e / KM;  // XT[i, j] = R[j, i]
+      XT[e] = (i < q && j < q && j <= i) ? G[j + cmap[i] * KM] : 0.0;
+    }
+    build_pairs<NT>(pairs_a, pairs_b, q + (q & 1));
+    __syncthreads();
+    jacobi<KM, NT>(XT, V, q, pairs_a, pairs_b);
+    for (int j = tid; j < q; j += NT) {
+      double ss = 0.0;
+      for (int i = 0; i < q; ++i) ss = fma(XT[i + j * KM], XT[i + j * KM], ss);
+      sig[j] = sqrt(ss);
+    }
+    __syncthreads();
+    for (int j = tid; j < q; j += NT) {
+      int rk = 0;
+      const double sj = sig[j];
+      for (int i = 0; i < q; ++i) rk += (sig[i] > sj) || (sig[i] == sj && i < j);
+      perm[rk] = j;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      const double s1 = sig[perm[0]];
+      int kk = 0;
+      if (s1 != 0.0) {
+        const double thr = c.eps * s1;  // eps == 0: every nonzero singular value
+        for (int i = 0; i < q; ++i) kk += sig[i] > thr;
+      }
+      if (c.kmax >= 0) kk = min(kk, c.kmax);
+      if (kk > o.cap) {
+        atomicAdd(&c.err[0], 1);
+        kk = o.cap;
+      }
+      s_kk = kk;
+    }
+    __syncthreads();
+    const int kk = s_kk;
+    // G = D  (!tr): A' = Q (V S)_sel, B' = P W_sel / S ;  G = D^T (tr): A' = P W_sel, B' = Q V_sel
+    double *outA = c.pool + o.out_a, *outB = c.pool + o.out_b;
+    double *WQ = tr ? outB : outA;  // p rows, the side Q is applied to
+    double *WP = tr ? outA : outB;  // q rows, permuted
+    const int ldq = p, ldp = q;
+    for (int e = tid; e < p * kk; e += NT) {
+      const int i = e % p, cidx = e / p;
+      const int j = perm[cidx];
+      WQ[i + cidx * ldq] = (i < q) ? (tr ? V[i + j * KM] : V[i + j * KM] * sig[j]) : 0.0;
+    }
+    for (int e = tid; e < q * kk; e += NT) {
+      const int i = e % q, cidx = e / q;
+      const int j = perm[cidx];
+      WP[cmap[i] + cidx * ldp] = tr ? XT[i + j * KM] : XT[i + j * KM] / sig[j];
+    }
+    __syncthreads();
+    for (int col = wq; col < kk; col += NW) qrcp_apply<KM>(G, p, q, tau, cmap, WQ + col * ldq);
+    __syncthreads();
+    if (tid == 0) {
+      c.ranks[o.out_slot] = kk;
+      c.log[o.log + 2] = kk;
+    }
+    __syncthreads();
+  }
+}
+
 // ---------------------------------------------------------------- phase C
 
 // BIG: the large-buffer row blocks (see k_rkt_a); their moving block holds
@@ -1497,6 +1618,7 @@ static void rkt_init() {
   cudaFuncSetAttribute(k_rkt_r<2, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RCfg<2, 8>::smem());
   cudaFuncSetAttribute(k_rkt_r<2, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RCfg<2, 16>::smem());
   cudaFuncSetAttribute(k_rkt_bw<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)BwCfg<16>::smem());
+  cudaFuncSetAttribute(k_rkt_d0, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_d0());
   if (dev < 64) done |= 1ull << dev;
 }
 
@@ -1513,7 +1635,7 @@ static void launch_r(const hlu_ctx *ctx, hlu_rkt_desc *d, const hlu_rkpart *part
 }
 
 // kernels of one level: 0 classify, 1 register warp K<=8, 2 register warp K<=16,
-// 3 (none), 4 block TSQR, 5 core by one warp (K<=16), 6 core K<=32, 7 core K>32, 8 Q apply,
+// 3 eps == 0 dense fallback (launched only when ctx->eps == 0), 4 block TSQR, 5 core by one warp (K<=16), 6 core K<=32, 7 core K>32, 8 Q apply,
 // 9 block TSQR (large buffer), 10 Q apply (large buffer)
 #define RK_NKERN 11
 static int rkt_launch(int which, const hlu_ctx *ctx, hlu_rkt_desc *d, const hlu_rkpart *parts, int64_t first,
@@ -1526,7 +1648,7 @@ static int rkt_launch(int which, const hlu_ctx *ctx, hlu_rkt_desc *d, const hlu_
       break;
     case 1: launch_r<2, 8>(ctx, d, parts, count, s, slot, st); break;
     case 2: launch_r<2, 16>(ctx, d, parts, count, s, slot, st); break;
-    case 3: break;  // no kernel (kept so the stamp slots stay stable)
+    case 3: k_rkt_d0<<<lim(count, 1), D0_NT, smem_d0(), st>>>(*ctx, d, parts, s, slot); break;
     case 4: k_rkt_a<false><<<lim(2 * (int64_t)count, 4), HLU_NT, smem_a(false), st>>>(*ctx, d, parts, s, slot); break;
     case 9: k_rkt_a<true><<<lim(2 * (int64_t)count, 1), HLU_NT, smem_a(true), st>>>(*ctx, d, parts, s, slot); break;
     case 5:
@@ -1573,7 +1695,10 @@ extern "C" int hlu_rkt_phases(const hlu_ctx *ctx, hlu_rkt_desc *d, const hlu_rkp
   };
   if (!aux) {
     static const int order[RK_NKERN] = {0, 1, 2, 3, 4, 9, 5, 6, 7, 8, 10};
-    for (int w : order) run(w, st);
+    for (int w : order) {
+      if (w == 3 && ctx->eps != 0.0) continue;
+      run(w, st);
+    }
     stamp(RK_NKERN, st);
     return cudaGetLastError() == cudaSuccess ? 0 : -1;
   }
@@ -1587,7 +1712,8 @@ extern "C" int hlu_rkt_phases(const hlu_ctx *ctx, hlu_rkt_desc *d, const hlu_rkp
   run(1, s0);
   cudaEventRecord(ev[1], s0);
   run(2, s1);
-  stamp(3, s1);
+  if (ctx->eps == 0.0) run(3, s1);  // dense-fallback ops exist only with eps == 0
+  else stamp(3, s1);
   cudaEventRecord(ev[2], s1);
   // block TSQR: large-buffer items on side[2] beside the small ones
   cudaStreamWaitEvent(s2, ev[0], 0);

@@ -84,6 +84,25 @@ def test_add_truncated_shortcuts(rng):
     assert got.k == 3 and np.array_equal(got.value(), x.value())
 
 
+@pytest.mark.parametrize("m,n,k1,k2,kmax", [(8, 8, 3, 3, None), (10, 10, 3, 3, 2), (16, 12, 4, 3, None),
+                                            (64, 40, 12, 10, None), (40, 30, 3, 4, None), (33, 64, 20, 20, 5)])
+def test_add_truncated_eps0(rng, m, n, k1, k2, kmax):
+    """TruncationControl(0.0[, kmax]) (reference tests/test_lowrank.py:115): in
+    the dense-fallback branch (k1 + k2 >= min(m, n) / 2, lowrank.py:164) the
+    reference SVDs the dense sum and keeps every nonzero singular value, so the
+    rank is min(m, n) (or kmax), not k1 + k2; the GPU takes the same route."""
+    ctl = TruncationControl(0.0, kmax)
+    x1, x2 = _lr(rng, m, n, k1), _lr(rng, m, n, k2)
+    want = orc.add_truncated(x1, x2, ctl)
+    got = device_ops.add_truncated(x1, x2, ctl)
+    assert got.k == want.k
+    exact = x1.value() + x2.value()
+    if kmax is None:
+        assert np.linalg.norm(got.value() - exact) <= 1e-12 * np.linalg.norm(exact)
+    else:
+        assert _spec(got.value() - want.value()) <= 1e-10 * _spec(exact)
+
+
 def test_add_truncated_parallel_outer(rng):
     a = rng.standard_normal((8, 1))
     b = rng.standard_normal((5, 1))
