@@ -53,8 +53,14 @@ __device__ __forceinline__ void dmma16884(double (&d)[4], const double (&a)[4], 
 }
 
 // 8-byte global -> shared copy that bypasses the registers (LDGSTS);
-// ok == false writes a zero (src-size 0: nothing is read)
-__device__ __forceinline__ void cp_async8(double *sdst, const double *gsrc, bool ok) {
+// ok == false writes a zero (src-size 0: nothing is read).  Operands that
+// already live in shared memory (the W block of a triple term) are copied
+// with a plain load / store instead (cp.async takes global sources only).
+__device__ __forceinline__ void cp_async8(double *sdst, const double *gsrc, bool ok, bool src_shared) {
+  if (src_shared) {
+    *sdst = ok ? *gsrc : 0.0;
+    return;
+  }
   const unsigned s = (unsigned)__cvta_generic_to_shared(sdst);
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gsrc), "r"(ok ? 8 : 0) : "memory");
 }
@@ -73,6 +79,7 @@ __device__ __noinline__ void tile_gemm(const Mat &C, const Mat &A, const Mat &B,
   const int wm = (wid & 3) * 16, wn = (wid >> 2) * 32;
   // coalescing: walk each operand's unit-stride dimension fastest
   const bool a_rf = A.rs == 1, b_rf = B.rs == 1;
+  const bool a_sh = __isShared(A.p), b_sh = __isShared(B.p);
   // element (row r, depth q) of the A tile / (depth q, col c) of the B tile
   const int am = a_rf ? 1 : GL32, ak = a_rf ? GL64 : 1;
   const int bk = b_rf ? 1 : GL64, bn = b_rf ? GL32 : 1;
@@ -91,11 +98,11 @@ __device__ __noinline__ void tile_gemm(const Mat &C, const Mat &A, const Mat &B,
           const int r = a_rf ? e % GB : e / GK, q = a_rf ? e / GB : e % GK;
           const int gi = i0 + r, gk = k0 + q;
           const bool oka = gi < m && gk < k;
-          cp_async8(ta + r * am + q * ak, oka ? &A.at(gi, gk) : A.p, oka);
+          cp_async8(ta + r * am + q * ak, oka ? &A.at(gi, gk) : A.p, oka, a_sh);
           const int qq = b_rf ? e % GK : e / GB, cc = b_rf ? e / GK : e % GB;
           const int bj = j0 + cc, bkk = k0 + qq;
           const bool okb = bkk < k && bj < n;
-          cp_async8(tb + qq * bk + cc * bn, okb ? &B.at(bkk, bj) : B.p, okb);
+          cp_async8(tb + qq * bk + cc * bn, okb ? &B.at(bkk, bj) : B.p, okb, b_sh);
         }
         cp_async_commit();
       };
@@ -155,6 +162,7 @@ __device__ __noinline__ void tile_gemm(const Mat &C, const Mat &A, const Mat &B,
       }
     }
   }
+  __syncthreads();  // C may be a shared block the next call reads
 }
 
 __device__ __forceinline__ Mat sub(const Mat &x, int i0, int j0, int rows, int cols) {

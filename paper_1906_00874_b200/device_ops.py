@@ -80,6 +80,8 @@ def _truncate_parts(parts_pairs, m, n, ctl, mode, signs=None):
     ks = [p.k for p in parts_pairs]
     K = sum(ks)
     cap = max(K, 1)
+    if ctl is not None and ctl.eps == 0.0 and mode == ir.RK_ADD:
+        cap = max(cap, min(m, n))  # the dense-fallback route keeps up to min(m, n) columns
     kb = K
     ws = ir.rkt_ws_doubles(m, n, kb)
     size = sum(p.a.size + p.b.size for p in parts_pairs) + (m + n) * cap + ws + 16

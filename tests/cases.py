@@ -63,6 +63,7 @@ CASES = {
     "cfg3p_8192": (lambda: bem(3, 8192, 2.0, 64, 1e-4, None), (1e-4, None)),
     "cfg2": (lambda: bem(3, 32768, 2.0, 64, 1e-6, 32), (1e-6, 32)),
     "cfg3": (lambda: bem(3, 131072, 2.0, 64, 1e-4, None), (1e-4, None)),
+    "cfg4p_16384": (lambda: bem(3, 16384, 2.0, 128, 1e-4, 48), (1e-4, 48)),
 }
 
 

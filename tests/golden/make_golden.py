@@ -166,6 +166,8 @@ CASES = {
     "cfg3p_8192": (bem(3, 8192, 2.0, 64, 1e-4, None), (1e-4, None), False, False),
     "cfg2": (bem(3, 32768, 2.0, 64, 1e-6, 32), (1e-6, 32), False, False),
     "cfg3": (bem(3, 131072, 2.0, 64, 1e-4, None), (1e-4, None), False, False),
+    # cfg4 geometry / leaf size / truncation at a size the reference finishes in minutes
+    "cfg4p_16384": (bem(3, 16384, 2.0, 128, 1e-4, 48), (1e-4, 48), False, False),
 }
 
 DEFAULT = ["mixed_192", "mixed_256_kmax", "dense2x2_256_r3", "bem1d_1024", "sphere_1024",

@@ -62,7 +62,8 @@ def run(name):
     # the reference's factors, leaf by leaf, in our (identical) structure
     cfgargs = {"cfg1": (3, 4096, 2.0, 32, 0.0, 8), "cfg2": (3, 32768, 2.0, 64, 1e-6, 32),
                "cfg3": (3, 131072, 2.0, 64, 1e-4, None), "cfg3p_8192": (3, 8192, 2.0, 64, 1e-4, None),
-               "sphere_2048_l64": (3, 2048, 2.0, 64, 1e-4, None)}[name]
+               "sphere_2048_l64": (3, 2048, 2.0, 64, 1e-4, None),
+               "cfg4p_16384": (3, 16384, 2.0, 128, 1e-4, 48)}[name]
     d, n, eta, leaf, eps, kmax = cfgargs
     ours = make_bem_case(d, n, eta, leafsize=leaf, eps=eps, kmax=kmax,
                          workers=os.cpu_count() or 1).hmatrix

@@ -216,7 +216,7 @@ def test_singular_pivot_names_block():
     assert "lu[0:4)" in str(err.value)
 
 
-@pytest.mark.parametrize("name", ["cfg3p_8192", "cfg2", "cfg3"])
+@pytest.mark.parametrize("name", ["cfg3p_8192", "cfg4p_16384", "cfg2", "cfg3"])
 def test_baseline_config_rank_parity(name):
     """BASELINE configs at full size: structure/assembly bit-exact vs the
     reference, every Rk block rank identical after the GPU H-LU, effective-flop
@@ -228,6 +228,7 @@ def test_baseline_config_rank_parity(name):
     import os
 
     d, n, eta, leaf, eps, kmax = {"cfg3p_8192": (3, 8192, 2.0, 64, 1e-4, None),
+                                  "cfg4p_16384": (3, 16384, 2.0, 128, 1e-4, 48),
                                   "cfg2": (3, 32768, 2.0, 64, 1e-6, 32),
                                   "cfg3": (3, 131072, 2.0, 64, 1e-4, None)}[name]
     h, _ = cases.bem(d, n, eta, leaf, eps, kmax, workers=os.cpu_count())
