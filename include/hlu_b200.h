@@ -214,6 +214,30 @@ int hlu_schedule_create_chains(hlu_schedule **out, const hlu_ctx *ctx, const hlu
                                const hlu_term *terms, hlu_rkt_desc *rkt, const hlu_rkpart *parts,
                                const hlu_rkt_scratch *scratch, const int32_t *wait_dense, const int32_t *wait_rkt,
                                int64_t nlevels, int use_graph, void *stream);
+/* --- multi-GPU: owner-computes H-LU over a communicator (NCCL, NVLink) --- */
+typedef struct hlu_comm hlu_comm;
+struct hlu_xfer_s;
+int hlu_comm_available(void);            /* 1 when libnccl.so.2 could be loaded */
+int hlu_comm_unique_id(void *out128);    /* rank 0: returns the id size (128) */
+int hlu_comm_init(hlu_comm **out, const void *id128, int nranks, int rank); /* on the rank's device */
+int hlu_comm_destroy(hlu_comm *c);
+/* Sharded schedule (include/hlu_plan.h hlu_plan_build_sharded): this rank's
+ * launches level by level; after every level the exchange groups of that level
+ * (xfer records: host copy for the grouping, device copy for the kernels; the
+ * staging buffer holds hlu_xfer_staging_doubles); after the last level the
+ * final gather and the reduction of the nlog flop-log entries and the error
+ * words over the communicator.  Every rank ends with the whole factorization. */
+int hlu_schedule_create_sharded(hlu_schedule **out, const hlu_ctx *ctx, const hlu_launch *launches, int64_t nlaunch,
+                                const hlu_getrf_desc *getrf, const hlu_trsm_desc *trsm, const hlu_gemm_desc *gemm,
+                                const hlu_term *terms, hlu_rkt_desc *rkt, const hlu_rkpart *parts,
+                                const hlu_rkt_scratch *scratch, hlu_comm *comm, const void *xfer_host,
+                                const void *xfer_dev, int64_t nxfer, int64_t nlevels, int64_t nlog, double *staging,
+                                int use_graph, void *stream);
+int64_t hlu_xfer_staging_doubles(const void *xfer, int64_t n);
+/* one exchange group (diagnostics / tests): gather -> ncclBroadcast -> scatter */
+int hlu_xfer_group(hlu_comm *c, double *pool, int32_t *ranks, const void *xfer_dev, int n, int src, int64_t count,
+                   double *staging, void *stream);
+
 int hlu_schedule_launch(hlu_schedule *s, void *stream);
 int hlu_schedule_destroy(hlu_schedule *s);
 /* diagnostics: with HLU_STAMPS=1 at creation, the %globaltimer (ns) before the first and

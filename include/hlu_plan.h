@@ -59,6 +59,15 @@ typedef struct hlu_plan hlu_plan;
 int hlu_plan_build(hlu_plan **out, const hlu_plan_node *nodes, int64_t nnodes, const hlu_plan_cmd *cmds,
                    int64_t ncmds, int32_t cap, int64_t ident_off, int64_t nslots, int32_t nrk, int64_t arena_base,
                    int32_t split_rows);
+/* Owner-computes sharding over nranks GPUs: slot_owner[s] is
+ * the rank owning skeleton slot s; the plan for `rank` holds only the ops that
+ * rank executes (the writer's owner; temp producers on every consuming rank),
+ * with the single-GPU levels, temps and op order, plus the slot exchange
+ * records (hlu_plan_xfer).  slot_owner == NULL is hlu_plan_build. */
+int hlu_plan_build_sharded(hlu_plan **out, const hlu_plan_node *nodes, int64_t nnodes, const hlu_plan_cmd *cmds,
+                           int64_t ncmds, int32_t cap, int64_t ident_off, int64_t nslots, int32_t nrk,
+                           int64_t arena_base, int32_t split_rows, const int32_t *slot_owner, int32_t nranks,
+                           int32_t rank);
 const char *hlu_plan_error(const hlu_plan *p);
 /* sizes[14]: getrf, trsm, gemm, terms, rkt, parts, launches, ops, levels, arena doubles,
  *            log entries, rank slots, LU count, temps */
@@ -73,6 +82,22 @@ int hlu_plan_copy(const hlu_plan *p, void *getrf, void *trsm, void *gemm, void *
  * hazard the two chains cannot express (the caller keeps level barriers). */
 int hlu_plan_level_waits(const hlu_plan *p, int32_t *wait_dense, int32_t *wait_rkt);
 void hlu_plan_free(hlu_plan *p);
+
+/* One slot exchange record of a sharded plan: after level `level` (level ==
+ * nlevels: the final gather) rank `src` broadcasts pool[off, off+len) and, for
+ * an Rk slot, ranks[rank_slot] (as a double after the payload) to every rank,
+ * staged at boff of group `group`'s buffer.  Records are ordered by (level,
+ * src, group); a group's staging buffer holds sum(len + 1) doubles. */
+typedef struct {
+  int32_t level, src;
+  int32_t group, rank_slot; /* rank_slot -1: dense slot */
+  int64_t off, len, boff;
+} hlu_xfer; /* 40 bytes */
+
+/* exchange records of a sharded plan (out may be NULL); returns their count */
+int64_t hlu_plan_xfer(const hlu_plan *p, hlu_xfer *out);
+/* per op: bit r set when rank r executes it (sharded plans only; else -1) */
+int hlu_plan_op_owners(const hlu_plan *p, uint64_t *out);
 
 /* --- host payload staging (the upload / download of hlu_factorize) ---
  * One leaf payload: a row-major host array (numpy C order, rows x cols, row

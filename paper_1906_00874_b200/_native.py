@@ -33,6 +33,13 @@ SYMBOLS = (
     "hlu_device_check",
     "hlu_debug_sweeps",
     "hlu_debug_bprof",
+    "hlu_comm_available",
+    "hlu_comm_unique_id",
+    "hlu_comm_init",
+    "hlu_comm_destroy",
+    "hlu_schedule_create_sharded",
+    "hlu_xfer_staging_doubles",
+    "hlu_xfer_group",
 )
 
 
@@ -98,6 +105,20 @@ def lib():
     L.hlu_schedule_destroy.argtypes = [vp]
     L.hlu_schedule_stamps.argtypes = [vp, vp]
     L.hlu_schedule_stamps.restype = i64
+    L.hlu_comm_available.restype = ctypes.c_int
+    L.hlu_comm_unique_id.argtypes = [vp]
+    L.hlu_comm_unique_id.restype = ctypes.c_int
+    L.hlu_comm_init.argtypes = [ctypes.POINTER(vp), vp, ctypes.c_int, ctypes.c_int]
+    L.hlu_comm_init.restype = ctypes.c_int
+    L.hlu_comm_destroy.argtypes = [vp]
+    L.hlu_comm_destroy.restype = ctypes.c_int
+    L.hlu_schedule_create_sharded.argtypes = [ctypes.POINTER(vp), ctypes.POINTER(HluCtx), vp, i64,
+                                              vp, vp, vp, vp, vp, vp, sp, vp, vp, vp, i64, i64, i64, vp, i32, vp]
+    L.hlu_schedule_create_sharded.restype = ctypes.c_int
+    L.hlu_xfer_staging_doubles.argtypes = [vp, i64]
+    L.hlu_xfer_staging_doubles.restype = i64
+    L.hlu_xfer_group.argtypes = [vp, vp, vp, vp, ctypes.c_int, ctypes.c_int, i64, vp, vp]
+    L.hlu_xfer_group.restype = ctypes.c_int
     L.hlu_version.restype = ctypes.c_char_p
     for name in ("hlu_getrf_batched_f64", "hlu_trsm_batched_f64", "hlu_gemm_batched_f64", "hlu_gemm_small_batched_f64",
                  "hlu_rk_update_batched_f64", "hlu_rkt_phases", "hlu_rkt_phase", "hlu_schedule_create", "hlu_schedule_create_chains",

@@ -28,8 +28,8 @@
 namespace {
 
 constexpr int64_t TEMP_SHIFT = 36;  // temp t at (t+1) << 36: up to 2^27 temps, 2^36-double offsets
-constexpr int KMAX_STACK = 64;
-constexpr int IDENT = 64;
+constexpr int KMAX_STACK = RK_KMAXW;  // widest factor pair a truncation takes
+constexpr int IDENT = RK_KMAXW;  // identity block edge kept in the pool
 constexpr int F_STATIC = 0, F_LIN = 1, F_RKUPD = 2, F_QUAD = 3;
 
 struct View {
@@ -812,6 +812,12 @@ struct Planner {
 
   // ---------------------------------------------------------- schedule
   std::vector<int64_t> levels;
+  // owner-computes sharding: ranks executing every op, and the
+  // slot exchange records (include/hlu_plan.h hlu_xfer)
+  int nranks = 1, my_rank = 0;
+  const int32_t *slot_owner = nullptr;  // per skeleton slot
+  std::vector<uint64_t> op_mask;
+  std::vector<hlu_xfer> o_xfer;
   std::vector<int64_t> toffs;
   std::vector<int64_t> tbirth;  // level of each temp's producer
   std::vector<int64_t> reuse_from;  // temp whose arena block a temp takes over (-1: fresh)
@@ -1127,6 +1133,145 @@ struct Planner {
   std::vector<hlu_term> chain_terms;
   std::vector<int64_t> chain_bounds;
 
+  // Every op runs on the owner of the skeleton slot it writes; an op writing
+  // only temps (a product / accumulated Rk temp, a hoisted inner product) runs
+  // on every rank that consumes the temp, so temps never cross ranks and the
+  // per-destination op order (hence every rank decision) is the single-GPU one.
+  void shard_ops() {
+    const size_t n = ops.size();
+    if (nranks > 64) throw std::runtime_error("at most 64 ranks");
+    op_mask.assign(n, 0);
+    std::vector<uint64_t> cons(temp_size.size(), 0);
+    for (size_t ii = n; ii-- > 0;) {
+      const Op &o = ops[ii];
+      int owner = -1;
+      for (int64_t w = o.w_begin; w < o.w_end; ++w) {
+        const Iv &v = ivs[w];
+        if (v.lo >= nslots) continue;
+        for (int64_t sl = v.lo; sl < v.hi; ++sl) {
+          const int r = slot_owner[sl];
+          if (owner >= 0 && r != owner) throw std::runtime_error("an op writes slots of two owners");
+          owner = r;
+        }
+      }
+      uint64_t m = 0;
+      if (owner >= 0) {
+        m = 1ull << owner;
+      } else {
+        for (int64_t k = o.to_begin; k < o.to_end; ++k) m |= cons[tids[k]];
+        if (!m) m = 1ull;  // an unread temp: rank 0
+      }
+      op_mask[ii] = m;
+      for (int64_t k = o.ti_begin; k < o.ti_end; ++k) cons[tids[k]] |= m;
+    }
+  }
+
+  // slot payload region (pool offset, doubles) and rank slot of skeleton slot s
+  std::vector<int32_t> slot_node;
+  void slot_nodes() {
+    slot_node.assign(nslots, -1);
+    for (int64_t i = 0; i < nnodes; ++i)
+      if (N[i].kind != 2 && N[i].lo >= 0 && N[i].lo < nslots) slot_node[N[i].lo] = (int32_t)i;
+  }
+  bool slot_region(int64_t sl, int64_t *off, int64_t *len, int32_t *rslot) const {
+    const int32_t k = slot_node[sl];
+    if (k < 0) return false;
+    const auto &x = N[k];
+    const int64_t rows = x.r1 - x.r0, cols = x.c1 - x.c0;
+    *off = x.off_a;
+    if (x.kind == 0) {
+      *len = rows * cols;
+      *rslot = -1;
+    } else {
+      *len = (rows + cols) * (int64_t)cap;  // a slab (rows x cap) then b slab (cols x cap)
+      *rslot = x.slot;
+    }
+    return true;
+  }
+
+  // Exchange records: after level lv, rank w broadcasts every slot it wrote in
+  // lv that an op of another rank reads (at any level: a superset of what the
+  // later levels need); a final step (level nlevels) ships every written slot
+  // from its owner, so each rank ends with the whole factorization.  Records
+  // are grouped by (level, src), groups capped at XFER_GROUP doubles, with
+  // their offsets in the group's staging buffer (payload, then the rank).
+  static constexpr int64_t XFER_GROUP = int64_t(1) << 26;  // 512 MB
+  void exchange(const std::vector<int64_t> &order) {
+    slot_nodes();
+    const int64_t S = nslots;
+    std::vector<uint64_t> readers(S, 0);
+    {
+      std::vector<int32_t> diff((size_t)(S + 1) * nranks, 0);
+      for (size_t i = 0; i < ops.size(); ++i) {
+        const Op &o = ops[i];
+        for (int64_t r = o.r_begin; r < o.r_end; ++r) {
+          const Iv &v = ivs[r];
+          if (v.lo >= S) continue;
+          const int64_t hi = std::min<int64_t>(v.hi, S);
+          for (int b = 0; b < nranks; ++b)
+            if ((op_mask[i] >> b) & 1ull) {
+              ++diff[(size_t)v.lo * nranks + b];
+              --diff[(size_t)hi * nranks + b];
+            }
+        }
+      }
+      std::vector<int32_t> run(nranks, 0);
+      for (int64_t sl = 0; sl < S; ++sl)
+        for (int b = 0; b < nranks; ++b) {
+          run[b] += diff[(size_t)sl * nranks + b];
+          if (run[b] > 0) readers[sl] |= 1ull << b;
+        }
+    }
+    std::vector<char> written(S, 0);
+    struct X {
+      int64_t lv;
+      int32_t src;
+      int64_t sl;
+    };
+    std::vector<X> xs;
+    for (int64_t i : order) {  // level order
+      const Op &o = ops[i];
+      for (int64_t w = o.w_begin; w < o.w_end; ++w) {
+        const Iv &v = ivs[w];
+        if (v.lo >= S) continue;
+        for (int64_t sl = v.lo; sl < std::min<int64_t>(v.hi, S); ++sl) {
+          written[sl] = 1;
+          const int32_t src = slot_owner[sl];
+          if (readers[sl] & ~(1ull << src)) xs.push_back(X{levels[i], src, sl});
+        }
+      }
+    }
+    for (int64_t sl = 0; sl < S; ++sl)
+      if (written[sl]) xs.push_back(X{nlevels, slot_owner[sl], sl});
+    std::stable_sort(xs.begin(), xs.end(), [](const X &a, const X &b) {
+      return a.lv != b.lv ? a.lv < b.lv : a.src < b.src;
+    });
+    o_xfer.clear();
+    int64_t glv = -1, gsrc = -1, gfill = 0;
+    int32_t group = -1;
+    for (const X &x : xs) {
+      int64_t off, len;
+      int32_t rslot;
+      if (!slot_region(x.sl, &off, &len, &rslot)) continue;
+      if (x.lv != glv || x.src != gsrc || gfill + len + 1 > XFER_GROUP) {
+        ++group;
+        glv = x.lv;
+        gsrc = x.src;
+        gfill = 0;
+      }
+      hlu_xfer r;
+      r.level = (int32_t)x.lv;
+      r.src = x.src;
+      r.group = group;
+      r.rank_slot = rslot;
+      r.off = off;
+      r.len = len;
+      r.boff = gfill;
+      gfill += len + 1;
+      o_xfer.push_back(r);
+    }
+  }
+
   static double now_s() {
     return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
   }
@@ -1138,6 +1283,7 @@ struct Planner {
     allocate_temps();
     if (timing) std::fprintf(stderr, "plan: temps %.2fs\n", now_s() - t0), t0 = now_s();
     const size_t n = ops.size();
+    if (slot_owner) shard_ops();
     // ops ordered by (level, kind), program order inside: a stable counting sort
     std::vector<int64_t> order(n);
     {
@@ -1181,6 +1327,7 @@ struct Planner {
     for (int64_t i : order) {
       const Op &o = ops[i];
       const int64_t lv = levels[i];
+      if (slot_owner && !((op_mask[i] >> my_rank) & 1ull)) continue;  // another rank's op
       if (pending_lv >= 0 && (o.kind != 2 || lv != pending_lv)) {
         flush_gemm();
         pending_lv = -1;
@@ -1271,7 +1418,7 @@ struct Planner {
       L.first = r.first;
       L.level = (int32_t)r.lv;
       if (r.kind == HLU_K_RKT32) {
-        L.smem_dim = r.dep ? 1 : 0;
+        L.smem_dim = (r.dep ? 1 : 0) | (r.dim > RK_KMAX ? 2 : 0);  // bit 2: may take the wide path
         o_launch.push_back(L);
       } else {
         L.smem_dim = r.dim;
@@ -1279,6 +1426,7 @@ struct Planner {
       }
     }
     nlevels = n ? (*std::max_element(levels.begin(), levels.end()) + 1) : 0;
+    if (slot_owner) exchange(order);
     if (timing) std::fprintf(stderr, "plan: pack %.2fs\n", now_s() - t0), t0 = now_s();
     compute_waits();
     if (timing) std::fprintf(stderr, "plan: waits %.2fs\n", now_s() - t0);
@@ -1374,9 +1522,26 @@ struct hlu_plan {
 extern "C" int hlu_plan_build(hlu_plan **out, const hlu_plan_node *nodes, int64_t nnodes, const hlu_plan_cmd *cmds,
                               int64_t ncmds, int32_t cap, int64_t ident_off, int64_t nslots, int32_t nrk,
                               int64_t arena_base, int32_t split_rows) {
+  return hlu_plan_build_sharded(out, nodes, nnodes, cmds, ncmds, cap, ident_off, nslots, nrk, arena_base, split_rows,
+                                nullptr, 1, 0);
+}
+
+extern "C" int hlu_plan_build_sharded(hlu_plan **out, const hlu_plan_node *nodes, int64_t nnodes,
+                                      const hlu_plan_cmd *cmds, int64_t ncmds, int32_t cap, int64_t ident_off,
+                                      int64_t nslots, int32_t nrk, int64_t arena_base, int32_t split_rows,
+                                      const int32_t *slot_owner, int32_t nranks, int32_t rank) {
   hlu_plan *p = new hlu_plan();
   *out = p;
   Planner &P = p->P;
+  if (slot_owner) {  // nranks == 1 with an owner map: the sharded machinery on one GPU (final gather only)
+    if (nranks < 1 || rank < 0 || rank >= nranks) {
+      p->error = "sharded plan: bad rank / owner map";
+      return -1;
+    }
+    P.nranks = nranks;
+    P.my_rank = rank;
+    P.slot_owner = slot_owner;
+  }
   P.N = nodes;
   P.nnodes = nnodes;
   P.cap = cap;
@@ -1445,6 +1610,19 @@ extern "C" int hlu_plan_sizes(const hlu_plan *p, int64_t *s) {
   s[11] = P.nrank;
   s[12] = (int64_t)P.lu_ops.size();
   s[13] = (int64_t)P.temp_size.size();
+  return 0;
+}
+
+extern "C" int64_t hlu_plan_xfer(const hlu_plan *p, hlu_xfer *out) {
+  const Planner &P = p->P;
+  if (out && !P.o_xfer.empty()) std::memcpy(out, P.o_xfer.data(), P.o_xfer.size() * sizeof(hlu_xfer));
+  return (int64_t)P.o_xfer.size();
+}
+
+extern "C" int hlu_plan_op_owners(const hlu_plan *p, uint64_t *out) {
+  const Planner &P = p->P;
+  if (P.op_mask.empty()) return -1;
+  std::memcpy(out, P.op_mask.data(), P.op_mask.size() * sizeof(uint64_t));
   return 0;
 }
 

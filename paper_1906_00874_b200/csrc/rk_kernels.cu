@@ -654,7 +654,8 @@ struct StackedR {  // the blocks' R factors stacked: block b at R + b K K (ld K)
 #define RK_CNT_BIGITEMS 2  // row blocks of the CTA-path ops for the large-buffer phase A/C kernels
 #define RK_SEG_BIG 3    // CTA phases (and the ADD shortcuts / empty recompressions)
 #define RK_SEG_C16 4    // CTA-path ops with K <= 16, m, n <= RK_BR: core SVD by one warp
-#define RK_SEG_D0 5    // eps == 0 dense-fallback ops (k_rkt_d0); segment 6: unused
+#define RK_SEG_D0 5    // eps == 0 dense-fallback ops (k_rkt_d0)
+#define RK_SEG_W 6     // stacked rank 64 < K <= 128: the wide path (k_rkt_w)
 #define RK_NSEG 7
 #define RK_CNT_ITEMS 7  // row blocks of the CTA-path ops for the small-buffer phase A/C kernels
 
@@ -686,7 +687,7 @@ __global__ void k_rkt_classify(hlu_ctx c, const hlu_rkt_desc *__restrict__ d, co
     s.list[RK_SEG_BIG * s.max_ops + atomicAdd(&cnt[RK_SEG_BIG], 1)] = op;
     return;
   }
-  if (K > RK_KMAX || o.part_count > RK_MAXP) {
+  if (K > RK_KMAXW || o.part_count > RK_MAXP) {
     atomicAdd(&c.err[2], 1);
     return;
   }
@@ -696,6 +697,10 @@ __global__ void k_rkt_classify(hlu_ctx c, const hlu_rkt_desc *__restrict__ d, co
       return;
     }
     s.list[RK_SEG_D0 * s.max_ops + atomicAdd(&cnt[RK_SEG_D0], 1)] = op;
+    return;
+  }
+  if (K > RK_KMAX) {  // wide path
+    s.list[RK_SEG_W * s.max_ops + atomicAdd(&cnt[RK_SEG_W], 1)] = op;
     return;
   }
   if (max(o.m, o.n) <= 64 && K <= 16) {
@@ -1555,6 +1560,134 @@ __global__ void __launch_bounds__(D0_NT)
   }
 }
 
+// ---------------------------------------------------------------- wide path (64 < K <= 128)
+//
+// The same truncation as phases A-C (recompress, lowrank.py:137-145: QR of the
+// stacked factors, SVD of R_x R_y^T, truncation, Q applied to the kept
+// vectors) for stacked ranks above the block-TSQR pipeline's 64 -- merges of
+// several kmax-wide parts and compress_dense of dense products with a wide
+// inner dimension at leaf 128 (cfg4).  One 512-thread CTA per op with its
+// operands in the op's global workspace (L2-resident): Householder QR of X
+// and Y on two warp groups, M = R_x R_y^T (K x K), one-sided Jacobi on M
+// (M V = W = U S), rank sigma_i > eps sigma_1 (strict) and kmax, then
+// A' = Q_x [W_sel; 0], B' = Q_y [V_sel; 0].
+#define RW_NT 512
+
+// z (rows, stride 1) <- Q [z] with the reflectors of house_qr (below the
+// diagonal of column j of S, ld rows, tau[j]); one warp
+__device__ void house_apply(const double *S, int rows, int t, const double *tau, double *z) {
+  const int l = threadIdx.x & 31;
+  for (int j = t - 1; j >= 0; --j) {
+    const double tj = tau[j];
+    if (tj == 0.0) continue;
+    const double *v = S + (int64_t)j * rows;
+    double acc = 0.0;
+    for (int i = j + 1 + l; i < rows; i += 32) acc = fma(v[i], z[i], acc);
+    acc = warp_sum(acc) + z[j];
+    const double f = tj * acc;
+    for (int i = j + 1 + l; i < rows; i += 32) z[i] -= f * v[i];
+    __syncwarp();
+    if (l == 0) z[j] -= f;
+    __syncwarp();
+  }
+}
+
+__global__ void __launch_bounds__(RW_NT)
+    k_rkt_w(hlu_ctx c, const hlu_rkt_desc *__restrict__ d, const hlu_rkpart *__restrict__ parts, hlu_rkt_scratch sc,
+            int slot) {
+  constexpr int KW = RK_KMAXW, NT = RW_NT, NW = NT / 32;
+  __shared__ PartInfo P[RK_MAXP];
+  __shared__ int perm[KW];
+  __shared__ unsigned char pairs_a[(KW - 1) * (KW / 2)], pairs_b[(KW - 1) * (KW / 2)];
+  __shared__ int s_kk;
+  const int tid = threadIdx.x, wq = tid >> 5;
+  const int nops = sc.counts[RK_CNT * slot + RK_SEG_W];
+  const int32_t *lst = sc.list + RK_SEG_W * sc.max_ops;
+  for (int idx = blockIdx.x; idx < nops; idx += gridDim.x) {
+    const hlu_rkt_desc o = d[lst[idx]];
+    const int np = load_parts(c, o, parts, P);
+    bool shortcut;
+    const int K = logged_K(c, o, &shortcut);
+    const int m = o.m, n = o.n;
+    double *X = c.pool + o.ws;
+    double *Y = X + (int64_t)m * K;
+    double *M = Y + (int64_t)n * K;
+    double *V = M + KW * KW;
+    double *tx = V + KW * KW;
+    double *ty = tx + KW;
+    double *sig = ty + KW;
+    for (int64_t e = tid; e < (int64_t)m * K; e += NT) X[e] = stacked(P, np, true, (int)(e % m), (int)(e / m));
+    for (int64_t e = tid; e < (int64_t)n * K; e += NT) Y[e] = stacked(P, np, false, (int)(e % n), (int)(e / n));
+    __syncthreads();
+    {
+      const Grp g{1 + (wq >= NW / 2), NW / 2, wq % (NW / 2), tid & 31, tid % (NT / 2)};
+      if (wq < NW / 2) house_qr(X, m, m, K, tx, g);
+      else house_qr(Y, n, n, K, ty, g);
+    }
+    __syncthreads();
+    const int rx = min(m, K), ry = min(n, K);
+    for (int e = tid; e < KW * KW; e += NT) {  // M = R_x R_y^T, zero outside rx x ry
+      const int i = e % KW, j = e / KW;
+      double acc = 0.0;
+      if (i < rx && j < ry)
+        for (int t = max(i, j); t < K; ++t) acc = fma(X[i + (int64_t)t * m], Y[j + (int64_t)t * n], acc);
+      M[e] = acc;
+    }
+    build_pairs<NT>(pairs_a, pairs_b, K + (K & 1));
+    __syncthreads();
+    jacobi<KW, NT>(M, V, K, pairs_a, pairs_b);
+    for (int j = tid; j < K; j += NT) {
+      double ss = 0.0;
+      for (int i = 0; i < rx; ++i) ss = fma(M[i + j * KW], M[i + j * KW], ss);
+      sig[j] = sqrt(ss);
+    }
+    __syncthreads();
+    for (int j = tid; j < K; j += NT) {
+      int rk = 0;
+      const double sj = sig[j];
+      for (int i = 0; i < K; ++i) rk += (sig[i] > sj) || (sig[i] == sj && i < j);
+      perm[rk] = j;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      const double s1 = sig[perm[0]];
+      int kk = 0;
+      if (s1 != 0.0) {
+        const double thr = c.eps * s1;
+        for (int i = 0; i < K; ++i) kk += sig[i] > thr;
+      }
+      if (c.kmax >= 0) kk = min(kk, c.kmax);
+      if (kk > o.cap) {
+        atomicAdd(&c.err[0], 1);
+        kk = o.cap;
+      }
+      s_kk = kk;
+    }
+    __syncthreads();
+    const int kk = s_kk;
+    double *outA = c.pool + o.out_a, *outB = c.pool + o.out_b;
+    for (int64_t e = tid; e < (int64_t)m * kk; e += NT) {
+      const int i = (int)(e % m), col = (int)(e / m);
+      outA[e] = i < rx ? M[i + perm[col] * KW] : 0.0;  // (U S)_sel = W_sel
+    }
+    for (int64_t e = tid; e < (int64_t)n * kk; e += NT) {
+      const int i = (int)(e % n), col = (int)(e / n);
+      outB[e] = i < ry ? V[i + perm[col] * KW] : 0.0;
+    }
+    __syncthreads();
+    for (int col = wq; col < 2 * kk; col += NW) {
+      if (col < kk) house_apply(X, m, rx, tx, outA + (int64_t)col * m);
+      else house_apply(Y, n, ry, ty, outB + (int64_t)(col - kk) * n);
+    }
+    __syncthreads();
+    if (tid == 0) {
+      c.ranks[o.out_slot] = kk;
+      c.log[o.log + 2] = kk;
+    }
+    __syncthreads();
+  }
+}
+
 // ---------------------------------------------------------------- phase C
 
 // BIG: the large-buffer row blocks (see k_rkt_a); their moving block holds
@@ -1635,7 +1768,8 @@ static void launch_r(const hlu_ctx *ctx, hlu_rkt_desc *d, const hlu_rkpart *part
 }
 
 // kernels of one level: 0 classify, 1 register warp K<=8, 2 register warp K<=16,
-// 3 eps == 0 dense fallback (launched only when ctx->eps == 0), 4 block TSQR, 5 core by one warp (K<=16), 6 core K<=32, 7 core K>32, 8 Q apply,
+// 3 rare routes: eps == 0 dense fallback and the wide path (launched only when
+// ctx->eps == 0 or the level may stack more than 64 columns, hlu_rkt_set_wide_hint), 4 block TSQR, 5 core by one warp (K<=16), 6 core K<=32, 7 core K>32, 8 Q apply,
 // 9 block TSQR (large buffer), 10 Q apply (large buffer)
 #define RK_NKERN 11
 static int rkt_launch(int which, const hlu_ctx *ctx, hlu_rkt_desc *d, const hlu_rkpart *parts, int64_t first,
@@ -1648,7 +1782,10 @@ static int rkt_launch(int which, const hlu_ctx *ctx, hlu_rkt_desc *d, const hlu_
       break;
     case 1: launch_r<2, 8>(ctx, d, parts, count, s, slot, st); break;
     case 2: launch_r<2, 16>(ctx, d, parts, count, s, slot, st); break;
-    case 3: k_rkt_d0<<<lim(count, 1), D0_NT, smem_d0(), st>>>(*ctx, d, parts, s, slot); break;
+    case 3:  // the rare routes: eps == 0 dense fallback, stacked rank 64 < K <= 128
+      if (ctx->eps == 0.0) k_rkt_d0<<<lim(count, 1), D0_NT, smem_d0(), st>>>(*ctx, d, parts, s, slot);
+      k_rkt_w<<<lim(count, 1), RW_NT, 0, st>>>(*ctx, d, parts, s, slot);
+      break;
     case 4: k_rkt_a<false><<<lim(2 * (int64_t)count, 4), HLU_NT, smem_a(false), st>>>(*ctx, d, parts, s, slot); break;
     case 9: k_rkt_a<true><<<lim(2 * (int64_t)count, 1), HLU_NT, smem_a(true), st>>>(*ctx, d, parts, s, slot); break;
     case 5:
@@ -1675,6 +1812,12 @@ __global__ void k_rkt_stamp(unsigned long long *slot) {
 static unsigned long long *g_phase_stamps = nullptr;
 extern "C" void hlu_rkt_set_phase_stamps(unsigned long long *p) { g_phase_stamps = p; }
 
+// set by the schedule before each truncation launch (the launch record's
+// bit 2: an op of the level may stack more than RK_KMAX columns); single-op
+// calls (hlu_rk_update_batched_f64) always enable the rare routes
+static int g_wide_hint = 1;
+extern "C" void hlu_rkt_set_wide_hint(int on) { g_wide_hint = on; }
+
 // one level.  With aux: the two register warp kernels on side[0], side[1] and,
 // after the block TSQR, the three core kernels on the main stream, side[2],
 // side[3], all joined before the Q apply (8 events); without aux all in order.
@@ -1696,7 +1839,7 @@ extern "C" int hlu_rkt_phases(const hlu_ctx *ctx, hlu_rkt_desc *d, const hlu_rkp
   if (!aux) {
     static const int order[RK_NKERN] = {0, 1, 2, 3, 4, 9, 5, 6, 7, 8, 10};
     for (int w : order) {
-      if (w == 3 && ctx->eps != 0.0) continue;
+      if (w == 3 && ctx->eps != 0.0 && !g_wide_hint) continue;
       run(w, st);
     }
     stamp(RK_NKERN, st);
@@ -1712,7 +1855,7 @@ extern "C" int hlu_rkt_phases(const hlu_ctx *ctx, hlu_rkt_desc *d, const hlu_rkp
   run(1, s0);
   cudaEventRecord(ev[1], s0);
   run(2, s1);
-  if (ctx->eps == 0.0) run(3, s1);  // dense-fallback ops exist only with eps == 0
+  if (ctx->eps == 0.0 || g_wide_hint) run(3, s1);  // rare routes exist only then
   else stamp(3, s1);
   cudaEventRecord(ev[2], s1);
   // block TSQR: large-buffer items on side[2] beside the small ones

@@ -29,7 +29,8 @@
 #define RK_HD inline
 #endif
 
-#define RK_KMAX 64
+#define RK_KMAX 64       /* stacked rank of the block-TSQR pipeline (phases A, B, C) */
+#define RK_KMAXW 128     /* stacked rank of the wide path (k_rkt_w, 64 < K <= 128) */
 #define RK_BR 512        /* rows per block (one phase-A / phase-C work item) */
 #define RK_BUFA 16384    /* chunk buffer of the layout: (ch + K) K <= RK_BUFA (doubles) */
 #define RK_BUFS 6144     /* small phase A/C kernels: items whose chunk fits (min(ch, rows) + K) K */
@@ -76,9 +77,16 @@ RK_HD rk_side_t rk_side(int M, int K) {
   return s;
 }
 
+/* wide path workspace (global memory, K in (RK_KMAX, RK_KMAXW]):
+ * X (m x K) | Y (n x K) | M (KW x KW) | V (KW x KW) | tau_x | tau_y | sigma (KW each) */
+RK_HD int64_t rk_wide_doubles(int m, int n, int K) {
+  return (int64_t)(m + n) * K + 2 * (int64_t)RK_KMAXW * RK_KMAXW + 3 * RK_KMAXW;
+}
+
 /* reserved workspace (doubles) of one truncation with stacked rank <= kbound:
  * the maximum over K of the runtime layout.  The layout grows with K while
- * (ch, chc) stay fixed, so only the last K of every (ch, chc) class matters. */
+ * (ch, chc) stay fixed, so only the last K of every (ch, chc) class matters;
+ * kbound > RK_KMAX adds the wide path's workspace. */
 RK_HD int64_t rk_ws_doubles(int m, int n, int kbound) {
   if (m <= 0 || n <= 0 || kbound <= 0) return 0;
   const int kb = kbound < RK_KMAX ? kbound : RK_KMAX;
@@ -86,6 +94,11 @@ RK_HD int64_t rk_ws_doubles(int m, int n, int kbound) {
   for (int K = 1; K <= kb; ++K) {
     if (K < kb && rk_ch(K + 1, RK_BUFA) == rk_ch(K, RK_BUFA) && rk_chc(K + 1) == rk_chc(K)) continue;
     const int64_t t = rk_side(m, K).total + rk_side(n, K).total;
+    if (t > best) best = t;
+  }
+  if (kbound > RK_KMAX) {
+    const int kw = kbound < RK_KMAXW ? kbound : RK_KMAXW;
+    const int64_t t = rk_wide_doubles(m, n, kw);
     if (t > best) best = t;
   }
   return best;

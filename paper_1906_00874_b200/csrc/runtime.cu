@@ -6,12 +6,24 @@
 // skeleton slot is encoded in the level numbers computed on the host.
 #include <cstdio>
 #include <cstdlib>
+#include <algorithm>
 #include <cstring>
 #include <vector>
 
 #include "common.cuh"
+#include "hlu_plan.h"
 
 extern "C" void hlu_rkt_set_phase_stamps(unsigned long long *p);
+extern "C" void hlu_rkt_set_wide_hint(int on);
+struct hlu_comm;
+
+extern "C" int hlu_comm_reduce_logs(hlu_comm *c, int32_t *log, int64_t nlog, int32_t *err, void *stream);
+
+// one (level, source rank) exchange group of a sharded schedule
+struct XGroup {
+  int32_t level, src;
+  int64_t first, n, count;  // records [first, first + n) of the device table, staging doubles
+};
 
 struct hlu_schedule {
   hlu_ctx ctx;
@@ -34,6 +46,12 @@ struct hlu_schedule {
   // two-chain mode: per-level cross-chain waits and the events they wait on
   std::vector<int32_t> wait_d, wait_r;
   std::vector<cudaEvent_t> ev_d, ev_r;  // after the dense / truncation launches of a level (needed ones only)
+  // sharded mode (owner computes over a communicator): exchange groups after levels
+  hlu_comm *comm = nullptr;
+  const hlu_xfer *d_xfer = nullptr;
+  std::vector<XGroup> xgroups;
+  double *staging = nullptr;
+  int64_t nlevels = 0, nlog = 0;
 };
 
 __global__ void k_stamp(unsigned long long *slot) {
@@ -48,8 +66,12 @@ static int launch_one(hlu_schedule *s, const hlu_launch &L, int &slot, cudaStrea
     case HLU_K_TRSM: return hlu_trsm_batched_f64(&s->ctx, s->trsm + L.first, L.count, L.smem_dim, st);
     case HLU_K_GEMM: return hlu_gemm_batched_f64(&s->ctx, s->gemm + L.first, s->terms, L.count, st);
     case HLU_K_GEMM_SMALL: return hlu_gemm_small_batched_f64(&s->ctx, s->gemm + L.first, s->terms, L.count, st);
-    case HLU_K_RKT32:
-      return hlu_rkt_phases(&s->ctx, s->rkt, s->parts, L.first, L.count, &s->scratch, slot++, st, &s->aux);
+    case HLU_K_RKT32: {
+      hlu_rkt_set_wide_hint((L.smem_dim & 2) != 0);
+      const int rc = hlu_rkt_phases(&s->ctx, s->rkt, s->parts, L.first, L.count, &s->scratch, slot++, st, &s->aux);
+      hlu_rkt_set_wide_hint(1);
+      return rc;
+    }
     case HLU_K_RKT64: return 0;
     default: return -3;
   }
@@ -124,7 +146,53 @@ static int run_chains(hlu_schedule *s, cudaStream_t st) {
   return 0;
 }
 
+static int run_launches(hlu_schedule *s, cudaStream_t st);
+
+// Sharded: this rank's launches level by level (a level that also truncates
+// runs its dense launches on the side stream, as run_launches), then the
+// level's exchange groups; after the last level the final gather and the
+// reduction of the flop logs / error words.
+static int run_sharded(hlu_schedule *s, cudaStream_t st) {
+  const size_t nl = s->launches.size();
+  if (s->nrkt) cudaMemsetAsync(s->scratch.counts, 0, 8 * sizeof(int32_t) * s->nrkt, st);
+  int slot = 0;
+  size_t i = 0, g = 0;
+  for (int64_t lv = 0; lv <= s->nlevels; ++lv) {
+    size_t j = i;
+    bool rk = false, dn = false, dep = false;
+    while (j < nl && s->launches[j].level == lv) {
+      (s->launches[j].kind == HLU_K_RKT32 ? rk : dn) = true;
+      dep = dep || (s->launches[j].kind == HLU_K_RKT32 && (s->launches[j].smem_dim & 1));
+      ++j;
+    }
+    const bool split = rk && dn && !dep;
+    if (split) {
+      cudaEventRecord(s->fork, st);
+      cudaStreamWaitEvent(s->dense, s->fork, 0);
+    }
+    for (size_t k = i; k < j; ++k) {
+      const hlu_launch &L = s->launches[k];
+      const int rc = launch_one(s, L, slot, (split && L.kind != HLU_K_RKT32) ? s->dense : st);
+      if (rc != 0) return rc;
+    }
+    if (split) {
+      cudaEventRecord(s->join, s->dense);
+      cudaStreamWaitEvent(st, s->join, 0);
+    }
+    i = j;
+    for (; g < s->xgroups.size() && s->xgroups[g].level == lv; ++g) {
+      const XGroup &x = s->xgroups[g];
+      const int rc = hlu_xfer_group(s->comm, s->ctx.pool, s->ctx.ranks, (const void *)(s->d_xfer + x.first),
+                                    (int)x.n, x.src, x.count, s->staging, st);
+      if (rc != 0) return rc;
+    }
+  }
+  if (i != nl || g != s->xgroups.size()) return -17;  // launches / exchanges beyond nlevels
+  return hlu_comm_reduce_logs(s->comm, s->ctx.log, s->nlog, s->ctx.err, st);
+}
+
 static int run_launches(hlu_schedule *s, cudaStream_t st) {
+  if (s->comm) return run_sharded(s, st);
   if (!s->wait_d.empty() && !s->stamps) return run_chains(s, st);
   const size_t nl = s->launches.size();
   if (s->stamps) k_stamp<<<1, 1, 0, st>>>(s->stamps);
@@ -137,7 +205,7 @@ static int run_launches(hlu_schedule *s, cudaStream_t st) {
     bool dep = false;
     while (j < nl && s->launches[j].level == s->launches[i].level) {
       (s->launches[j].kind == HLU_K_RKT32 ? rk : dn) = true;
-      dep = dep || (s->launches[j].kind == HLU_K_RKT32 && s->launches[j].smem_dim != 0);
+      dep = dep || (s->launches[j].kind == HLU_K_RKT32 && (s->launches[j].smem_dim & 1));
       ++j;
     }
     const bool split = rk && dn && !dep && !s->stamps;
@@ -179,13 +247,82 @@ static void destroy_events(hlu_schedule *s) {
   s->ev_r.clear();
 }
 
+struct ShardArgs {
+  hlu_comm *comm;
+  const hlu_xfer *xfer_host, *xfer_dev;
+  int64_t nxfer, nlevels, nlog;
+  double *staging;
+};
+
+static int create(hlu_schedule **out, const hlu_ctx *ctx, const hlu_launch *launches, int64_t nlaunch,
+                  const hlu_getrf_desc *getrf, const hlu_trsm_desc *trsm, const hlu_gemm_desc *gemm,
+                  const hlu_term *terms, hlu_rkt_desc *rkt, const hlu_rkpart *parts, const hlu_rkt_scratch *scratch,
+                  const int32_t *wait_dense, const int32_t *wait_rkt, int64_t nlevels, int use_graph, void *stream,
+                  const ShardArgs *sh);
+
 extern "C" int hlu_schedule_create_chains(hlu_schedule **out, const hlu_ctx *ctx, const hlu_launch *launches,
                                           int64_t nlaunch, const hlu_getrf_desc *getrf, const hlu_trsm_desc *trsm,
                                           const hlu_gemm_desc *gemm, const hlu_term *terms, hlu_rkt_desc *rkt,
                                           const hlu_rkpart *parts, const hlu_rkt_scratch *scratch,
                                           const int32_t *wait_dense, const int32_t *wait_rkt, int64_t nlevels,
                                           int use_graph, void *stream) {
+  return create(out, ctx, launches, nlaunch, getrf, trsm, gemm, terms, rkt, parts, scratch, wait_dense, wait_rkt,
+                nlevels, use_graph, stream, nullptr);
+}
+
+extern "C" int hlu_schedule_create_sharded(hlu_schedule **out, const hlu_ctx *ctx, const hlu_launch *launches,
+                                           int64_t nlaunch, const hlu_getrf_desc *getrf, const hlu_trsm_desc *trsm,
+                                           const hlu_gemm_desc *gemm, const hlu_term *terms, hlu_rkt_desc *rkt,
+                                           const hlu_rkpart *parts, const hlu_rkt_scratch *scratch, hlu_comm *comm,
+                                           const void *xfer_host, const void *xfer_dev, int64_t nxfer,
+                                           int64_t nlevels, int64_t nlog, double *staging, int use_graph,
+                                           void *stream) {
+  if (!comm) return -18;
+  const ShardArgs sh{comm, (const hlu_xfer *)xfer_host, (const hlu_xfer *)xfer_dev, nxfer, nlevels, nlog, staging};
+  return create(out, ctx, launches, nlaunch, getrf, trsm, gemm, terms, rkt, parts, scratch, nullptr, nullptr, 0,
+                use_graph, stream, &sh);
+}
+
+// staging doubles the exchange groups of a sharded plan need (the largest group)
+extern "C" int64_t hlu_xfer_staging_doubles(const void *xfer, int64_t n) {
+  const hlu_xfer *x = (const hlu_xfer *)xfer;
+  int64_t best = 0;
+  for (int64_t i = 0; i < n; ++i) best = std::max<int64_t>(best, x[i].boff + x[i].len + 1);
+  return best;
+}
+
+static int create(hlu_schedule **out, const hlu_ctx *ctx, const hlu_launch *launches, int64_t nlaunch,
+                  const hlu_getrf_desc *getrf, const hlu_trsm_desc *trsm, const hlu_gemm_desc *gemm,
+                  const hlu_term *terms, hlu_rkt_desc *rkt, const hlu_rkpart *parts, const hlu_rkt_scratch *scratch,
+                  const int32_t *wait_dense, const int32_t *wait_rkt, int64_t nlevels, int use_graph, void *stream,
+                  const ShardArgs *sh) {
   hlu_schedule *s = new hlu_schedule();
+  if (sh) {
+    s->comm = sh->comm;
+    s->d_xfer = sh->xfer_dev;
+    s->staging = sh->staging;
+    s->nlevels = sh->nlevels;
+    s->nlog = sh->nlog;
+    for (int64_t i = 0; i < sh->nxfer; ++i) {
+      const hlu_xfer &r = sh->xfer_host[i];
+      if (s->xgroups.empty() || s->xgroups.back().level != r.level || s->xgroups.back().src != r.src ||
+          r.boff == 0) {
+        if (!s->xgroups.empty() && (r.level < s->xgroups.back().level)) {
+          delete s;
+          return -19;  // records out of level order
+        }
+        s->xgroups.push_back(XGroup{r.level, r.src, i, 0, 0});
+      }
+      XGroup &g = s->xgroups.back();
+      ++g.n;
+      g.count = std::max<int64_t>(g.count, r.boff + r.len + 1);
+    }
+    for (int64_t i = 0; i < nlaunch; ++i)
+      if (i > 0 && launches[i].level < launches[i - 1].level) {
+        delete s;
+        return -19;
+      }
+  }
   if (wait_dense && wait_rkt && nlevels > 0) {
     for (int64_t i = 0; i < nlaunch; ++i)
       if (launches[i].level < 0 || launches[i].level >= nlevels) {

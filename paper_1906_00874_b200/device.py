@@ -47,7 +47,7 @@ def _dev_bytes(torch, arr, device):
 class DeviceCall:
     """One planned H-arithmetic call resident on the GPU."""
 
-    def __init__(self, layout, packed, ctl, device=None, use_graph=True, extras=None):
+    def __init__(self, layout, packed, ctl, device=None, use_graph=True, extras=None, comm=None):
         torch = _torch()
         self.torch = torch
         self.device = torch.device(device if device is not None else "cuda")
@@ -89,22 +89,43 @@ class DeviceCall:
             )
             handle = ctypes.c_void_p()
             launches = np.ascontiguousarray(p.launches)
-            # two chains (dense / truncation) with the planner's cross-chain
-            # waits; HLU_CHAINS=0 keeps a barrier after every level
-            chains = p.wait_dense is not None and os.environ.get("HLU_CHAINS", "1") != "0"
-            self.chains = chains
-            wd = np.ascontiguousarray(p.wait_dense) if chains else None
-            wr = np.ascontiguousarray(p.wait_rkt) if chains else None
-            rc = lib.hlu_schedule_create_chains(
-                ctypes.byref(handle), ctypes.byref(self.ctx), launches.ctypes.data, len(launches),
-                self.d_getrf.data_ptr(), self.d_trsm.data_ptr(), self.d_gemm.data_ptr(),
-                self.d_terms.data_ptr(), self.d_rkt.data_ptr(), self.d_parts.data_ptr(),
-                ctypes.byref(self.scratch),
-                wd.ctypes.data if chains else None, wr.ctypes.data if chains else None,
-                int(p.nlevels) if chains else 0,
-                1 if use_graph else 0, ctypes.c_void_p(self.stream.cuda_stream),
-            )
-            _native.check(rc, "hlu_schedule_create")
+            self.comm = comm
+            if p.shard is not None:
+                # owner computes over the communicator: this rank's launches, the
+                # slot exchanges after every level, the final gather
+                if comm is None:
+                    raise ValueError("a sharded plan needs a communicator (multigpu.Communicator)")
+                self.chains = False
+                xfer = np.ascontiguousarray(p.xfer)
+                self.d_xfer = _dev_bytes(torch, xfer, self.device)
+                nst = max(int(lib.hlu_xfer_staging_doubles(xfer.ctypes.data, len(xfer))), 1)
+                self.staging = torch.empty(nst, dtype=torch.float64, device=self.device)
+                rc = lib.hlu_schedule_create_sharded(
+                    ctypes.byref(handle), ctypes.byref(self.ctx), launches.ctypes.data, len(launches),
+                    self.d_getrf.data_ptr(), self.d_trsm.data_ptr(), self.d_gemm.data_ptr(),
+                    self.d_terms.data_ptr(), self.d_rkt.data_ptr(), self.d_parts.data_ptr(),
+                    ctypes.byref(self.scratch), comm.handle, xfer.ctypes.data, self.d_xfer.data_ptr(),
+                    len(xfer), int(p.nlevels), int(p.nlog), self.staging.data_ptr(),
+                    1 if use_graph else 0, ctypes.c_void_p(self.stream.cuda_stream),
+                )
+                _native.check(rc, "hlu_schedule_create_sharded")
+            else:
+                # two chains (dense / truncation) with the planner's cross-chain
+                # waits; HLU_CHAINS=0 keeps a barrier after every level
+                chains = p.wait_dense is not None and os.environ.get("HLU_CHAINS", "1") != "0"
+                self.chains = chains
+                wd = np.ascontiguousarray(p.wait_dense) if chains else None
+                wr = np.ascontiguousarray(p.wait_rkt) if chains else None
+                rc = lib.hlu_schedule_create_chains(
+                    ctypes.byref(handle), ctypes.byref(self.ctx), launches.ctypes.data, len(launches),
+                    self.d_getrf.data_ptr(), self.d_trsm.data_ptr(), self.d_gemm.data_ptr(),
+                    self.d_terms.data_ptr(), self.d_rkt.data_ptr(), self.d_parts.data_ptr(),
+                    ctypes.byref(self.scratch),
+                    wd.ctypes.data if chains else None, wr.ctypes.data if chains else None,
+                    int(p.nlevels) if chains else 0,
+                    1 if use_graph else 0, ctypes.c_void_p(self.stream.cuda_stream),
+                )
+                _native.check(rc, "hlu_schedule_create")
             self.handle = handle
         self.nkernels = int(p.launches["count"].astype(bool).sum()) if len(p.launches) else 0
 

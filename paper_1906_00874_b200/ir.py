@@ -29,7 +29,10 @@ LAUNCH = np.dtype([("kind", "<i4"), ("count", "<i4"), ("first", "<i8"), ("smem_d
 
 assert VIEW.itemsize == 32 and GETRF.itemsize == 40 and TRSM.itemsize == 72
 assert TERM.itemsize == 144 and GEMM.itemsize == 16 and RKPART.itemsize == 80
-assert RKT.itemsize == 64 and LAUNCH.itemsize == 24 and RKT_ITEM.itemsize == 8
+# slot exchange record of a sharded plan (include/hlu_plan.h hlu_xfer)
+XFER = np.dtype([("level", "<i4"), ("src", "<i4"), ("group", "<i4"), ("rank_slot", "<i4"), ("off", "<i8"),
+                 ("len", "<i8"), ("boff", "<i8")])
+assert RKT.itemsize == 64 and LAUNCH.itemsize == 24 and RKT_ITEM.itemsize == 8 and XFER.itemsize == 40
 
 # kinds (hlu_b200.h)
 K_GETRF, K_TRSM, K_GEMM, K_RKT32, K_RKT64, K_GEMM_SMALL = 0, 1, 2, 3, 4, 5
@@ -110,6 +113,9 @@ def rk_side_total(M, K):
     return off_Z + srows * K
 
 
+RK_KMAXW = 128  # stacked rank of the wide truncation path (csrc/rk_layout.h)
+
+
 def rkt_ws_doubles(m, n, kbound):
     """Mirror of hlu_rkt_ws_doubles / rk_ws_doubles (csrc/rk_layout.h)."""
     if m <= 0 or n <= 0 or kbound <= 0:
@@ -120,6 +126,9 @@ def rkt_ws_doubles(m, n, kbound):
         if K < kb and rk_ch(K + 1, RK_BUFA) == rk_ch(K, RK_BUFA) and rk_chc(K + 1) == rk_chc(K):
             continue
         best = max(best, rk_side_total(m, K) + rk_side_total(n, K))
+    if kbound > RK_KMAX:
+        kw = min(kbound, RK_KMAXW)
+        best = max(best, (m + n) * kw + 2 * RK_KMAXW * RK_KMAXW + 3 * RK_KMAXW)
     return best
 
 

@@ -14,7 +14,15 @@
   list is static, computed here from the plan.
 
 ``run_level_exchange`` drives any per-rank executor with a
-``torch.distributed`` process group (gloo on CPU in the tests; NCCL on GPUs).
+``torch.distributed`` process group (the readable specification, gloo on CPU
+in the tests).
+
+The production path is native: ``native_plan.plan(..., shard=(owner, N, r))``
+(``hlu_plan_build_sharded``) emits rank r's launches and the exchange records;
+``Communicator`` + ``DeviceCall(..., comm=)`` replay them as one CUDA graph in
+which every exchange group is a gather kernel, one ``ncclBroadcast`` over
+NVLink and a scatter kernel (``csrc/comm.cu``); ``factorize_sharded`` is the
+H-LU entry point on N GPUs (one process per GPU).
 """
 
 from __future__ import annotations
@@ -172,3 +180,62 @@ def _ship(dist, rank, src, dst, off, ln, lf, L, pool, ranks_arr, buf):
         pool[off:off + ln] = t.numpy()[:ln]
         if lf.kind != DENSE:
             ranks_arr[L.rk[id(lf)][2]] = int(t.numpy()[ln])
+
+
+class Communicator:
+    """NCCL communicator of the sharded H-LU (csrc/comm.cu), one per process /
+    GPU.  The unique id travels over an existing torch.distributed group."""
+
+    def __init__(self, dist, rank, world, device):
+        import ctypes
+
+        import torch
+
+        from . import _native
+
+        self.lib = _native.lib()
+        if not self.lib.hlu_comm_available():
+            raise RuntimeError("libnccl.so.2 could not be loaded")
+        self.rank, self.world = rank, world
+        buf = (ctypes.c_char * 128)()
+        if rank == 0:
+            _native.check(0 if self.lib.hlu_comm_unique_id(buf) > 0 else -1, "hlu_comm_unique_id")
+        if world > 1:
+            obj = [bytes(buf)]
+            dist.broadcast_object_list(obj, src=0)
+            buf = (ctypes.c_char * 128).from_buffer_copy(obj[0])
+        self.handle = ctypes.c_void_p()
+        with torch.cuda.device(device):
+            _native.check(self.lib.hlu_comm_init(ctypes.byref(self.handle), buf, world, rank), "hlu_comm_init")
+
+    def close(self):
+        if self.handle:
+            self.lib.hlu_comm_destroy(self.handle)
+            self.handle = None
+
+
+def shard_plan(h, nranks, rank, capacity, blocks_per_rank=4):
+    """Layout, slot owners and this rank's sharded native plan for H-LU of h."""
+    from . import native_plan
+    from .planner import Layout
+
+    layout = Layout([h], cap=capacity)
+    owner = owner_map(layout, nranks, blocks_per_rank=blocks_per_rank)
+    packed, _ = native_plan.plan(layout, [("factor", h)], shard=(owner, nranks, rank))
+    return layout, owner, packed
+
+
+def factorize_sharded(h, ctl, comm, device, capacity=None, use_graph=True):
+    """H-LU of h over comm.world GPUs (owner computes, NCCL exchanges); every
+    rank ends with the whole factorization, which is installed in h.  Returns
+    the DeviceCall (flops() gives the reference effective-flop count)."""
+    from .device import DeviceCall
+    from .hlu import _auto_capacity
+
+    cap = _auto_capacity([h], ctl) if capacity is None else int(capacity)
+    layout, _, packed = shard_plan(h, comm.world, comm.rank, cap)
+    call = DeviceCall(layout, packed, ctl, device=device, use_graph=use_graph, comm=comm)
+    call.launch()
+    call.check_errors()
+    call.download()
+    return call

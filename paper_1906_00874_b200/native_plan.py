@@ -53,6 +53,13 @@ def lib():
         L.hlu_plan_free.argtypes = [vp]
         L.hlu_plan_level_waits.argtypes = [vp, vp, vp]
         L.hlu_plan_level_waits.restype = ctypes.c_int
+        L.hlu_plan_build_sharded.argtypes = [ctypes.POINTER(vp), vp, i64, vp, i64, i32, i64, i64, i32, i64, i32,
+                                             vp, i32, i32]
+        L.hlu_plan_build_sharded.restype = ctypes.c_int
+        L.hlu_plan_xfer.argtypes = [vp, vp]
+        L.hlu_plan_xfer.restype = i64
+        L.hlu_plan_op_owners.argtypes = [vp, vp]
+        L.hlu_plan_op_owners.restype = ctypes.c_int
         L.hlu_host_pack.argtypes = [vp, i64, vp, ctypes.c_int]
         L.hlu_host_unpack.argtypes = [vp, i64, vp, ctypes.c_int]
         _lib = L
@@ -175,7 +182,7 @@ def load_packed(path):
         return Packed(**kw), int(z["nops"])
 
 
-def plan(layout, commands, split_rows=SPLIT_ROWS, cache_dir=None):
+def plan(layout, commands, split_rows=SPLIT_ROWS, cache_dir=None, shard=None):
     """commands: list of (kind, nodes..., extras) in the planner's terms:
     ("factor", h) | ("solve_lower", l, b) | ("solve_upper", b, u) |
     ("update", c, a, b) | ("fwd", h, name) | ("bwd", h, name) |
@@ -204,6 +211,8 @@ def plan(layout, commands, split_rows=SPLIT_ROWS, cache_dir=None):
             cmds[i] = (_MATVEC_CMDS[kind], index[id(c[1])], 0, 0, xo, cols, 0, xr, yo, yr)
         else:
             raise ValueError(kind)
+    if shard is not None:  # (slot_owner, nranks, rank): per-rank plans are not cached
+        return _build(layout, nodes, cmds, split_rows, shard)
     explicit = cache_dir is not None
     cache_dir = cache_dir if explicit else cache_dir_default()
     path = None
@@ -220,12 +229,22 @@ def plan(layout, commands, split_rows=SPLIT_ROWS, cache_dir=None):
     return packed, nops
 
 
-def _build(layout, nodes, cmds, split_rows):
+def _build(layout, nodes, cmds, split_rows, shard=None):
     L = lib()
     h = ctypes.c_void_p()
-    rc = L.hlu_plan_build(ctypes.byref(h), nodes.ctypes.data, len(nodes), cmds.ctypes.data, len(cmds),
-                          layout.cap, layout.ident_off, layout.nslots, layout.nrk, layout.payload_doubles,
-                          int(split_rows))
+    if shard is None:
+        rc = L.hlu_plan_build(ctypes.byref(h), nodes.ctypes.data, len(nodes), cmds.ctypes.data, len(cmds),
+                              layout.cap, layout.ident_off, layout.nslots, layout.nrk, layout.payload_doubles,
+                              int(split_rows))
+    else:
+        owner, nranks, rank = shard
+        owner = np.ascontiguousarray(owner, dtype=np.int32)
+        if owner.shape != (layout.nslots,):
+            raise ValueError("slot owner map must cover every skeleton slot")
+        rc = L.hlu_plan_build_sharded(ctypes.byref(h), nodes.ctypes.data, len(nodes), cmds.ctypes.data, len(cmds),
+                                      layout.cap, layout.ident_off, layout.nslots, layout.nrk,
+                                      layout.payload_doubles, int(split_rows), owner.ctypes.data, int(nranks),
+                                      int(rank))
     try:
         if rc != 0:
             from .hmatrix import StructureError
@@ -254,6 +273,14 @@ def _build(layout, nodes, cmds, split_rows):
         wr = np.full(max(nlev, 1), -1, dtype=np.int32)
         if L.hlu_plan_level_waits(h, wd.ctypes.data, wr.ctypes.data) != 0:
             wd = wr = None
+        xfer = mask = None
+        if shard is not None:
+            xfer = np.zeros(max(int(L.hlu_plan_xfer(h, None)), 1), dtype=ir.XFER)
+            nx = int(L.hlu_plan_xfer(h, xfer.ctypes.data))
+            xfer = xfer[:nx]
+            mask = np.zeros(nops, dtype=np.uint64)
+            L.hlu_plan_op_owners(h, mask.ctypes.data)
+            wd = wr = None  # level barriers: the exchange steps sit between levels
     finally:
         L.hlu_plan_free(h)
     labels = []
@@ -265,5 +292,6 @@ def _build(layout, nodes, cmds, split_rows):
         launches=launches, nlevels=nlev, arena_doubles=arena,
         flop_formula=ff.astype(np.int64), flop_coef=fc, flop_log=fl, nlog=max(nlog, 1),
         nranks=max(nrank, 1), lu_op_ids=lu_ops[:nlu], lu_labels=labels, op_levels=lv,
-        wait_dense=wd, wait_rkt=wr,
+        wait_dense=wd, wait_rkt=wr, xfer=xfer, op_mask=mask,
+        shard=None if shard is None else (int(shard[1]), int(shard[2])),
     ), nops

@@ -40,8 +40,8 @@ from .ir import (
 
 TEMP_SHIFT = 36  # virtual address of temp t: (t + 1) << TEMP_SHIFT (2^27 temps, 2^36-double offsets)
 DEFAULT_CAP = 32
-IDENT = 64     # identity block edge kept in the pool
-KMAX_STACK = 64  # largest stacked rank the truncation kernel handles
+IDENT = 128    # identity block edge kept in the pool (= ir.RK_KMAXW)
+KMAX_STACK = 128  # widest factor pair a truncation takes (the wide path, ir.RK_KMAXW)
 MAX_CAP = 64     # largest per-block Rk capacity (= the stacked-rank limit of the kernels)
 
 

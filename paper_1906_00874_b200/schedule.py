@@ -145,6 +145,11 @@ class Packed:
     # other chain the dense / truncation launches wait for; None = level barriers
     wait_dense: np.ndarray = None
     wait_rkt: np.ndarray = None
+    # owner-computes sharding (native planner, nranks > 1): this rank's slot
+    # exchange records (ir.XFER) and per-op rank masks; None on one GPU
+    xfer: np.ndarray = None
+    op_mask: np.ndarray = None
+    shard: tuple = None  # (nranks, rank)
 
 
 def _view_rec(v):
@@ -218,7 +223,7 @@ def pack(pl: Planner, arena_base: int):
     out = []
     for kind, count, first, dim, lv, dep in launches:
         if kind == ir.K_RKT32:
-            out.append((ir.K_RKT32, count, first, int(dep), lv))
+            out.append((ir.K_RKT32, count, first, int(dep) | (2 if dim > ir.RK_KMAX else 0), lv))
         else:
             out.append((kind, count, first, dim, lv))
 

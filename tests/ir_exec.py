@@ -147,8 +147,8 @@ class CpuMachine:
             k = min(k, self.kmax)
         finish(qa @ (u[:, :k] * sv[:k]), qb @ vt[:k].T, k)
 
-    def run(self, packed):
-        for L in packed.launches:
+    def run(self, packed, launches=None):
+        for L in packed.launches if launches is None else launches:
             kind, count, first = int(L["kind"]), int(L["count"]), int(L["first"])
             if count == 0:
                 continue
@@ -165,3 +165,52 @@ class CpuMachine:
             elif kind == ir.K_RKT32:  # RKT64 launches cover the same ops
                 for i in rng:
                     self.rkt(packed.rkt[i], packed.parts)
+
+
+def xfer_groups(xfer):
+    """(level, src, group) -> record indices, in record order."""
+    out = {}
+    for i, r in enumerate(xfer):
+        out.setdefault((int(r["level"]), int(r["src"]), int(r["group"])), []).append(i)
+    return out
+
+
+def run_sharded(M, packed, rank, dist):
+    """The sharded schedule exactly as the GPU runtime replays it
+    (runtime.cu, hlu_schedule_create_sharded): every level's launches of this
+    rank, then the level's exchange groups in order -- the source packs the
+    slots (payload, then the rank as a double) into the group buffer, one
+    broadcast, the other ranks unpack -- and after the last level the final
+    gather; the flop log is max-reduced."""
+    import torch
+
+    lv = packed.launches["level"].astype(np.int64)
+    groups = xfer_groups(packed.xfer)
+    by_level = {}
+    for key, idx in groups.items():
+        by_level.setdefault(key[0], []).append((key, idx))
+    for level in range(packed.nlevels + 1):
+        if level < packed.nlevels:
+            M.run(packed, packed.launches[lv == level])
+        for (lvl, src, g), idx in sorted(by_level.get(level, []), key=lambda kv: kv[0]):
+            recs = packed.xfer[idx]
+            size = int((recs["len"] + 1).sum())
+            buf = np.zeros(size)
+            if rank == src:
+                for r in recs:
+                    o, n, b = int(r["off"]), int(r["len"]), int(r["boff"])
+                    buf[b : b + n] = M.pool[o : o + n]
+                    if int(r["rank_slot"]) >= 0:
+                        buf[b + n] = M.ranks[int(r["rank_slot"])]
+            t = torch.from_numpy(buf)
+            dist.broadcast(t, src)
+            if rank != src:
+                buf = t.numpy()
+                for r in recs:
+                    o, n, b = int(r["off"]), int(r["len"]), int(r["boff"])
+                    M.pool[o : o + n] = buf[b : b + n]
+                    if int(r["rank_slot"]) >= 0:
+                        M.ranks[int(r["rank_slot"])] = int(buf[b + n])
+    log = torch.from_numpy(M.log.astype(np.int64))
+    dist.all_reduce(log, op=dist.ReduceOp.MAX)
+    M.log[:] = log.numpy().astype(np.int32)

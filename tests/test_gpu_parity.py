@@ -103,6 +103,31 @@ def test_add_truncated_eps0(rng, m, n, k1, k2, kmax):
         assert _spec(got.value() - want.value()) <= 1e-10 * _spec(exact)
 
 
+@pytest.mark.parametrize("m,n,ks,eps,kmax", [(200, 150, (40, 40), 1e-8, None), (300, 260, (50, 30, 20), 1e-6, None),
+                                             (128, 128, (64, 64), 1e-10, 48), (700, 90, (70, 58), 1e-12, None)])
+def test_wide_truncation_vs_oracle(rng, m, n, ks, eps, kmax):
+    """Stacked ranks 64 < K <= 128 (the wide path): merges of several kmax-wide
+    parts and adds of two capacity-64 factors, against the oracle's recompress
+    / add_truncated (QR of the stacked factors + SVD of the core,
+    lowrank.py:137-168): identical ranks, values to rounding."""
+    ctl = TruncationControl(eps, kmax)
+    # a decaying spectrum so the truncation really cuts inside K
+    parts = []
+    for k in ks:
+        a = rng.standard_normal((m, k)) * (0.7 ** np.arange(k))
+        parts.append(LowRank(a, rng.standard_normal((n, k))))
+    if len(parts) == 2:
+        want = orc.add_truncated(parts[0], parts[1], ctl)
+        got = device_ops.add_truncated(parts[0], parts[1], ctl)
+    else:
+        x = LowRank(np.hstack([p.a for p in parts]), np.hstack([p.b for p in parts]))
+        want = orc.recompress(x, ctl)
+        got = device_ops.recompress(x, ctl)
+    assert got.k == want.k
+    exact = sum(p.value() for p in parts)
+    assert _spec(got.value() - want.value()) <= max(1e-10 * _spec(exact), 4 * eps * _spec(exact))
+
+
 def test_add_truncated_parallel_outer(rng):
     a = rng.standard_normal((8, 1))
     b = rng.standard_normal((5, 1))
@@ -277,3 +302,27 @@ def test_multi_column_solve_matches_columnwise():
     for j in range(3):
         xj = hlu_solve(h, B[:, j])
         assert np.linalg.norm(X[:, j] - xj) <= 1e-13 * np.linalg.norm(xj)
+
+
+def test_sharded_runtime_one_gpu():
+    """The multi-GPU machinery on one GPU: a sharded native plan (every op on
+    rank 0, the final-gather exchange groups), an NCCL communicator of one
+    rank, the sharded schedule (gather kernel -> ncclBroadcast -> scatter)
+    captured in the graph.  Ranks and the flop counter match the reference
+    fixture and the solve matches the single-GPU path."""
+    from paper_1906_00874_b200 import multigpu
+
+    g = cases.golden("sphere_1024")
+    build, ctl = cases.CASES["sphere_1024"]
+    h, _ = build()
+    comm = multigpu.Communicator(None, 0, 1, "cuda:0")
+    try:
+        call = multigpu.factorize_sharded(h, TruncationControl(*ctl), comm, "cuda:0")
+        assert len(call.packed.xfer) > 0
+        assert np.array_equal(cases.ranks(h), g["ranks_out"])
+        assert abs(call.flops() - float(g["flops"])) <= 1e-12 * float(g["flops"])
+        call.close()
+    finally:
+        comm.close()
+    y = forward_solve(h, g["rhs"])
+    assert np.linalg.norm(y - g["y_forward"]) <= 1e-8 * np.linalg.norm(g["y_forward"])

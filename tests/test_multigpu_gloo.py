@@ -102,3 +102,81 @@ def test_owner_map_balance_and_volume():
     for i, op in enumerate(pl.ops):
         for t in op.temps_in:
             assert owner[i] <= prod[t]
+
+
+# ---- the native sharded planner (hlu_plan_build_sharded) -------------------------
+
+
+def _native_worker(rank, world, name, port, out):
+    import torch.distributed as dist
+
+    from ir_exec import run_sharded
+    from paper_1906_00874_b200 import native_plan
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    build, ctl = cases.CASES[name]
+    h, _ = build()
+    L = Layout(h, cap=32)
+    owner = multigpu.owner_map(L, world)
+    p, _ = native_plan.plan(L, [("factor", h)], shard=(owner, world, rank))
+    M = _machine(L, p, ctl)
+    run_sharded(M, p, rank, dist)
+    np.save(f"{out}_{rank}_pool.npy", M.pool[: L.payload_doubles])
+    np.save(f"{out}_{rank}_ranks.npy", M.ranks[: L.nrk])
+    np.save(f"{out}_{rank}_log.npy", M.log)
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("name,world", [("mixed_192", 2), ("sphere_1024", 2), ("sphere_1024", 3)])
+def test_native_sharded_plan_matches_single(tmp_path, name, world):
+    """Every rank executes only its own ops from the native sharded plan, the
+    exchange records move the written slots after each level, and after the
+    final gather EVERY rank holds the single-GPU result bit for bit (payloads,
+    ranks and the flop log)."""
+    from paper_1906_00874_b200 import native_plan
+
+    build, ctl = cases.CASES[name]
+    h, _ = build()
+    L = Layout(h, cap=32)
+    p, _ = native_plan.plan(L, [("factor", h)])
+    ref = _machine(L, p, ctl)
+    ref.run(p)
+    port = 29700 + (os.getpid() % 200) + 7 * world
+    out = str(tmp_path / "r")
+    mp.start_processes(_native_worker, args=(world, name, port, out), nprocs=world, join=True, start_method="fork")
+    for r in range(world):
+        assert np.array_equal(np.load(f"{out}_{r}_ranks.npy"), ref.ranks[: L.nrk])
+        assert np.array_equal(np.load(f"{out}_{r}_pool.npy"), ref.pool[: L.payload_doubles])
+        assert np.array_equal(np.load(f"{out}_{r}_log.npy"), ref.log)
+
+
+def test_native_sharded_ops_partition():
+    """The ranks' op sets cover every op; slot writers are unique; temp
+    producers sit on every consuming rank; the exchange records never ship a
+    slot from a rank that does not own it."""
+    from paper_1906_00874_b200 import native_plan
+
+    build, _ = cases.CASES["sphere_1024"]
+    h, _ = build()
+    L = Layout(h, cap=32)
+    world = 4
+    owner = multigpu.owner_map(L, world)
+    full, nops = native_plan.plan(L, [("factor", h)])
+    per = [native_plan.plan(L, [("factor", h)], shard=(owner, world, r))[0] for r in range(world)]
+    mask = per[0].op_mask
+    assert all(np.array_equal(q.op_mask, mask) for q in per)
+    assert np.all(mask != 0)
+    counts = [int(((mask >> np.uint64(r)) & np.uint64(1)).sum()) for r in range(world)]
+    assert min(counts) > 0 and max(counts) / np.mean(counts) < 2.0
+    ndesc = sum(len(q.rkt) + len(q.getrf) + len(q.trsm) for q in per)
+    assert ndesc >= len(full.rkt) + len(full.getrf) + len(full.trsm)
+    for q in per:
+        x = q.xfer
+        assert np.array_equal(x, per[0].xfer)
+        slots = {}
+        for lf_i, lf in enumerate(L.leaves):
+            slots[multigpu.slot_region(L, lf_i)[0]] = lf_i
+        for r in x:
+            assert owner[slots[int(r["off"])]] == int(r["src"])
