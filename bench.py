@@ -38,6 +38,11 @@ CONFIGS = {
     "cfg1": (3, 4096, 2.0, 32, 0.0, 8, 1e-6, None),
     "cfg2": (3, 32768, 2.0, 64, 1e-6, 32, 1e-6, 32),
     "cfg3": (3, 131072, 2.0, 64, 1e-4, None, 1e-4, None),
+    # cfg4 geometry at the size one GPU holds (the full n=524288 needs the 8-GPU sharded path)
+    "cfg4p": (3, 131072, 2.0, 128, 1e-4, 48, 1e-4, 48),
+    # HODLR on the unit circle, rank-32 off-diagonal blocks (GPU cross approximation + truncation)
+    "cfg5": (2, 1048576, None, 256, 0.0, 32, 1e-10, 32),
+    "cfg5s": (2, 131072, None, 256, 0.0, 32, 1e-10, 32),
 }
 DEFAULT_CONFIG = os.environ.get("HLU_BENCH_CONFIG", "cfg3")  # BASELINE metric config (n=131072)
 
@@ -101,6 +106,11 @@ def build_case(cfg):
     from paper_1906_00874_b200 import make_bem_case
 
     d, n, eta, leaf, eps, kmax, _, _ = CONFIGS[cfg]
+    if eta is None:  # HODLR (cfg5): GPU generator
+        from paper_1906_00874_b200 import gpu_assembly
+
+        return gpu_assembly.hodlr_case(n, leafsize=leaf, k=kmax, generator="aca",
+                                       device=f"cuda:{os.environ.get('LOCAL_RANK', '0')}")[0]
     workers = int(os.environ.get("HLU_ASSEMBLY_WORKERS", str(os.cpu_count() or 1)))
     return make_bem_case(d, n, eta, leafsize=leaf, eps=eps, kmax=kmax, workers=workers).hmatrix
 
@@ -137,6 +147,117 @@ def time_rkt_launches(call, torch):
     return [float(t) for t, k in zip(dt, kinds) if int(k) == ir.K_RKT32], float(dt.sum())
 
 
+def run_sharded(args, world, rank, local, dev, dist):
+    """One H-LU factorization on WORLD_SIZE GPUs (one process each): owner
+    computes over a 2-D block-cyclic slot map, the native sharded plan per
+    rank, slot exchanges as gather -> ncclBroadcast -> scatter inside each
+    rank's CUDA graph, final gather (every rank ends with the whole factor).
+    Timed on the device with CUDA events, max over ranks; total work is fixed
+    as N grows (strong scaling)."""
+    import numpy as np
+    import torch
+
+    from paper_1906_00874_b200 import TruncationControl, multigpu
+    from paper_1906_00874_b200.device import DeviceCall
+    from paper_1906_00874_b200.hlu import _auto_capacity
+
+    cfg = args.config
+    *_, lu_eps, lu_kmax = CONFIGS[cfg]
+    ctl = TruncationControl(lu_eps, lu_kmax)
+    os.environ["HLU_ASSEMBLY_WORKERS"] = str(max(1, (os.cpu_count() or 1) // world))
+    t0 = time.perf_counter()
+    h = build_case(cfg)
+    t_asm = time.perf_counter() - t0
+    cap = _auto_capacity([h], ctl)
+    comm = multigpu.Communicator(dist, rank, world, dev)
+    t0 = time.perf_counter()
+    layout, owner, packed = multigpu.shard_plan(h, world, rank, cap)
+    t_plan = time.perf_counter() - t0
+    call = DeviceCall(layout, packed, ctl, device=dev, use_graph=True, comm=comm)
+    call.launch()
+    call.check_errors()
+    flops = call.flops()
+    call.upload()
+    call.snapshot()
+    flush = torch.empty(int(256 * 2**20 // 4), dtype=torch.float32, device=dev)
+    stream = call.stream
+    for _ in range(args.warmup):
+        call.restore()
+        call.launch()
+    call.sync()
+    dist.barrier()
+    torch.cuda.synchronize()
+    clocks = Clocks(local)
+    times = []
+    for _ in range(args.steps):
+        with torch.cuda.stream(stream):
+            flush.fill_(1.0)
+        call.restore()
+        call.sync()
+        dist.barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        call.launch()
+        e1.record(stream)
+        call.sync()
+        times.append(e0.elapsed_time(e1) * 1e-3)
+    torch.cuda.synchronize()
+    cl = clocks.stop()
+    call.check_errors()
+    tt = torch.tensor([float(np.mean(times))], device=dev)
+    dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    t_step = float(tt.item())
+    # end to end: pinned host payloads -> every GPU, sharded factorization,
+    # factors back to the host on rank 0; wall time, max over ranks
+    e2e = []
+    for _ in range(max(2, min(args.steps, 5))):
+        torch.cuda.synchronize()
+        dist.barrier()
+        s0 = time.perf_counter()
+        call.upload()
+        call.launch()
+        if rank == 0:
+            call.download()
+        call.sync()
+        e2e.append(time.perf_counter() - s0)
+    te = torch.tensor([float(np.mean(e2e[1:]))], device=dev)
+    dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    t_e2e = float(te.item())
+    mask = packed.op_mask
+    share = [int(((mask >> np.uint64(r)) & np.uint64(1)).sum()) for r in range(world)]
+    xfer_bytes = int(((packed.xfer["len"] + 1) * 8).sum()) if packed.xfer is not None else 0
+    res = {
+        "metric": "H-LU factorization effective fp64 GFLOP/s (reference FlopCounter / time)",
+        "value": flops / t_step / 1e9,
+        "unit": "GFLOP/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": t_step * 1e3,
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (BASELINE BEM sphere geometry, Laplace kernel; seeded)",
+        "config": bench_config(cfg),
+        "details": {"factor_time_s": t_step, "effective_flops": flops,
+                    "parallelism": f"owner computes over {world} GPUs (2-D block-cyclic slot owners), "
+                                   "NCCL slot exchanges per level, final gather",
+                    "ops_per_rank": share, "exchange_bytes_per_rank_broadcast_total": xfer_bytes,
+                    "levels": int(packed.nlevels), "assembly_s": t_asm, "plan_s": t_plan, "rank_capacity": cap},
+        "e2e": {"value": flops / t_e2e / 1e9, "unit": "GFLOP/s", "time_s": t_e2e,
+                "h2d_bytes_per_step": int(call.h2d_bytes) * world,
+                "d2h_bytes_per_step": int(layout.payload_doubles * 8 + call.ranks.numel() * 4)},
+        "gpu_launches": int(len(packed.launches)),
+        "roofline": None,
+        "clocks": cl,
+    }
+    call.close()
+    comm.close()
+    if rank == 0:
+        print(json.dumps(res))
+    dist.destroy_process_group()
+
+
 def bench_config(cfg):
     """The workload the line is quoted on; identical for both arms (--impl ours / reference)."""
     d, n, eta, leaf, eps, kmax, lu_eps, lu_kmax = CONFIGS[cfg]
@@ -168,10 +289,13 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1:
-        dist.init_process_group("nccl")
+    if world != args.gpus and rank == 0:
+        print(f"bench: --gpus {args.gpus} but WORLD_SIZE {world}: launch N ranks with torchrun", file=sys.stderr)
     torch.cuda.set_device(local)
     dev = f"cuda:{local}"
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device(dev))
+        return run_sharded(args, world, rank, local, dev, dist)
     cfg = args.config
     *_, lu_eps, lu_kmax = CONFIGS[cfg]
     ctl = TruncationControl(lu_eps, lu_kmax)
@@ -373,6 +497,9 @@ def cpu_baseline(h, ctl, cfg, budget=20.0, procs=None):
 
 def workload_name(cfg):
     *_, lu_eps, lu_kmax = CONFIGS[cfg]
+    if CONFIGS[cfg][2] is None:
+        return (f"{cfg}: H-LU of the n={CONFIGS[cfg][1]} HODLR circle matrix (-log|x-y|/2pi, A_ii=1, leaf "
+                f"{CONFIGS[cfg][3]}, rank-{CONFIGS[cfg][5]} off-diagonal blocks, LU eps {lu_eps}, kmax {lu_kmax})")
     return (f"{cfg}: H-LU of the n={CONFIGS[cfg][1]} BEM sphere matrix "
             f"(leaf {CONFIGS[cfg][3]}, eta 2, LU eps {lu_eps}, kmax {lu_kmax})")
 

@@ -246,6 +246,23 @@ int hlu_schedule_destroy(hlu_schedule *s);
  * (out may be NULL), 0 without stamps */
 int64_t hlu_schedule_stamps(hlu_schedule *s, unsigned long long *out);
 
+/* --- GPU assembly (reference kernels.py:73-168) --- */
+typedef struct {
+  int32_t r0, r1, c0, c1; /* point ranges (cluster-tree order) */
+  int32_t tcl, scl;       /* cluster ids of the interpolation data (Rk leaves) */
+  int32_t kind, pad;
+  int64_t out_a, out_b;   /* pool offsets: dense block (column-major) / factor pair X, Y */
+} hlu_asm_desc; /* 48 bytes */
+/* dense leaves: A_ij = g(|x_i - y_j|), coincident points at diag (assemble_dense_block) */
+int hlu_asm_dense_f64(const double *pts, int d, const void *desc, int count, double diag, double *pool, void *stream);
+/* Rk leaves: X = U_t K(nodes_t, nodes_s) (m x Gs), Y = U_s (n x Gs) by tensor Chebyshev
+ * interpolation (assemble_lowrank_block; recompressed by hlu_rk_update_batched_f64) */
+int hlu_asm_cheb_f64(const double *pts, int d, const void *desc, int count, const int32_t *cl_cnt,
+                     const double *cl_nodes, const double *cl_w, int max_grid, double *pool, void *stream);
+/* HODLR blocks: partially pivoted cross approximation to at most k terms (U, V; nterms per block) */
+int hlu_asm_aca_f64(const double *pts, int d, const void *desc, int count, int k, double diag, double *pool,
+                    int32_t *nterms, void *stream);
+
 /* library identity / sanity */
 const char *hlu_version(void);
 int hlu_device_check(void); /* 0 when a sm_100 device is present */

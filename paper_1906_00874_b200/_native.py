@@ -40,6 +40,9 @@ SYMBOLS = (
     "hlu_schedule_create_sharded",
     "hlu_xfer_staging_doubles",
     "hlu_xfer_group",
+    "hlu_asm_dense_f64",
+    "hlu_asm_cheb_f64",
+    "hlu_asm_aca_f64",
 )
 
 

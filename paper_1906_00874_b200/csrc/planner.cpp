@@ -28,7 +28,7 @@
 namespace {
 
 constexpr int64_t TEMP_SHIFT = 36;  // temp t at (t+1) << 36: up to 2^27 temps, 2^36-double offsets
-constexpr int KMAX_STACK = RK_KMAXW;  // widest factor pair a truncation takes
+constexpr int KMAX_STACK = RK_KMAX;  // widest dense-product factor pair truncated as (A, B^T)
 constexpr int IDENT = RK_KMAXW;  // identity block edge kept in the pool
 constexpr int F_STATIC = 0, F_LIN = 1, F_RKUPD = 2, F_QUAD = 3;
 
@@ -410,7 +410,10 @@ struct Planner {
       const View av = dense_view(a), bv = dense_view(b);
       const int m = av.rows, kin = av.cols, n = bv.cols;
       Pair p;
-      if (kin <= KMAX_STACK) {
+      // compress_dense(A @ B) as the narrower of the factor pair (A, B^T) (stacked
+      // rank kin) and the formed product (I, D^T) / (D, I) (rank min(m, n)),
+      // preferring the block-TSQR pipeline (<= RK_KMAX) over the wide path
+      if (kin <= product_pair_max || (std::min(m, n) > product_pair_max && kin <= IDENT)) {
         rkt_op(1, {Pair{av, bv.T(), 1.0, 0, 0}}, m, n, -1, reads, {}, true, false, 0.0, &p);
         tps->push_back(pair_temp(p));
         return p;
@@ -945,6 +948,7 @@ struct Planner {
     std::vector<int64_t> birth(nt, BIG), death(nt, -1);
     for (size_t i = 0; i < ops.size(); ++i) {
       const Op &o = ops[i];
+      if (slot_owner && !((op_mask[i] >> my_rank) & 1ull)) continue;  // temps never cross ranks
       const int64_t lv = levels[i];
       for (int64_t k = o.to_begin; k < o.to_end; ++k) {
         birth[tids[k]] = std::min(birth[tids[k]], lv);
@@ -971,7 +975,7 @@ struct Planner {
     int64_t top = 0;
     int64_t di = 0;
     for (int64_t t : order) {
-      if (temp_size[t] == 0) continue;
+      if (temp_size[t] == 0 || birth[t] == BIG) continue;  // empty, or another rank's temp
       const int64_t b = birth[t];
       while (di < nt && death[by_death[di]] < b) {
         const int64_t u = by_death[di++];
@@ -1015,6 +1019,10 @@ struct Planner {
   }
 
   int split_rows = 0;  // 0: never split chains; else minimum rows per sub-chain
+  // dense products A B with an inner dimension up to this are truncated as the
+  // factor pair (A, B^T) (HLU_PRODUCT_PAIR_MAX, default RK_KMAX); wider ones are
+  // formed and truncated as (I, D^T) / (D, I)
+  int product_pair_max = KMAX_STACK;
   bool small_gemm = false;  // route small chains to the warp-per-chain kernel
 
   void push_term(std::vector<hlu_term> &out, const Term &t, int64_t ab) {
@@ -1280,10 +1288,10 @@ struct Planner {
     double t0 = now_s();
     assign_levels();
     if (timing) std::fprintf(stderr, "plan: levels %.2fs\n", now_s() - t0), t0 = now_s();
+    if (slot_owner) shard_ops();  // before the arena: a rank allocates only its own temps
     allocate_temps();
     if (timing) std::fprintf(stderr, "plan: temps %.2fs\n", now_s() - t0), t0 = now_s();
     const size_t n = ops.size();
-    if (slot_owner) shard_ops();
     // ops ordered by (level, kind), program order inside: a stable counting sort
     std::vector<int64_t> order(n);
     {
@@ -1549,6 +1557,7 @@ extern "C" int hlu_plan_build_sharded(hlu_plan **out, const hlu_plan_node *nodes
   P.nslots = nslots;
   P.nrank = nrk;
   P.split_rows = split_rows;
+  if (const char *e = std::getenv("HLU_PRODUCT_PAIR_MAX")) P.product_pair_max = std::atoi(e);
   try {
     const double t0 = Planner::now_s();
     for (int64_t i = 0; i < ncmds; ++i) {

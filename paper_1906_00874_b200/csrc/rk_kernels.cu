@@ -500,7 +500,7 @@ __device__ __forceinline__ double part_sum(double v) {
 }
 
 template <int KM, int LP, int NT>
-__device__ void jacobi_lp(double *X, double *V, int n, const unsigned char *pa, const unsigned char *pb) {
+__device__ void jacobi_lp(double *X, double *V, int n, const unsigned char *pa, const unsigned char *pb, int rows) {
   const int tid = threadIdx.x;
   const int grp = tid / LP, l = tid % LP, ngrp = NT / LP;
   const int qq = n + (n & 1);
@@ -536,11 +536,11 @@ __device__ void jacobi_lp(double *X, double *V, int n, const unsigned char *pa, 
 #pragma unroll
         for (int q = 0; q < RPL; ++q) {
           const int i = l + q * LP;
-          const bool ok = i < n;
+          const bool ok = i < rows, okv = i < n;
           xa[q] = ok ? X[i + a * KM] : 0.0;
           xb[q] = ok ? X[i + b * KM] : 0.0;
-          va[q] = ok ? V[i + a * KM] : 0.0;
-          vb[q] = ok ? V[i + b * KM] : 0.0;
+          va[q] = okv ? V[i + a * KM] : 0.0;
+          vb[q] = okv ? V[i + b * KM] : 0.0;
         }
         double al = 0.0, be = 0.0, ga = 0.0;
 #pragma unroll
@@ -554,15 +554,18 @@ __device__ void jacobi_lp(double *X, double *V, int n, const unsigned char *pa, 
         ga = part_sum<LP>(ga);
         const double g2 = ga * ga, ab = al * be;
         if (ga == 0.0 || !(g2 > 1e-30 * ab)) continue;  // |ga| <= 1e-15 sqrt(al be)
+        if (!(ab > 1e-280)) continue;  // numerically null columns: no rotation (no denormal / ftz rsqrt)
         if (g2 > 1e-16 * ab) big = 1;                    // not yet in the quadratic regime
         double cs, sn;
         jacobi_rot(al, be, ga, g2, cs, sn);
 #pragma unroll
         for (int q = 0; q < RPL; ++q) {
           const int i = l + q * LP;
-          if (i < n) {
+          if (i < rows) {
             X[i + a * KM] = cs * xa[q] - sn * xb[q];
             X[i + b * KM] = sn * xa[q] + cs * xb[q];
+          }
+          if (i < n) {
             V[i + a * KM] = cs * va[q] - sn * vb[q];
             V[i + b * KM] = sn * va[q] + cs * vb[q];
           }
@@ -583,13 +586,15 @@ __device__ void jacobi_lp(double *X, double *V, int n, const unsigned char *pa, 
   }
 }
 
+// X: rows x n (rows defaults to n, at most KM), V: n x n
 template <int KM, int NT>
-__device__ void jacobi(double *X, double *V, int n, const unsigned char *pa, const unsigned char *pb) {
+__device__ void jacobi(double *X, double *V, int n, const unsigned char *pa, const unsigned char *pb, int rows = -1) {
+  if (rows < 0) rows = n;
   for (int e = threadIdx.x; e < KM * KM; e += NT) V[e] = ((e % KM) == (e / KM)) ? 1.0 : 0.0;
   __syncthreads();
   if (n < 2) return;
-  if ((n + 1) / 2 > NT / 32) jacobi_lp<KM, 16, NT>(X, V, n, pa, pb);
-  else jacobi_lp<KM, 32, NT>(X, V, n, pa, pb);
+  if ((n + 1) / 2 > NT / 32) jacobi_lp<KM, 16, NT>(X, V, n, pa, pb, rows);
+  else jacobi_lp<KM, 32, NT>(X, V, n, pa, pb, rows);
   __syncthreads();
 }
 
@@ -969,7 +974,7 @@ __device__ int r_core(const double *Rx, int ldx, const double *Ry, int ldy, int 
           const double al = is_a ? so : sp, be = is_a ? sp : so;
           const double ga = (g4[0] + g4[1]) + (g4[2] + g4[3]);
           const double g2 = ga * ga, ab = al * be;
-          if (ga != 0.0 && g2 > 1e-30 * ab) {
+          if (ga != 0.0 && g2 > 1e-30 * ab && ab > 1e-280) {  // (null columns: no rotation)
             if (g2 > 1e-16 * ab && fmax(al, be) > cmax) big = 1;
             jacobi_rot(al, be, ga, g2, cs, sn);
           }
@@ -1626,26 +1631,32 @@ __global__ void __launch_bounds__(RW_NT)
     }
     __syncthreads();
     const int rx = min(m, K), ry = min(n, K);
-    for (int e = tid; e < KW * KW; e += NT) {  // M = R_x R_y^T, zero outside rx x ry
+    // G = M = R_x R_y^T (rx x ry) or its transpose, so that G has q = min(rx, ry)
+    // columns (no null columns for the one-sided Jacobi); zero padded to KW x KW
+    const bool tr = ry > rx;
+    const int q = tr ? rx : ry;
+    for (int e = tid; e < KW * KW; e += NT) {
       const int i = e % KW, j = e / KW;
+      const int a = tr ? j : i, b = tr ? i : j;  // M(a, b)
       double acc = 0.0;
-      if (i < rx && j < ry)
-        for (int t = max(i, j); t < K; ++t) acc = fma(X[i + (int64_t)t * m], Y[j + (int64_t)t * n], acc);
+      if (a < rx && b < ry)
+        for (int t = max(a, b); t < K; ++t) acc = fma(X[a + (int64_t)t * m], Y[b + (int64_t)t * n], acc);
       M[e] = acc;
     }
-    build_pairs<NT>(pairs_a, pairs_b, K + (K & 1));
+    build_pairs<NT>(pairs_a, pairs_b, q + (q & 1));
     __syncthreads();
-    jacobi<KW, NT>(M, V, K, pairs_a, pairs_b);
-    for (int j = tid; j < K; j += NT) {
+    const int pr = tr ? ry : rx;                      // rows of G
+    jacobi<KW, NT>(M, V, q, pairs_a, pairs_b, pr);  // G V = W = U S
+    for (int j = tid; j < q; j += NT) {
       double ss = 0.0;
-      for (int i = 0; i < rx; ++i) ss = fma(M[i + j * KW], M[i + j * KW], ss);
+      for (int i = 0; i < pr; ++i) ss = fma(M[i + j * KW], M[i + j * KW], ss);
       sig[j] = sqrt(ss);
     }
     __syncthreads();
-    for (int j = tid; j < K; j += NT) {
+    for (int j = tid; j < q; j += NT) {
       int rk = 0;
       const double sj = sig[j];
-      for (int i = 0; i < K; ++i) rk += (sig[i] > sj) || (sig[i] == sj && i < j);
+      for (int i = 0; i < q; ++i) rk += (sig[i] > sj) || (sig[i] == sj && i < j);
       perm[rk] = j;
     }
     __syncthreads();
@@ -1654,7 +1665,7 @@ __global__ void __launch_bounds__(RW_NT)
       int kk = 0;
       if (s1 != 0.0) {
         const double thr = c.eps * s1;
-        for (int i = 0; i < K; ++i) kk += sig[i] > thr;
+        for (int i = 0; i < q; ++i) kk += sig[i] > thr;
       }
       if (c.kmax >= 0) kk = min(kk, c.kmax);
       if (kk > o.cap) {
@@ -1666,13 +1677,15 @@ __global__ void __launch_bounds__(RW_NT)
     __syncthreads();
     const int kk = s_kk;
     double *outA = c.pool + o.out_a, *outB = c.pool + o.out_b;
+    // G = M   (!tr): M = W V^T  -> A' = Q_x [W_sel; 0],        B' = Q_y [V_sel; 0]
+    // G = M^T (tr):  M = V W^T  -> A' = Q_x [(V S)_sel; 0],    B' = Q_y [(W / S)_sel; 0]
     for (int64_t e = tid; e < (int64_t)m * kk; e += NT) {
-      const int i = (int)(e % m), col = (int)(e / m);
-      outA[e] = i < rx ? M[i + perm[col] * KW] : 0.0;  // (U S)_sel = W_sel
+      const int i = (int)(e % m), col = (int)(e / m), j = perm[col];
+      outA[e] = i < rx ? (tr ? V[i + j * KW] * sig[j] : M[i + j * KW]) : 0.0;
     }
     for (int64_t e = tid; e < (int64_t)n * kk; e += NT) {
-      const int i = (int)(e % n), col = (int)(e / n);
-      outB[e] = i < ry ? V[i + perm[col] * KW] : 0.0;
+      const int i = (int)(e % n), col = (int)(e / n), j = perm[col];
+      outB[e] = i < ry ? (tr ? M[i + j * KW] / sig[j] : V[i + j * KW]) : 0.0;
     }
     __syncthreads();
     for (int col = wq; col < 2 * kk; col += NW) {
@@ -1853,10 +1866,13 @@ extern "C" int hlu_rkt_phases(const hlu_ctx *ctx, hlu_rkt_desc *d, const hlu_rkp
   cudaStreamWaitEvent(s0, ev[0], 0);
   cudaStreamWaitEvent(s1, ev[0], 0);
   run(1, s0);
+  // rare routes (exist only with eps == 0 or a stacked-rank bound above RK_KMAX)
+  // behind the short K <= 8 branch, off the K <= 16 branch that often sets
+  // the level time
+  if (ctx->eps == 0.0 || g_wide_hint) run(3, s0);
+  else stamp(3, s0);
   cudaEventRecord(ev[1], s0);
   run(2, s1);
-  if (ctx->eps == 0.0 || g_wide_hint) run(3, s1);  // rare routes exist only then
-  else stamp(3, s1);
   cudaEventRecord(ev[2], s1);
   // block TSQR: large-buffer items on side[2] beside the small ones
   cudaStreamWaitEvent(s2, ev[0], 0);

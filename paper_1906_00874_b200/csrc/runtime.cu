@@ -68,7 +68,9 @@ static int launch_one(hlu_schedule *s, const hlu_launch &L, int &slot, cudaStrea
     case HLU_K_GEMM_SMALL: return hlu_gemm_small_batched_f64(&s->ctx, s->gemm + L.first, s->terms, L.count, st);
     case HLU_K_RKT32: {
       hlu_rkt_set_wide_hint((L.smem_dim & 2) != 0);
-      const int rc = hlu_rkt_phases(&s->ctx, s->rkt, s->parts, L.first, L.count, &s->scratch, slot++, st, &s->aux);
+      static const bool serial = getenv("HLU_RKT_SERIAL") && getenv("HLU_RKT_SERIAL")[0] == '1';
+      const int rc = hlu_rkt_phases(&s->ctx, s->rkt, s->parts, L.first, L.count, &s->scratch, slot++, st,
+                                    serial ? nullptr : &s->aux);
       hlu_rkt_set_wide_hint(1);
       return rc;
     }

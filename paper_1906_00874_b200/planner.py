@@ -41,7 +41,7 @@ from .ir import (
 TEMP_SHIFT = 36  # virtual address of temp t: (t + 1) << TEMP_SHIFT (2^27 temps, 2^36-double offsets)
 DEFAULT_CAP = 32
 IDENT = 128    # identity block edge kept in the pool (= ir.RK_KMAXW)
-KMAX_STACK = 128  # widest factor pair a truncation takes (the wide path, ir.RK_KMAXW)
+KMAX_STACK = 64   # widest dense-product factor pair truncated as (A, B^T) (ir.RK_KMAX)
 MAX_CAP = 64     # largest per-block Rk capacity (= the stacked-rank limit of the kernels)
 
 
@@ -365,10 +365,13 @@ class Planner:
         if not _part(a) and not _part(b):
             av, bv = self.dense_view(a), self.dense_view(b)
             m, kin, n = av.rows, av.cols, bv.cols
-            if kin <= KMAX_STACK:  # compress_dense(A @ B) as the factor pair (A, B^T)
+            # compress_dense(A @ B) as the narrower of the factor pair (A, B^T)
+            # (stacked rank kin) and the formed product (I, D^T) / (D, I) (stacked
+            # rank min(m, n)), preferring the block-TSQR pipeline (<= KMAX_STACK)
+            # over the wide path (<= IDENT)
+            if kin <= KMAX_STACK or (min(m, n) > KMAX_STACK and kin <= IDENT):
                 p = self.rkt(RK_RECOMPRESS, [Pair(av, bv.T)], m, n, reads=reads, defer=True)
                 return p, reads, [self._pair_temp(p)]
-            # wide inner dimension: form D = A @ B, then truncate (I, D^T) or (D, I)
             if min(m, n) > IDENT:
                 raise StructureError(f"dense product {m}x{kin}x{n} exceeds the truncation kernel")
             t, base = self._temp(m * n)

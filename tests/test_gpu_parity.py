@@ -104,7 +104,9 @@ def test_add_truncated_eps0(rng, m, n, k1, k2, kmax):
 
 
 @pytest.mark.parametrize("m,n,ks,eps,kmax", [(200, 150, (40, 40), 1e-8, None), (300, 260, (50, 30, 20), 1e-6, None),
-                                             (128, 128, (64, 64), 1e-10, 48), (700, 90, (70, 58), 1e-12, None)])
+                                             (128, 128, (64, 64), 1e-10, 48), (700, 90, (70, 58), 1e-12, None),
+                                             (64, 80, (100,), 1e-4, None), (40, 50, (70, 30), 1e-4, None),
+                                             (128, 96, (128,), 1e-4, 48)])
 def test_wide_truncation_vs_oracle(rng, m, n, ks, eps, kmax):
     """Stacked ranks 64 < K <= 128 (the wide path): merges of several kmax-wide
     parts and adds of two capacity-64 factors, against the oracle's recompress
@@ -126,6 +128,45 @@ def test_wide_truncation_vs_oracle(rng, m, n, ks, eps, kmax):
     assert got.k == want.k
     exact = sum(p.value() for p in parts)
     assert _spec(got.value() - want.value()) <= max(1e-10 * _spec(exact), 4 * eps * _spec(exact))
+
+
+@pytest.mark.parametrize("m,kin,n", [(64, 100, 64), (64, 128, 48), (128, 128, 128), (100, 70, 120)])
+def test_wide_dense_product_vs_oracle(rng, m, kin, n):
+    """compress_dense(A @ B) of dense blocks with a wide inner dimension as the
+    factor pair (A, B^T) (K = kin > 64, K > m): same rank as the reference's
+    dense SVD of the product (lowrank.py:171-175)."""
+    ctl = TruncationControl(1e-4)
+    a = rng.standard_normal((m, kin)) * (0.8 ** np.arange(kin))
+    b = rng.standard_normal((kin, n))
+    want = orc.compress_dense(a @ b, ctl)
+    got = device_ops.recompress(LowRank(a, b.T.copy()), ctl)
+    assert got.k == want.k
+    assert _spec(got.value() - a @ b) <= 2e-4 * _spec(a @ b)
+
+
+def test_wide_dense_product_bem_blocks():
+    """The same with real near-field blocks of the BEM sphere (rapidly
+    decaying product spectra): every product A B of two dense leaves with a
+    shared inner cluster wider than 64, against the oracle's compress_dense."""
+    build, _ = cases.CASES["sphere_2048_l64"]
+    h, _ = build()
+    dense = [lf for lf in h.leaves() if lf.kind == hmatrix.DENSE]
+    by_row = {}
+    for lf in dense:
+        by_row.setdefault(lf.row_range, []).append(lf)
+    ctl = TruncationControl(1e-4)
+    checked = 0
+    for a in dense:
+        if a.cols <= 64:
+            continue
+        for b in by_row.get(a.col_range, [])[:3]:
+            want = orc.compress_dense(a.data @ b.data, ctl)
+            got = device_ops.recompress(LowRank(a.data.copy(), b.data.T.copy()), ctl)
+            assert got.k == want.k, (a.data.shape, b.data.shape, got.k, want.k)
+            checked += 1
+        if checked >= 40:
+            break
+    assert checked > 0
 
 
 def test_add_truncated_parallel_outer(rng):
