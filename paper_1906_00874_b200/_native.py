@@ -26,6 +26,8 @@ SYMBOLS = (
     "hlu_rkt_ws_doubles",
     "hlu_schedule_create",
     "hlu_schedule_create_chains",
+    "hlu_schedule_create_dag",
+    "hlu_schedule_graph_nodes",
     "hlu_schedule_launch",
     "hlu_schedule_destroy",
     "hlu_schedule_stamps",
@@ -104,6 +106,11 @@ def lib():
                                       vp, vp, vp, vp, vp, vp, sp, i32, vp]
     L.hlu_schedule_create_chains.argtypes = [ctypes.POINTER(vp), ctypes.POINTER(HluCtx), vp, i64,
                                              vp, vp, vp, vp, vp, vp, sp, vp, vp, i64, i32, vp]
+    L.hlu_schedule_create_dag.argtypes = [ctypes.POINTER(vp), ctypes.POINTER(HluCtx), vp, i64,
+                                          vp, vp, vp, vp, vp, vp, sp, vp, vp, vp, vp, vp]
+    L.hlu_schedule_create_dag.restype = ctypes.c_int
+    L.hlu_schedule_graph_nodes.argtypes = [vp]
+    L.hlu_schedule_graph_nodes.restype = i64
     L.hlu_schedule_launch.argtypes = [vp, vp]
     L.hlu_schedule_destroy.argtypes = [vp]
     L.hlu_schedule_stamps.argtypes = [vp, vp]
@@ -136,6 +143,39 @@ def lib():
 def check(rc, what):
     if rc != 0:
         raise RuntimeError(f"{what} failed with status {rc}")
+
+
+def rkt_scratch_dag(torch, device, rkt, launches):
+    """Scratch of a DAG schedule: truncation launches of different time slots run
+    concurrently, so every launch owns a window of the lists (7 ints per
+    descriptor, at 7 * first) and of the row-block items.  Returns (struct,
+    keep-alive tensors, item0[nlaunch], nitems[nlaunch])."""
+    import numpy as np
+
+    from . import ir
+
+    nl = len(launches)
+    isr = launches["kind"] == ir.K_RKT32 if nl else np.zeros(0, dtype=bool)
+    nrkt = int(isr.sum())
+    nops = int(len(rkt)) if nrkt else 1
+    item0 = np.zeros(max(nl, 1), dtype=np.int64)
+    nitems = np.zeros(max(nl, 1), dtype=np.int64)
+    total = 1
+    if nrkt:
+        m = rkt["m"].astype(np.int64)
+        n = rkt["n"].astype(np.int64)
+        start = np.zeros(len(m) + 1, dtype=np.int64)
+        np.cumsum((m + ir.RK_BR - 1) // ir.RK_BR + (n + ir.RK_BR - 1) // ir.RK_BR, out=start[1:])
+        f = launches["first"].astype(np.int64)[isr]
+        c = launches["count"].astype(np.int64)[isr]
+        item0[:nl][isr] = start[f]
+        nitems[:nl][isr] = start[f + c] - start[f]
+        total = max(int(start[-1]), 1)
+    counts = torch.zeros(8 * max(nrkt, 1), dtype=torch.int32, device=device)
+    lst = torch.zeros(7 * nops, dtype=torch.int32, device=device)
+    items = torch.zeros(total * ir.RKT_ITEM.itemsize, dtype=torch.uint8, device=device)
+    st = HluRktScratch(counts.data_ptr(), lst.data_ptr(), items.data_ptr(), nops, total)
+    return st, (counts, lst, items), item0, nitems
 
 
 def rkt_scratch(torch, device, rkt, launches):

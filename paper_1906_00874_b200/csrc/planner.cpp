@@ -942,6 +942,411 @@ struct Planner {
     }
   }
 
+  // ---------------------------------------------------------- DAG schedule
+  // (hlu_plan_build_dag) The level schedule pays the slowest op of every level.
+  // The DAG schedule drops the barriers: a hazard sweep in model time (per-op
+  // latency model op_cost_ns) gives every op a start time; ops whose start
+  // falls in the same dag_slot_ns window and that share a kernel class form one
+  // launch, and every launch lists the launches it depends on (RAW / WAR / WAW
+  // on skeleton slots and temps, arena-block reuse).  The runtime replays the
+  // launch DAG as one CUDA graph whose edges are exactly these dependencies:
+  // the GPU analogue of the paper's task DAG with fine-grained region
+  // dependencies instead of a wavefront per level.
+  // `levels` then holds the launch-group keys (time slot, class) in
+  // topological order; every hazard predecessor of an op has a smaller key.
+  int64_t dag_slot_ns = 0;  // 0: level schedule
+  std::vector<int64_t> op_start, op_ready;  // model ns: start, and when dependants may start
+  std::vector<int64_t> dag_ptr;             // per launch: [dag_ptr[l], dag_ptr[l+1]) into dag_idx
+  std::vector<int32_t> dag_idx;             // predecessor launches
+  std::vector<int32_t> op_rec[2];           // launch record(s) holding each op (-1: none)
+
+  int rkt_class(const RktP &r) const {
+    if (r.pn > 2) return 2;                        // merges: stacked rank usually > 32
+    return std::max(r.m, r.n) <= 64 ? 0 : 1;       // register warp path / CTA path
+  }
+
+  void assign_slots() {
+    const int64_t D = dag_slot_ns;
+    const int64_t nt = (int64_t)temp_size.size();
+    MaxTree lw;
+    TagTree lr;
+    lw.init(std::max<int64_t>(nslots, 1));
+    lr.init(std::max<int64_t>(nslots, 1));
+    std::fill(lw.t.begin(), lw.t.end(), 0);
+    std::fill(lr.t.begin(), lr.t.end(), 0);
+    std::vector<int64_t> lw_s(nslots, 0), lwT(nt, 0), lrT(nt, 0);
+    op_start.assign(ops.size(), 0);
+    op_ready.assign(ops.size(), 0);
+    auto constraint = [&](const Op &o) {
+      int64_t c = 0;
+      for (int64_t i = o.r_begin; i < o.r_end; ++i) {
+        const Iv &v = ivs[i];
+        if (v.lo >= nslots) c = std::max(c, lwT[v.lo - nslots]);
+        else if (v.hi - v.lo == 1) c = std::max(c, lw_s[v.lo]);
+        else c = std::max(c, lw.query(v.lo, v.hi));
+      }
+      for (int64_t i = o.ti_begin; i < o.ti_end; ++i) c = std::max(c, lwT[tids[i]]);
+      for (int64_t i = o.w_begin; i < o.w_end; ++i) {
+        const Iv &v = ivs[i];
+        if (v.lo >= nslots) {
+          const int64_t t = v.lo - nslots;
+          c = std::max(c, std::max(lwT[t], lrT[t]));
+        } else {
+          for (int64_t s = v.lo; s < v.hi; ++s) c = std::max(c, std::max(lw_s[s], lr.get(s)));
+        }
+      }
+      return c;
+    };
+    auto commit = [&](const Op &o, int64_t rd) {
+      for (int64_t i = o.r_begin; i < o.r_end; ++i) {
+        const Iv &v = ivs[i];
+        if (v.lo >= nslots) lrT[v.lo - nslots] = std::max(lrT[v.lo - nslots], rd);
+        else lr.chmax(v.lo, v.hi, rd);
+      }
+      for (int64_t i = o.ti_begin; i < o.ti_end; ++i) lrT[tids[i]] = std::max(lrT[tids[i]], rd);
+      for (int64_t i = o.w_begin; i < o.w_end; ++i) {
+        const Iv &v = ivs[i];
+        if (v.lo >= nslots) {
+          lwT[v.lo - nslots] = rd;
+        } else {
+          for (int64_t s = v.lo; s < v.hi; ++s) {
+            lw_s[s] = rd;
+            lw.set(s, rd);
+          }
+        }
+      }
+    };
+    auto place = [&](size_t i, int64_t st) {
+      op_start[i] = st;
+      op_ready[i] = std::max(st + op_cost_ns(ops[i]), (st / D + 1) * D);
+    };
+    std::vector<int64_t> pending;
+    for (size_t i = 0; i < ops.size(); ++i) {
+      const Op &o = ops[i];
+      if (o.defer) {  // a temp producer: placed as late as its consumer allows (below)
+        pending.push_back((int64_t)i);
+        continue;
+      }
+      if (!pending.empty()) {
+        // as-soon-as-possible pass over the pending producers (they write fresh
+        // temps only; the provisional temp times let them see one another) ...
+        int64_t last = 0;
+        for (int64_t p : pending) {
+          const Op &q = ops[p];
+          place((size_t)p, constraint(q));
+          for (int64_t k = q.w_begin; k < q.w_end; ++k)
+            if (ivs[k].lo >= nslots) lwT[ivs[k].lo - nslots] = op_ready[p];
+          last = std::max(last, op_ready[p]);
+        }
+        // ... then all of them later by whole slots, to end just before the consumer starts
+        const int64_t c = constraint(o);
+        const int64_t delay = std::max<int64_t>(0, (c - last) / D * D);
+        for (int64_t p : pending) {
+          op_start[p] += delay;
+          op_ready[p] += delay;
+          commit(ops[p], op_ready[p]);
+        }
+        pending.clear();
+      }
+      place(i, constraint(o));
+      commit(o, op_ready[i]);
+    }
+    for (int64_t p : pending) {
+      place((size_t)p, constraint(ops[p]));
+      commit(ops[p], op_ready[p]);
+    }
+    // launch-group keys: (time slot, class), compressed to consecutive ids
+    levels.assign(ops.size(), 0);
+    std::vector<int64_t> keys(ops.size());
+    for (size_t i = 0; i < ops.size(); ++i) {
+      const int sub = ops[i].kind == 3 ? rkt_class(rkt[ops[i].payload]) : 0;
+      keys[i] = op_start[i] / D * 4 + sub;
+    }
+    std::vector<int64_t> uniq(keys);
+    std::sort(uniq.begin(), uniq.end());
+    uniq.erase(std::unique(uniq.begin(), uniq.end()), uniq.end());
+    for (size_t i = 0; i < ops.size(); ++i)
+      levels[i] = std::lower_bound(uniq.begin(), uniq.end(), keys[i]) - uniq.begin();
+  }
+
+  // Launch-level dependency lists of the DAG schedule (after pack() filled
+  // op_rec): a second hazard sweep in program order that tracks, per skeleton
+  // slot and temp, the last writer op and the launches that read it since;
+  // a temp taking over an arena block waits for every launch that touched the
+  // block's previous holder.
+  void compute_dag_deps(int64_t nlaunch) {
+    const int64_t nt = (int64_t)temp_size.size();
+    struct Node {
+      int32_t launch, next;
+    };
+    std::vector<Node> pool;
+    pool.reserve(ops.size() * 2);
+    std::vector<int32_t> w_s(nslots, -1), w_t(nt, -1);        // last writer op
+    std::vector<int32_t> rd_s(nslots, -1), rd_t(nt, -1);      // readers since (launch lists)
+    std::vector<int32_t> touch_t(nt, -1);                     // every launch that touched a temp
+    std::vector<int32_t> first_t(nt, -1);                     // first op touching a temp
+    std::vector<int64_t> e_ptr(ops.size() + 1, 0);
+    std::vector<int32_t> e_idx;
+    e_idx.reserve(ops.size() * 4);
+    auto push = [&](int32_t &head, int32_t launch) {
+      if (launch < 0) return;
+      if (head >= 0 && pool[head].launch == launch) return;
+      pool.push_back(Node{launch, head});
+      head = (int32_t)pool.size() - 1;
+    };
+    auto add_op = [&](int32_t p) {
+      if (p < 0) return;
+      for (int k = 0; k < 2; ++k)
+        if (op_rec[k][p] >= 0) e_idx.push_back(op_rec[k][p]);
+    };
+    auto add_list = [&](int32_t head) {
+      for (int32_t h = head; h >= 0; h = pool[h].next) e_idx.push_back(pool[h].launch);
+    };
+    for (size_t i = 0; i < ops.size(); ++i) {
+      const Op &o = ops[i];
+      // the first op (program order) that touches a temp: every other toucher
+      // follows it through a RAW / WAW hazard, so the hand-over of an arena
+      // block only has to hold this op back (edges added after the sweep: the
+      // previous holder's users may come later in program order)
+      auto first_touch = [&](int64_t t) {
+        if (first_t[t] < 0) first_t[t] = (int32_t)i;
+      };
+      for (int64_t k = o.r_begin; k < o.r_end; ++k) {
+        const Iv &v = ivs[k];
+        if (v.lo >= nslots) add_op(w_t[v.lo - nslots]), first_touch(v.lo - nslots);
+        else
+          for (int64_t s = v.lo; s < v.hi; ++s) add_op(w_s[s]);
+      }
+      for (int64_t k = o.ti_begin; k < o.ti_end; ++k) add_op(w_t[tids[k]]), first_touch(tids[k]);
+      for (int64_t k = o.to_begin; k < o.to_end; ++k) first_touch(tids[k]);
+      for (int64_t k = o.w_begin; k < o.w_end; ++k) {
+        const Iv &v = ivs[k];
+        if (v.lo >= nslots) {
+          const int64_t t = v.lo - nslots;
+          first_touch(t);
+          add_op(w_t[t]);
+          add_list(rd_t[t]);
+        } else {
+          for (int64_t s = v.lo; s < v.hi; ++s) {
+            add_op(w_s[s]);
+            add_list(rd_s[s]);
+          }
+        }
+      }
+      e_ptr[i + 1] = (int64_t)e_idx.size();
+      // commit
+      for (int k2 = 0; k2 < 2; ++k2) {
+        const int32_t me = op_rec[k2][i];
+        if (me < 0) continue;
+        for (int64_t k = o.r_begin; k < o.r_end; ++k) {
+          const Iv &v = ivs[k];
+          if (v.lo >= nslots) push(rd_t[v.lo - nslots], me), push(touch_t[v.lo - nslots], me);
+          else
+            for (int64_t s = v.lo; s < v.hi; ++s) push(rd_s[s], me);
+        }
+        for (int64_t k = o.ti_begin; k < o.ti_end; ++k) push(rd_t[tids[k]], me), push(touch_t[tids[k]], me);
+        for (int64_t k = o.to_begin; k < o.to_end; ++k) push(touch_t[tids[k]], me);
+        for (int64_t k = o.w_begin; k < o.w_end; ++k)
+          if (ivs[k].lo >= nslots) push(touch_t[ivs[k].lo - nslots], me);
+      }
+      for (int64_t k = o.w_begin; k < o.w_end; ++k) {
+        const Iv &v = ivs[k];
+        if (v.lo >= nslots) {
+          w_t[v.lo - nslots] = (int32_t)i;
+          rd_t[v.lo - nslots] = -1;
+        } else {
+          for (int64_t s = v.lo; s < v.hi; ++s) w_s[s] = (int32_t)i, rd_s[s] = -1;
+        }
+      }
+    }
+    // arena-block hand-over: the first op of a temp waits for every launch that
+    // touched the block's previous holder
+    std::vector<std::pair<int32_t, int32_t>> extra;  // (op, predecessor launch)
+    for (int64_t t = 0; t < nt; ++t) {
+      if (first_t[t] < 0 || reuse_from[t] < 0) continue;
+      for (int32_t h = touch_t[reuse_from[t]]; h >= 0; h = pool[h].next) extra.push_back({first_t[t], pool[h].launch});
+    }
+    std::sort(extra.begin(), extra.end());
+    extra.erase(std::unique(extra.begin(), extra.end()), extra.end());
+    // group by launch, dedupe with a stamp per predecessor
+    std::vector<int64_t> lcount(nlaunch + 1, 0);
+    for (size_t i = 0; i < ops.size(); ++i)
+      for (int k = 0; k < 2; ++k)
+        if (op_rec[k][i] >= 0) ++lcount[op_rec[k][i] + 1];
+    for (int64_t l = 0; l < nlaunch; ++l) lcount[l + 1] += lcount[l];
+    std::vector<int32_t> lops(lcount[nlaunch]);
+    {
+      std::vector<int64_t> at(lcount.begin(), lcount.end() - 1);
+      for (size_t i = 0; i < ops.size(); ++i)
+        for (int k = 0; k < 2; ++k)
+          if (op_rec[k][i] >= 0) lops[at[op_rec[k][i]]++] = (int32_t)i;
+    }
+    std::vector<int32_t> stamp(nlaunch, -1);
+    dag_ptr.assign(nlaunch + 1, 0);
+    dag_idx.clear();
+    for (int64_t l = 0; l < nlaunch; ++l) {
+      for (int64_t q = lcount[l]; q < lcount[l + 1]; ++q) {
+        const int32_t i = lops[q];
+        auto take = [&](int32_t p) {
+          if (p >= l) throw std::runtime_error("dag schedule: a dependency does not precede its launch");
+          if (stamp[p] == l) return;
+          stamp[p] = (int32_t)l;
+          dag_idx.push_back(p);
+        };
+        for (int64_t e = e_ptr[i]; e < e_ptr[i + 1]; ++e) take(e_idx[e]);
+        const auto xr = std::equal_range(extra.begin(), extra.end(), std::make_pair(i, (int32_t)0),
+                                         [](const std::pair<int32_t, int32_t> &a, const std::pair<int32_t, int32_t> &b) {
+                                           return a.first < b.first;
+                                         });
+        for (auto it = xr.first; it != xr.second; ++it) take(it->second);
+      }
+      // drop predecessors another predecessor already waits for (one step of
+      // transitive reduction: most hazards repeat the same few chains)
+      const int64_t b = dag_ptr[l], e = (int64_t)dag_idx.size();
+      if (e - b > 1) {
+        std::sort(dag_idx.begin() + b, dag_idx.end());
+        for (int64_t x = b; x < e; ++x) stamp[dag_idx[x]] = (int32_t)l;
+        std::vector<int32_t> keep;
+        // mark implied ones: a predecessor of a predecessor
+        std::vector<char> implied(e - b, 0);
+        for (int64_t x = b; x < e; ++x) {
+          const int32_t p = dag_idx[x];
+          for (int64_t y = dag_ptr[p]; y < dag_ptr[p + 1]; ++y) {
+            const int32_t g = dag_idx[y];
+            if (stamp[g] == l) {
+              const auto it = std::lower_bound(dag_idx.begin() + b, dag_idx.begin() + e, g);
+              implied[it - (dag_idx.begin() + b)] = 1;
+            }
+          }
+        }
+        int64_t w = b;
+        for (int64_t x = b; x < e; ++x)
+          if (!implied[x - b]) dag_idx[w++] = dag_idx[x];
+        dag_idx.resize(w);
+      }
+      dag_ptr[l + 1] = (int64_t)dag_idx.size();
+    }
+  }
+
+  // Diagnostics (HLU_PLAN_CP=1): weighted critical path of the op DAG under a
+  // per-op latency model (ns), beside the level schedule's sum of per-level
+  // maxima under the same model.  Same hazard sweep as assign_levels with
+  // finish times in place of levels.
+  int64_t op_cost_ns(const Op &o) const {
+    switch (o.kind) {
+      case 0: return 25000;
+      case 1: return 40000;
+      case 2: return 30000 + 4000 * std::min<int64_t>(gemm[o.payload].tn, 16);
+      default: {
+        const RktP &r = rkt[o.payload];
+        if (r.pn > 2) return 400000;
+        if (std::max(r.m, r.n) <= 64) return 85000;
+        return 150000;
+      }
+    }
+  }
+  void critical_path_report() {
+    const int64_t nt = (int64_t)temp_size.size();
+    MaxTree lw;
+    TagTree lr;
+    lw.init(std::max<int64_t>(nslots, 1));
+    lr.init(std::max<int64_t>(nslots, 1));
+    std::vector<int64_t> lw_s(nslots, 0), lwT(nt, 0), lrT(nt, 0);
+    for (auto &x : lw.t) x = 0;
+    for (auto &x : lr.t) x = 0;
+    std::vector<int64_t> fin(ops.size(), 0);
+    int64_t cp = 0;
+    int64_t crit_kind[5] = {0, 0, 0, 0, 0};
+    std::vector<int32_t> pred(ops.size(), -1);
+    // last writer op per slot / temp for the walk back
+    std::vector<int32_t> wop_s(nslots, -1), wop_t(nt, -1);
+    for (size_t i = 0; i < ops.size(); ++i) {
+      const Op &o = ops[i];
+      int64_t c = 0;
+      int32_t pr = -1;
+      auto take = [&](int64_t v, int32_t who) { if (v > c) c = v, pr = who; };
+      for (int64_t k = o.r_begin; k < o.r_end; ++k) {
+        const Iv &v = ivs[k];
+        if (v.lo >= nslots) take(lwT[v.lo - nslots], wop_t[v.lo - nslots]);
+        else if (v.hi - v.lo == 1) take(lw_s[v.lo], wop_s[v.lo]);
+        else {
+          const int64_t q = lw.query(v.lo, v.hi);
+          if (q > c) {
+            c = q;
+            for (int64_t s = v.lo; s < v.hi; ++s) if (lw_s[s] == q) { pr = wop_s[s]; break; }
+          }
+        }
+      }
+      for (int64_t k = o.ti_begin; k < o.ti_end; ++k) take(lwT[tids[k]], wop_t[tids[k]]);
+      for (int64_t k = o.w_begin; k < o.w_end; ++k) {
+        const Iv &v = ivs[k];
+        if (v.lo >= nslots) {
+          const int64_t t = v.lo - nslots;
+          take(lwT[t], wop_t[t]);
+          take(lrT[t], -1);
+        } else {
+          for (int64_t s = v.lo; s < v.hi; ++s) take(lw_s[s], wop_s[s]), take(lr.get(s), -1);
+        }
+      }
+      const int64_t f = c + op_cost_ns(o);
+      fin[i] = f;
+      pred[i] = pr;
+      for (int64_t k = o.r_begin; k < o.r_end; ++k) {
+        const Iv &v = ivs[k];
+        if (v.lo >= nslots) lrT[v.lo - nslots] = std::max(lrT[v.lo - nslots], f);
+        else lr.chmax(v.lo, v.hi, f);
+      }
+      for (int64_t k = o.ti_begin; k < o.ti_end; ++k) lrT[tids[k]] = std::max(lrT[tids[k]], f);
+      for (int64_t k = o.w_begin; k < o.w_end; ++k) {
+        const Iv &v = ivs[k];
+        if (v.lo >= nslots) lwT[v.lo - nslots] = f, wop_t[v.lo - nslots] = (int32_t)i;
+        else
+          for (int64_t s = v.lo; s < v.hi; ++s) lw_s[s] = f, lw.set(s, f), wop_s[s] = (int32_t)i;
+      }
+      for (int64_t k = o.to_begin; k < o.to_end; ++k) lwT[tids[k]] = f, wop_t[tids[k]] = (int32_t)i;
+      cp = std::max(cp, f);
+    }
+    {
+      int64_t sr = 0, sw = 0, nwide = 0, mx = 0;
+      for (const Op &o : ops) {
+        for (int64_t k = o.r_begin; k < o.r_end; ++k)
+          if (ivs[k].lo < nslots) { sr += ivs[k].hi - ivs[k].lo; nwide += (ivs[k].hi - ivs[k].lo) > 1; mx = std::max(mx, ivs[k].hi - ivs[k].lo); }
+        for (int64_t k = o.w_begin; k < o.w_end; ++k)
+          if (ivs[k].lo < nslots) sw += ivs[k].hi - ivs[k].lo;
+      }
+      std::fprintf(stderr, "plan cp: nslots %lld read-range sum %lld (wide ivs %lld, max %lld) write-range sum %lld\n",
+                   (long long)nslots, (long long)sr, (long long)nwide, (long long)mx, (long long)sw);
+    }
+    // sum over levels of the max op cost (what the level schedule pays)
+    int64_t nlv = 0;
+    for (auto l : levels) nlv = std::max(nlv, l + 1);
+    std::vector<int64_t> lmax(nlv, 0);
+    for (size_t i = 0; i < ops.size(); ++i) lmax[levels[i]] = std::max(lmax[levels[i]], op_cost_ns(ops[i]));
+    int64_t tl = 0;
+    for (auto x : lmax) tl += x;
+    // walk the critical path back
+    int64_t at = -1;
+    for (size_t i = 0; i < ops.size(); ++i) if (fin[i] == cp) { at = (int64_t)i; break; }
+    int64_t steps = 0;
+    int64_t tk[5] = {0, 0, 0, 0, 0};
+    while (at >= 0) {
+      const Op &o = ops[at];
+      int kd = o.kind;
+      if (kd == 3 && rkt[o.payload].pn > 2) kd = 4;
+      ++crit_kind[kd];
+      tk[kd] += op_cost_ns(o);
+      ++steps;
+      at = pred[at];
+    }
+    std::fprintf(stderr,
+                 "plan cp: ops %zu levels %lld | level-sum %.1f ms | critical path %.1f ms over %lld ops "
+                 "(getrf %lld/%.0fms trsm %lld/%.0fms gemm %lld/%.0fms rkt %lld/%.0fms merge %lld/%.0fms)\n",
+                 ops.size(), (long long)nlv, tl / 1e6, cp / 1e6, (long long)steps, (long long)crit_kind[0], tk[0] / 1e6,
+                 (long long)crit_kind[1], tk[1] / 1e6, (long long)crit_kind[2], tk[2] / 1e6, (long long)crit_kind[3],
+                 tk[3] / 1e6, (long long)crit_kind[4], tk[4] / 1e6);
+  }
+
+  static constexpr int64_t DAG_REUSE_GUARD_NS = 200000;
   void allocate_temps() {
     const int64_t nt = (int64_t)temp_size.size();
     const int64_t BIG = std::numeric_limits<int64_t>::max();
@@ -949,12 +1354,24 @@ struct Planner {
     for (size_t i = 0; i < ops.size(); ++i) {
       const Op &o = ops[i];
       if (slot_owner && !((op_mask[i] >> my_rank) & 1ull)) continue;  // temps never cross ranks
-      const int64_t lv = levels[i];
+      // level schedule: a block is free once its last user's level is over.
+      // DAG schedule: lifetimes in model time with a guard (a block changes
+      // hands only well after its last user should have ended; the launch
+      // dependencies of compute_dag_deps make the hand-over safe regardless)
+      const int64_t lv = dag_slot_ns ? op_start[i] : levels[i];
+      const int64_t le = dag_slot_ns ? op_ready[i] + dag_slot_ns + DAG_REUSE_GUARD_NS : levels[i];
       for (int64_t k = o.to_begin; k < o.to_end; ++k) {
         birth[tids[k]] = std::min(birth[tids[k]], lv);
-        death[tids[k]] = std::max(death[tids[k]], lv);
+        death[tids[k]] = std::max(death[tids[k]], le);
       }
-      for (int64_t k = o.ti_begin; k < o.ti_end; ++k) death[tids[k]] = std::max(death[tids[k]], lv);
+      for (int64_t k = o.ti_begin; k < o.ti_end; ++k) death[tids[k]] = std::max(death[tids[k]], le);
+      if (dag_slot_ns)  // temps read or written through a resource interval only
+        for (int64_t k = o.r_begin; k < o.w_end; ++k)
+          if (ivs[k].lo >= nslots) {
+            const int64_t t = ivs[k].lo - nslots;
+            birth[t] = std::min(birth[t], lv);
+            death[t] = std::max(death[t], le);
+          }
     }
     tbirth = birth;
     std::vector<int> cls(nt);
@@ -1286,8 +1703,10 @@ struct Planner {
   void pack(int64_t arena_base) {
     const bool timing = std::getenv("HLU_PLAN_TIMING") != nullptr;
     double t0 = now_s();
-    assign_levels();
+    if (dag_slot_ns) assign_slots();
+    else assign_levels();
     if (timing) std::fprintf(stderr, "plan: levels %.2fs\n", now_s() - t0), t0 = now_s();
+    if (std::getenv("HLU_PLAN_CP")) critical_path_report();
     if (slot_owner) shard_ops();  // before the arena: a rank allocates only its own temps
     allocate_temps();
     if (timing) std::fprintf(stderr, "plan: temps %.2fs\n", now_s() - t0), t0 = now_s();
@@ -1307,8 +1726,14 @@ struct Planner {
       int dim;
       int64_t lv;
       bool dep;  // truncation launch reading a temp produced in the same level
+      int min_mn = 1 << 30;  // truncation launches: smallest max(m, n) of the ops
     };
     std::vector<Rec> recs;
+    std::vector<int64_t> staged_ops[2];  // DAG schedule: gemm ops staged into the large / small launch
+    if (dag_slot_ns) {
+      op_rec[0].assign(n, -1);
+      op_rec[1].assign(n, -1);
+    }
     int64_t cur_lv = -1;
     int cur_kind = -1;
     int64_t pending_lv = -1;
@@ -1329,6 +1754,9 @@ struct Planner {
         o_terms.insert(o_terms.end(), st.terms.begin(), st.terms.end());
         recs.push_back(Rec{pass == 0 ? HLU_K_GEMM : HLU_K_GEMM_SMALL, (int64_t)st.size(), first, 0, pending_lv, false});
         st.clear();
+        if (dag_slot_ns)
+          for (int64_t q : staged_ops[pass]) op_rec[pass][q] = (int32_t)recs.size() - 1;
+        staged_ops[pass].clear();
       }
       cur_kind = -1;
     };
@@ -1371,6 +1799,7 @@ struct Planner {
           const int64_t nt_ = chain_bounds[c + 1] - chain_bounds[c];
           const bool sm = small_gemm && small_chain(t, (int)nt_);
           (sm ? stage_small : stage_large).add(t, nt_, g.log, g.log_slot);
+          if (dag_slot_ns && (staged_ops[sm].empty() || staged_ops[sm].back() != i)) staged_ops[sm].push_back(i);
         }
         pending_lv = lv;
         continue;
@@ -1406,7 +1835,7 @@ struct Planner {
         dim = r.kb;
       }
       bool dep = false;
-      if (kind == HLU_K_RKT32)
+      if (kind == HLU_K_RKT32 && !dag_slot_ns)
         for (int64_t k = o.ti_begin; k < o.ti_end; ++k) dep = dep || tbirth[tids[k]] == lv;
       if (!recs.empty() && cur_lv == lv && cur_kind == kind) {
         recs.back().count += 1 + extra;
@@ -1417,6 +1846,9 @@ struct Planner {
         cur_lv = lv;
         cur_kind = kind;
       }
+      if (kind == HLU_K_RKT32)
+        recs.back().min_mn = std::min(recs.back().min_mn, std::max(rkt[o.payload].m, rkt[o.payload].n));
+      if (dag_slot_ns) op_rec[0][i] = (int32_t)recs.size() - 1;
     }
     if (pending_lv >= 0) flush_gemm();
     for (const Rec &r : recs) {
@@ -1427,6 +1859,7 @@ struct Planner {
       L.level = (int32_t)r.lv;
       if (r.kind == HLU_K_RKT32) {
         L.smem_dim = (r.dep ? 1 : 0) | (r.dim > RK_KMAX ? 2 : 0);  // bit 2: may take the wide path
+        if (dag_slot_ns && r.min_mn > 64) L.smem_dim |= 4;  // no op fits the register warp kernels
         o_launch.push_back(L);
       } else {
         L.smem_dim = r.dim;
@@ -1436,6 +1869,19 @@ struct Planner {
     nlevels = n ? (*std::max_element(levels.begin(), levels.end()) + 1) : 0;
     if (slot_owner) exchange(order);
     if (timing) std::fprintf(stderr, "plan: pack %.2fs\n", now_s() - t0), t0 = now_s();
+    if (dag_slot_ns) {
+      compute_dag_deps((int64_t)o_launch.size());
+      waits_ok = false;
+      if (timing) {
+        int64_t mx = 0;
+        for (size_t l = 0; l + 1 < dag_ptr.size(); ++l) mx = std::max(mx, dag_ptr[l + 1] - dag_ptr[l]);
+        int64_t span = 0;
+        for (size_t i = 0; i < n; ++i) span = std::max(span, op_ready[i]);
+        std::fprintf(stderr, "plan: dag %.2fs: %zu launches, %zu edges (max in-degree %lld), model span %.1f ms\n",
+                     now_s() - t0, o_launch.size(), dag_idx.size(), (long long)mx, span / 1e6);
+      }
+      return;
+    }
     compute_waits();
     if (timing) std::fprintf(stderr, "plan: waits %.2fs\n", now_s() - t0);
   }
@@ -1527,6 +1973,8 @@ struct hlu_plan {
   std::string error;
 };
 
+static thread_local int64_t g_dag_slot_ns = 0;  // set by hlu_plan_build_dag around the build
+
 extern "C" int hlu_plan_build(hlu_plan **out, const hlu_plan_node *nodes, int64_t nnodes, const hlu_plan_cmd *cmds,
                               int64_t ncmds, int32_t cap, int64_t ident_off, int64_t nslots, int32_t nrk,
                               int64_t arena_base, int32_t split_rows) {
@@ -1557,6 +2005,7 @@ extern "C" int hlu_plan_build_sharded(hlu_plan **out, const hlu_plan_node *nodes
   P.nslots = nslots;
   P.nrank = nrk;
   P.split_rows = split_rows;
+  P.dag_slot_ns = g_dag_slot_ns;
   if (const char *e = std::getenv("HLU_PRODUCT_PAIR_MAX")) P.product_pair_max = std::atoi(e);
   try {
     const double t0 = Planner::now_s();
@@ -1599,6 +2048,24 @@ extern "C" int hlu_plan_build_sharded(hlu_plan **out, const hlu_plan_node *nodes
     return -1;
   }
   return 0;
+}
+
+extern "C" int hlu_plan_build_dag(hlu_plan **out, const hlu_plan_node *nodes, int64_t nnodes, const hlu_plan_cmd *cmds,
+                                  int64_t ncmds, int32_t cap, int64_t ident_off, int64_t nslots, int32_t nrk,
+                                  int64_t arena_base, int32_t split_rows, int64_t slot_ns) {
+  g_dag_slot_ns = slot_ns > 0 ? slot_ns : 0;
+  const int rc = hlu_plan_build_sharded(out, nodes, nnodes, cmds, ncmds, cap, ident_off, nslots, nrk, arena_base,
+                                        split_rows, nullptr, 1, 0);
+  g_dag_slot_ns = 0;
+  return rc;
+}
+
+extern "C" int64_t hlu_plan_dag(const hlu_plan *p, int64_t *ptr, int32_t *idx) {
+  const Planner &P = p->P;
+  if (P.dag_ptr.empty()) return -1;
+  if (ptr) std::memcpy(ptr, P.dag_ptr.data(), P.dag_ptr.size() * sizeof(int64_t));
+  if (idx && !P.dag_idx.empty()) std::memcpy(idx, P.dag_idx.data(), P.dag_idx.size() * sizeof(int32_t));
+  return (int64_t)P.dag_idx.size();
 }
 
 extern "C" const char *hlu_plan_error(const hlu_plan *p) { return p->error.c_str(); }

@@ -15,6 +15,8 @@
 
 extern "C" void hlu_rkt_set_phase_stamps(unsigned long long *p);
 extern "C" void hlu_rkt_set_wide_hint(int on);
+extern "C" int hlu_rkt_phase(const hlu_ctx *ctx, hlu_rkt_desc *d, const hlu_rkpart *parts, int64_t first, int count,
+                             const hlu_rkt_scratch *scratch, int slot, int which, void *stream);
 struct hlu_comm;
 
 extern "C" int hlu_comm_reduce_logs(hlu_comm *c, int32_t *log, int64_t nlog, int32_t *err, void *stream);
@@ -52,6 +54,13 @@ struct hlu_schedule {
   std::vector<XGroup> xgroups;
   double *staging = nullptr;
   int64_t nlevels = 0, nlog = 0;
+  // DAG mode (hlu_schedule_create_dag): predecessor launches of every launch and,
+  // per truncation launch, its private window of the scratch lists / items
+  std::vector<int64_t> dag_ptr;
+  std::vector<int32_t> dag_idx;
+  std::vector<int64_t> rkt_op0, rkt_item0, rkt_items;  // per launch (truncation launches only)
+  int64_t dag_nodes = 0;
+  unsigned long long *dag_join = nullptr;  // written by the graph's last node
 };
 
 __global__ void k_stamp(unsigned long long *slot) {
@@ -193,7 +202,120 @@ static int run_sharded(hlu_schedule *s, cudaStream_t st) {
   return hlu_comm_reduce_logs(s->comm, s->ctx.log, s->nlog, s->ctx.err, st);
 }
 
+// ---------------------------------------------------------------- DAG mode
+// The launch list replayed as a task DAG: every launch is captured with
+// exactly the planner's predecessor launches as graph dependencies
+// (cudaStreamUpdateCaptureDependencies replaces the capturing stream's
+// dependency set before each launch), so independent launches of different
+// time slots overlap and a slow truncation no longer holds a whole level.
+// A truncation launch is itself a small DAG of kernels (classify -> register
+// warp kernels | block TSQR -> cores -> Q apply) with its own window of the
+// scratch lists, because several truncation launches are in flight at once.
+static int capture_tail(cudaStream_t st, std::vector<cudaGraphNode_t> &out) {
+  cudaStreamCaptureStatus status;
+  const cudaGraphNode_t *deps = nullptr;
+  size_t n = 0;
+  if (cudaStreamGetCaptureInfo(st, &status, nullptr, nullptr, &deps, &n) != cudaSuccess) return -20;
+  if (status != cudaStreamCaptureStatusActive) return -20;
+  out.assign(deps, deps + n);
+  return 0;
+}
+
+static int set_deps(cudaStream_t st, std::vector<cudaGraphNode_t> &deps) {
+  return cudaStreamUpdateCaptureDependencies(st, deps.data(), deps.size(), cudaStreamSetCaptureDependencies) ==
+                 cudaSuccess
+             ? 0
+             : -21;
+}
+
+static int run_dag(hlu_schedule *s, cudaStream_t st) {
+  const size_t nl = s->launches.size();
+  std::vector<cudaGraphNode_t> root, deps, tail, a_tail, b_tail, tmp;
+  cudaMemsetAsync(s->scratch.counts, 0, 8 * sizeof(int32_t) * std::max(s->nrkt, 1), st);
+  int rc = capture_tail(st, root);
+  if (rc) return rc;
+  std::vector<int64_t> tptr(nl + 1, 0);
+  std::vector<cudaGraphNode_t> tails;
+  tails.reserve(nl * 2);
+  std::vector<char> has_succ(nl, 0);
+  int slot = 0;
+  static const bool all_routes = getenv("HLU_RKT_ALL_ROUTES") && getenv("HLU_RKT_ALL_ROUTES")[0] == '1';
+  for (size_t l = 0; l < nl; ++l) {
+    const hlu_launch &L = s->launches[l];
+    deps.clear();
+    for (int64_t e = s->dag_ptr[l]; e < s->dag_ptr[l + 1]; ++e) {
+      const int32_t p = s->dag_idx[e];
+      if (p < 0 || (size_t)p >= l) return -22;
+      has_succ[p] = 1;
+      deps.insert(deps.end(), tails.begin() + tptr[p], tails.begin() + tptr[p + 1]);
+    }
+    if (deps.empty()) deps = root;
+    if (L.count <= 0) {  // nothing to run: successors wait for the predecessors directly
+      tails.insert(tails.end(), deps.begin(), deps.end());
+      tptr[l + 1] = (int64_t)tails.size();
+      continue;
+    }
+    if (L.kind != HLU_K_RKT32) {
+      if ((rc = set_deps(st, deps))) return rc;
+      int dummy = 0;
+      if ((rc = launch_one(s, L, dummy, st))) return rc;
+      if ((rc = capture_tail(st, tail))) return rc;
+      s->dag_nodes += 1;
+    } else {
+      hlu_rkt_scratch sc = s->scratch;
+      sc.list = s->scratch.list + 7 * s->rkt_op0[l];
+      sc.max_ops = L.count;
+      sc.items = s->scratch.items + s->rkt_item0[l];
+      sc.max_items = std::max<int64_t>(s->rkt_items[l], 1);
+      const int my = slot++;
+      auto K = [&](int which, std::vector<cudaGraphNode_t> &d, std::vector<cudaGraphNode_t> &out) -> int {
+        int r = set_deps(st, d);
+        if (r) return r;
+        r = hlu_rkt_phase(&s->ctx, s->rkt, s->parts, L.first, L.count, &sc, my, which, st);
+        if (r) return r;
+        tmp.clear();
+        r = capture_tail(st, tmp);
+        out.insert(out.end(), tmp.begin(), tmp.end());
+        s->dag_nodes += 1;
+        return r;
+      };
+      // plan-time route hints (smem_dim bits): 2 may stack > 64 columns, 4 no
+      // op fits the register warp kernels (every max(m, n) > 64)
+      const bool wide = (L.smem_dim & 2) != 0 || s->ctx.eps == 0.0 || all_routes;
+      const bool no_warp = (L.smem_dim & 4) != 0 && !all_routes;
+      std::vector<cudaGraphNode_t> c;
+      tail.clear();
+      a_tail.clear();
+      b_tail.clear();
+      if ((rc = K(0, deps, c))) return rc;
+      if (!no_warp) {
+        if ((rc = K(1, c, tail))) return rc;
+        if ((rc = K(2, c, tail))) return rc;
+      }
+      if (wide && (rc = K(3, c, tail))) return rc;
+      if ((rc = K(4, c, a_tail))) return rc;
+      if ((rc = K(9, c, a_tail))) return rc;
+      if ((rc = K(5, a_tail, b_tail))) return rc;
+      if ((rc = K(6, a_tail, b_tail))) return rc;
+      if ((rc = K(7, a_tail, b_tail))) return rc;
+      if ((rc = K(8, b_tail, tail))) return rc;
+      if ((rc = K(10, b_tail, tail))) return rc;
+    }
+    tails.insert(tails.end(), tail.begin(), tail.end());
+    tptr[l + 1] = (int64_t)tails.size();
+  }
+  // join: the capturing stream ends behind every launch nothing else waits for
+  deps.clear();
+  for (size_t l = 0; l < nl; ++l)
+    if (!has_succ[l]) deps.insert(deps.end(), tails.begin() + tptr[l], tails.begin() + tptr[l + 1]);
+  if (deps.empty()) deps = root;
+  if ((rc = set_deps(st, deps))) return rc;
+  k_stamp<<<1, 1, 0, st>>>(s->dag_join);
+  return cudaGetLastError() == cudaSuccess ? 0 : -1;
+}
+
 static int run_launches(hlu_schedule *s, cudaStream_t st) {
+  if (!s->dag_ptr.empty()) return run_dag(s, st);
   if (s->comm) return run_sharded(s, st);
   if (!s->wait_d.empty() && !s->stamps) return run_chains(s, st);
   const size_t nl = s->launches.size();
@@ -249,6 +371,12 @@ static void destroy_events(hlu_schedule *s) {
   s->ev_r.clear();
 }
 
+struct DagArgs {
+  const int64_t *dep_ptr;
+  const int32_t *dep_idx;
+  const int64_t *item0, *nitems;  // per launch: first row-block item and item count (truncation launches)
+};
+
 struct ShardArgs {
   hlu_comm *comm;
   const hlu_xfer *xfer_host, *xfer_dev;
@@ -260,7 +388,7 @@ static int create(hlu_schedule **out, const hlu_ctx *ctx, const hlu_launch *laun
                   const hlu_getrf_desc *getrf, const hlu_trsm_desc *trsm, const hlu_gemm_desc *gemm,
                   const hlu_term *terms, hlu_rkt_desc *rkt, const hlu_rkpart *parts, const hlu_rkt_scratch *scratch,
                   const int32_t *wait_dense, const int32_t *wait_rkt, int64_t nlevels, int use_graph, void *stream,
-                  const ShardArgs *sh);
+                  const ShardArgs *sh, const DagArgs *dag = nullptr);
 
 extern "C" int hlu_schedule_create_chains(hlu_schedule **out, const hlu_ctx *ctx, const hlu_launch *launches,
                                           int64_t nlaunch, const hlu_getrf_desc *getrf, const hlu_trsm_desc *trsm,
@@ -285,6 +413,24 @@ extern "C" int hlu_schedule_create_sharded(hlu_schedule **out, const hlu_ctx *ct
                 use_graph, stream, &sh);
 }
 
+// DAG schedule (include/hlu_plan.h hlu_plan_build_dag): launch l waits for the
+// launches dep_idx[dep_ptr[l] .. dep_ptr[l+1]) (all < l); scratch->list holds 7
+// ints per truncation descriptor and scratch->items every row-block item
+// (item0 / nitems: each truncation launch's window, from hlu_rkt_items).
+extern "C" int hlu_schedule_create_dag(hlu_schedule **out, const hlu_ctx *ctx, const hlu_launch *launches,
+                                       int64_t nlaunch, const hlu_getrf_desc *getrf, const hlu_trsm_desc *trsm,
+                                       const hlu_gemm_desc *gemm, const hlu_term *terms, hlu_rkt_desc *rkt,
+                                       const hlu_rkpart *parts, const hlu_rkt_scratch *scratch,
+                                       const int64_t *dep_ptr, const int32_t *dep_idx, const int64_t *item0,
+                                       const int64_t *nitems, void *stream) {
+  if (!dep_ptr || !item0 || !nitems) return -23;
+  const DagArgs dag{dep_ptr, dep_idx, item0, nitems};
+  return create(out, ctx, launches, nlaunch, getrf, trsm, gemm, terms, rkt, parts, scratch, nullptr, nullptr, 0, 1,
+                stream, nullptr, &dag);
+}
+
+extern "C" int64_t hlu_schedule_graph_nodes(const hlu_schedule *s) { return s->dag_nodes; }
+
 // staging doubles the exchange groups of a sharded plan need (the largest group)
 extern "C" int64_t hlu_xfer_staging_doubles(const void *xfer, int64_t n) {
   const hlu_xfer *x = (const hlu_xfer *)xfer;
@@ -297,8 +443,22 @@ static int create(hlu_schedule **out, const hlu_ctx *ctx, const hlu_launch *laun
                   const hlu_getrf_desc *getrf, const hlu_trsm_desc *trsm, const hlu_gemm_desc *gemm,
                   const hlu_term *terms, hlu_rkt_desc *rkt, const hlu_rkpart *parts, const hlu_rkt_scratch *scratch,
                   const int32_t *wait_dense, const int32_t *wait_rkt, int64_t nlevels, int use_graph, void *stream,
-                  const ShardArgs *sh) {
+                  const ShardArgs *sh, const DagArgs *dag) {
   hlu_schedule *s = new hlu_schedule();
+  if (dag) {
+    if (!use_graph) {
+      delete s;
+      return -23;  // the DAG schedule exists only as a CUDA graph
+    }
+    s->dag_ptr.assign(dag->dep_ptr, dag->dep_ptr + nlaunch + 1);
+    s->dag_idx.assign(dag->dep_idx, dag->dep_idx + dag->dep_ptr[nlaunch]);
+    s->rkt_op0.assign(nlaunch, 0);
+    s->rkt_item0.assign(dag->item0, dag->item0 + nlaunch);
+    s->rkt_items.assign(dag->nitems, dag->nitems + nlaunch);
+    for (int64_t i = 0; i < nlaunch; ++i) s->rkt_op0[i] = launches[i].first;
+    if (s->dag_ptr.empty()) s->dag_ptr.push_back(0);
+    cudaMalloc(&s->dag_join, sizeof(unsigned long long));
+  }
   if (sh) {
     s->comm = sh->comm;
     s->d_xfer = sh->xfer_dev;
@@ -359,7 +519,11 @@ static int create(hlu_schedule **out, const hlu_ctx *ctx, const hlu_launch *laun
   for (const hlu_launch &L : s->launches) {
     if (L.kind != HLU_K_RKT32) continue;
     ++s->nrkt;
-    if (L.count > s->scratch.max_ops) {
+    if (!dag && L.count > s->scratch.max_ops) {
+      delete s;
+      return -14;
+    }
+    if (dag && L.first + L.count > s->scratch.max_ops) {  // DAG mode: the lists cover every descriptor
       delete s;
       return -14;
     }
@@ -426,6 +590,7 @@ extern "C" int hlu_schedule_destroy(hlu_schedule *s) {
   if (s->exec) cudaGraphExecDestroy(s->exec);
   if (s->graph) cudaGraphDestroy(s->graph);
   if (s->stamps) cudaFree(s->stamps);
+  if (s->dag_join) cudaFree(s->dag_join);
   for (int i = 0; i < 8; ++i) cudaEventDestroy((cudaEvent_t)s->aux.ev[i]);
   for (int i = 0; i < 4; ++i) cudaStreamDestroy((cudaStream_t)s->aux.side[i]);
   cudaEventDestroy(s->fork);

@@ -80,8 +80,13 @@ class DeviceCall:
             self.d_terms = _dev_bytes(torch, p.terms, self.device)
             self.d_rkt = _dev_bytes(torch, p.rkt, self.device)
             self.d_parts = _dev_bytes(torch, p.parts, self.device)
-            # truncation scratch: per-level counters, op lists, row-block items
-            self.scratch, self._scratch_keep = _native.rkt_scratch(torch, self.device, p.rkt, p.launches)
+            # truncation scratch: per-launch counters, op lists, row-block items
+            self.dag = p.dag_ptr is not None and p.shard is None and use_graph
+            if self.dag:
+                self.scratch, self._scratch_keep, item0, nitems = _native.rkt_scratch_dag(
+                    torch, self.device, p.rkt, p.launches)
+            else:
+                self.scratch, self._scratch_keep = _native.rkt_scratch(torch, self.device, p.rkt, p.launches)
             self.upload()
             self.ctx = _native.HluCtx(
                 self.pool.data_ptr(), self.ranks.data_ptr(), self.log.data_ptr(), self.err.data_ptr(),
@@ -109,6 +114,20 @@ class DeviceCall:
                     1 if use_graph else 0, ctypes.c_void_p(self.stream.cuda_stream),
                 )
                 _native.check(rc, "hlu_schedule_create_sharded")
+            elif self.dag:
+                # the launch DAG: one CUDA graph whose edges are the planner's
+                # launch dependencies (no level barriers)
+                self.chains = False
+                dp = np.ascontiguousarray(p.dag_ptr, dtype=np.int64)
+                di = np.ascontiguousarray(p.dag_idx if len(p.dag_idx) else np.zeros(1, np.int32), dtype=np.int32)
+                rc = lib.hlu_schedule_create_dag(
+                    ctypes.byref(handle), ctypes.byref(self.ctx), launches.ctypes.data, len(launches),
+                    self.d_getrf.data_ptr(), self.d_trsm.data_ptr(), self.d_gemm.data_ptr(),
+                    self.d_terms.data_ptr(), self.d_rkt.data_ptr(), self.d_parts.data_ptr(),
+                    ctypes.byref(self.scratch), dp.ctypes.data, di.ctypes.data, item0.ctypes.data,
+                    nitems.ctypes.data, ctypes.c_void_p(self.stream.cuda_stream),
+                )
+                _native.check(rc, "hlu_schedule_create_dag")
             else:
                 # two chains (dense / truncation) with the planner's cross-chain
                 # waits; HLU_CHAINS=0 keeps a barrier after every level

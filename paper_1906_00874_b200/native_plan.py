@@ -60,6 +60,10 @@ def lib():
         L.hlu_plan_xfer.restype = i64
         L.hlu_plan_op_owners.argtypes = [vp, vp]
         L.hlu_plan_op_owners.restype = ctypes.c_int
+        L.hlu_plan_build_dag.argtypes = [ctypes.POINTER(vp), vp, i64, vp, i64, i32, i64, i64, i32, i64, i32, i64]
+        L.hlu_plan_build_dag.restype = ctypes.c_int
+        L.hlu_plan_dag.argtypes = [vp, vp, vp]
+        L.hlu_plan_dag.restype = i64
         L.hlu_host_pack.argtypes = [vp, i64, vp, ctypes.c_int]
         L.hlu_host_unpack.argtypes = [vp, i64, vp, ctypes.c_int]
         _lib = L
@@ -126,9 +130,9 @@ def cache_dir_default():
         return DEFAULT_CACHE
     return None if d in ("", "0") else d
 _PACKED_ARRAYS = ("getrf", "trsm", "gemm", "terms", "rkt", "parts", "launches", "flop_formula", "flop_coef",
-                  "flop_log", "lu_op_ids", "op_levels", "wait_dense", "wait_rkt")
+                  "flop_log", "lu_op_ids", "op_levels", "wait_dense", "wait_rkt", "dag_ptr", "dag_idx")
 _PACKED_INTS = ("nlevels", "arena_doubles", "nlog", "nranks")
-PLAN_FORMAT = 2  # bump when the packing (Python side) or the npz layout changes
+PLAN_FORMAT = 3  # bump when the packing (Python side) or the npz layout changes
 
 
 def plan_key(nodes, cmds, scalars):
@@ -182,7 +186,17 @@ def load_packed(path):
         return Packed(**kw), int(z["nops"])
 
 
-def plan(layout, commands, split_rows=SPLIT_ROWS, cache_dir=None, shard=None):
+DAG_SLOT_ENV = "HLU_DAG_SLOT_US"  # time-slot width of the DAG schedule in us; "0": level schedule
+DAG_SLOT_US_DEFAULT = 20.0
+
+
+def dag_slot_ns_default():
+    """Slot width (ns) of the default single-GPU schedule: the launch DAG
+    (hlu_plan_build_dag); HLU_DAG_SLOT_US=0 selects the level schedule."""
+    return int(round(float(os.environ.get(DAG_SLOT_ENV, DAG_SLOT_US_DEFAULT)) * 1000.0))
+
+
+def plan(layout, commands, split_rows=SPLIT_ROWS, cache_dir=None, shard=None, dag_slot_ns=None):
     """commands: list of (kind, nodes..., extras) in the planner's terms:
     ("factor", h) | ("solve_lower", l, b) | ("solve_upper", b, u) |
     ("update", c, a, b) | ("fwd", h, name) | ("bwd", h, name) |
@@ -213,26 +227,31 @@ def plan(layout, commands, split_rows=SPLIT_ROWS, cache_dir=None, shard=None):
             raise ValueError(kind)
     if shard is not None:  # (slot_owner, nranks, rank): per-rank plans are not cached
         return _build(layout, nodes, cmds, split_rows, shard)
+    dag = dag_slot_ns_default() if dag_slot_ns is None else int(dag_slot_ns)
     explicit = cache_dir is not None
     cache_dir = cache_dir if explicit else cache_dir_default()
     path = None
     if cache_dir:
         key = plan_key(nodes, cmds, (layout.cap, layout.ident_off, layout.nslots, layout.nrk,
-                                     layout.payload_doubles, split_rows))
+                                     layout.payload_doubles, split_rows, dag))
         path = os.path.join(cache_dir, f"plan_{key[:32]}.npz")
         if os.path.exists(path):
             return load_packed(path)
-    packed, nops = _build(layout, nodes, cmds, split_rows)
+    packed, nops = _build(layout, nodes, cmds, split_rows, dag_slot_ns=dag)
     if path is not None and (explicit or nops >= CACHE_MIN_OPS):
         os.makedirs(cache_dir, exist_ok=True)
         save_packed(path, packed, nops)
     return packed, nops
 
 
-def _build(layout, nodes, cmds, split_rows, shard=None):
+def _build(layout, nodes, cmds, split_rows, shard=None, dag_slot_ns=0):
     L = lib()
     h = ctypes.c_void_p()
-    if shard is None:
+    if shard is None and dag_slot_ns > 0:
+        rc = L.hlu_plan_build_dag(ctypes.byref(h), nodes.ctypes.data, len(nodes), cmds.ctypes.data, len(cmds),
+                                  layout.cap, layout.ident_off, layout.nslots, layout.nrk, layout.payload_doubles,
+                                  int(split_rows), int(dag_slot_ns))
+    elif shard is None:
         rc = L.hlu_plan_build(ctypes.byref(h), nodes.ctypes.data, len(nodes), cmds.ctypes.data, len(cmds),
                               layout.cap, layout.ident_off, layout.nslots, layout.nrk, layout.payload_doubles,
                               int(split_rows))
@@ -273,6 +292,13 @@ def _build(layout, nodes, cmds, split_rows, shard=None):
         wr = np.full(max(nlev, 1), -1, dtype=np.int32)
         if L.hlu_plan_level_waits(h, wd.ctypes.data, wr.ctypes.data) != 0:
             wd = wr = None
+        dag_ptr = dag_idx = None
+        ne = int(L.hlu_plan_dag(h, None, None))
+        if ne >= 0:
+            dag_ptr = np.zeros(nl + 1, dtype=np.int64)
+            dag_idx = np.zeros(max(ne, 1), dtype=np.int32)
+            L.hlu_plan_dag(h, dag_ptr.ctypes.data, dag_idx.ctypes.data)
+            dag_idx = dag_idx[:ne]
         xfer = mask = None
         if shard is not None:
             xfer = np.zeros(max(int(L.hlu_plan_xfer(h, None)), 1), dtype=ir.XFER)
@@ -294,4 +320,5 @@ def _build(layout, nodes, cmds, split_rows, shard=None):
         nranks=max(nrank, 1), lu_op_ids=lu_ops[:nlu], lu_labels=labels, op_levels=lv,
         wait_dense=wd, wait_rkt=wr, xfer=xfer, op_mask=mask,
         shard=None if shard is None else (int(shard[1]), int(shard[2])),
+        dag_ptr=dag_ptr, dag_idx=dag_idx,
     ), nops

@@ -150,6 +150,10 @@ class Packed:
     xfer: np.ndarray = None
     op_mask: np.ndarray = None
     shard: tuple = None  # (nranks, rank)
+    # DAG schedule (native planner, hlu_plan_build_dag): launch l waits for the
+    # launches dag_idx[dag_ptr[l] : dag_ptr[l + 1]]; None = level schedule
+    dag_ptr: np.ndarray = None
+    dag_idx: np.ndarray = None
 
 
 def _view_rec(v):

@@ -33,7 +33,7 @@ def test_factor_plans_identical(name):
     pl = Planner(L)
     pl.factor(h)
     p_py = pack(pl, L.payload_doubles)
-    p_nat, nops = native_plan.plan(L, [("factor", h)], split_rows=0)
+    p_nat, nops = native_plan.plan(L, [("factor", h)], split_rows=0, dag_slot_ns=0)
     assert nops == len(pl.ops)
     _compare(p_py, p_nat)
 
@@ -47,7 +47,7 @@ def test_solve_and_update_plans_identical():
         L = Layout(roots, cap=32)
         pl = Planner(L)
         getattr(pl, cmd[0])(*cmd[1:])
-        _compare(pack(pl, L.payload_doubles), native_plan.plan(L, [cmd], split_rows=0)[0])
+        _compare(pack(pl, L.payload_doubles), native_plan.plan(L, [cmd], split_rows=0, dag_slot_ns=0)[0])
 
 
 def test_vector_solve_plans_identical():
@@ -56,7 +56,7 @@ def test_vector_solve_plans_identical():
     pl = Planner(L)
     pl.forward_vector(h, "x")
     pl.backward_vector(h, "x")
-    _compare(pack(pl, L.payload_doubles), native_plan.plan(L, [("fwd", h, "x"), ("bwd", h, "x")], split_rows=0)[0])
+    _compare(pack(pl, L.payload_doubles), native_plan.plan(L, [("fwd", h, "x"), ("bwd", h, "x")], split_rows=0, dag_slot_ns=0)[0])
 
 
 @pytest.mark.parametrize("name", ["mixed_192", "bem1d_1024", "sphere_1024"])
@@ -71,8 +71,8 @@ def test_split_chains_reproduce_reference(name):
     build, ctl = cases.CASES[name]
     h, _ = build()
     L = Layout(h, cap=32)
-    p, _ = native_plan.plan(L, [("factor", h)], split_rows=16)
-    p0, _ = native_plan.plan(L, [("factor", h)], split_rows=0)
+    p, _ = native_plan.plan(L, [("factor", h)], split_rows=16, dag_slot_ns=0)
+    p0, _ = native_plan.plan(L, [("factor", h)], split_rows=0, dag_slot_ns=0)
     assert len(p.gemm) >= len(p0.gemm)
     pool = np.zeros(L.payload_doubles + p.arena_doubles)
     ranks = np.zeros(p.nranks, np.int32)
@@ -141,7 +141,7 @@ def test_two_chain_waits_reproduce_reference(name, dense_first):
     build, ctl = cases.CASES[name]
     h, _ = build()
     L = Layout(h, cap=32)
-    p, _ = native_plan.plan(L, [("factor", h)], split_rows=16)
+    p, _ = native_plan.plan(L, [("factor", h)], split_rows=16, dag_slot_ns=0)
     assert p.wait_dense is not None and len(p.wait_dense) == p.nlevels
     order = _chain_order(p, dense_first)
     assert sorted(order) == list(range(len(p.launches)))
@@ -162,15 +162,125 @@ def test_plan_cache_round_trip(tmp_path):
     """A cached plan (keyed by the planner's inputs) loads back identical."""
     h, _ = cases.CASES["sphere_1024"][0]()
     L = Layout(h, cap=32)
-    fresh, n0 = native_plan.plan(L, [("factor", h)])
-    first, n1 = native_plan.plan(L, [("factor", h)], cache_dir=str(tmp_path))
+    fresh, n0 = native_plan.plan(L, [("factor", h)], dag_slot_ns=0)
+    first, n1 = native_plan.plan(L, [("factor", h)], cache_dir=str(tmp_path), dag_slot_ns=0)
     files = list(tmp_path.iterdir())
     assert len(files) == 1
-    cached, n2 = native_plan.plan(L, [("factor", h)], cache_dir=str(tmp_path))
+    cached, n2 = native_plan.plan(L, [("factor", h)], cache_dir=str(tmp_path), dag_slot_ns=0)
     assert n0 == n1 == n2
     for p in (first, cached):
         _compare(fresh, p)
         assert np.array_equal(fresh.wait_dense, p.wait_dense) and np.array_equal(fresh.wait_rkt, p.wait_rkt)
     # a different capacity is a different plan
-    native_plan.plan(Layout(h, cap=48), [("factor", h)], cache_dir=str(tmp_path))
+    native_plan.plan(Layout(h, cap=48), [("factor", h)], cache_dir=str(tmp_path), dag_slot_ns=0)
     assert len(list(tmp_path.iterdir())) == 2
+    # so is the DAG schedule of the same structure, and its dependency lists survive the cache
+    d1, _ = native_plan.plan(L, [("factor", h)], cache_dir=str(tmp_path), dag_slot_ns=20000)
+    assert len(list(tmp_path.iterdir())) == 3
+    d2, _ = native_plan.plan(L, [("factor", h)], cache_dir=str(tmp_path), dag_slot_ns=20000)
+    assert d1.dag_ptr is not None and np.array_equal(d1.dag_ptr, d2.dag_ptr) and np.array_equal(d1.dag_idx, d2.dag_idx)
+    assert d1.launches.tobytes() == d2.launches.tobytes()
+
+
+# ---------------------------------------------------------------- DAG schedule
+
+
+def _dag_order(packed, rng, mode):
+    """A launch order the DAG runtime may produce: any topological order of the
+    planner's launch dependencies ("late": always the newest ready launch, i.e.
+    run as far ahead as the dependencies allow; "random": a random ready one)."""
+    nl = len(packed.launches)
+    ptr, idx = packed.dag_ptr, packed.dag_idx
+    indeg = np.diff(ptr).astype(np.int64)
+    succ = [[] for _ in range(nl)]
+    for l in range(nl):
+        for p in idx[ptr[l]:ptr[l + 1]]:
+            assert 0 <= p < l  # dependencies precede their launch
+            succ[int(p)].append(l)
+    ready = [l for l in range(nl) if indeg[l] == 0]
+    order = []
+    while ready:
+        k = len(ready) - 1 if mode == "late" else int(rng.integers(len(ready)))
+        if mode == "late":
+            ready.sort()
+        l = ready.pop(k)
+        order.append(l)
+        for q in succ[l]:
+            indeg[q] -= 1
+            if indeg[q] == 0:
+                ready.append(q)
+    assert len(order) == nl
+    return order
+
+
+@pytest.mark.parametrize("name", ["mixed_192", "mixed_256_kmax", "dense2x2_256_r3", "bem1d_1024", "sphere_1024"])
+@pytest.mark.parametrize("slot_us", [5, 20, 200])
+def test_dag_schedule_reproduces_level_schedule(name, slot_us):
+    """The launch dependencies of the DAG schedule are sufficient: the launches
+    executed in adversarial topological orders (newest ready first, random)
+    leave the pool, ranks and flop log bit-identical to the level schedule
+    (same ops, same per-destination order; temps may share arena blocks)."""
+    import dataclasses
+
+    from ir_exec import CpuMachine
+    from paper_1906_00874_b200.pool import fill_pool
+    from paper_1906_00874_b200.schedule import effective_flops
+
+    g = cases.golden(name)
+    build, ctl = cases.CASES[name]
+    h, _ = build()
+    L = Layout(h, cap=32)
+
+    def run(p, order=None):
+        pool = np.zeros(L.payload_doubles + p.arena_doubles)
+        ranks = np.zeros(p.nranks, np.int32)
+        fill_pool(L, pool, ranks)
+        M = CpuMachine(pool, ranks, p.nlog, ctl[0], ctl[1])
+        M.run(p if order is None else dataclasses.replace(p, launches=p.launches[order]))
+        return pool[:L.payload_doubles].copy(), ranks.copy(), M
+
+    p0, n0 = native_plan.plan(L, [("factor", h)], split_rows=16, dag_slot_ns=0)
+    ref_pool, ref_ranks, M0 = run(p0)
+    p, n1 = native_plan.plan(L, [("factor", h)], split_rows=16, dag_slot_ns=slot_us * 1000)
+    assert n0 == n1 and p.dag_ptr is not None and len(p.dag_ptr) == len(p.launches) + 1
+    assert int(p.launches["count"].sum()) == int(p0.launches["count"].sum())
+    rng = np.random.default_rng(7)
+    for mode in ("late", "random", "random"):
+        order = _dag_order(p, rng, mode)
+        pool, ranks, M = run(p, order)
+        assert np.array_equal(ranks, ref_ranks)
+        assert pool.tobytes() == ref_pool.tobytes()
+        assert effective_flops(p, M.log) == effective_flops(p0, M0.log)
+    if g is not None and "flops" in g:
+        assert abs(effective_flops(p, M.log) - float(g["flops"])) <= 1e-12 * float(g["flops"])
+
+
+def test_dag_schedule_overlaps_levels():
+    """The point of the DAG: launches of different time slots are independent
+    of one another where the level schedule put a barrier (the longest
+    dependency chain is shorter than the launch list)."""
+    h, _ = cases.CASES["sphere_1024"][0]()
+    L = Layout(h, cap=32)
+    p, _ = native_plan.plan(L, [("factor", h)], dag_slot_ns=20000)
+    nl = len(p.launches)
+    depth = np.zeros(nl, dtype=np.int64)
+    for l in range(nl):
+        d = p.dag_idx[p.dag_ptr[l]:p.dag_ptr[l + 1]]
+        depth[l] = 1 + (depth[d].max() if len(d) else 0)
+    assert depth.max() < nl
+    # launch keys are topological
+    assert np.all(np.diff(p.launches["level"].astype(np.int64)) >= 0)
+
+
+@pytest.mark.parametrize("name", ["mixed_192", "mixed_256_kmax", "bem1d_1024", "sphere_1024"])
+@pytest.mark.parametrize("slot_us", [5, 40])
+def test_dag_dependencies_cover_memory_conflicts(name, slot_us):
+    """Footprint check from the packed descriptors alone (tests/dag_check.py):
+    launches that conflict in the pool (payloads, temp arena incl. block
+    reuse, truncation workspaces) or in the rank table are ordered by the DAG."""
+    import dag_check
+
+    h, _ = cases.CASES[name][0]()
+    L = Layout(h, cap=32)
+    p, _ = native_plan.plan(L, [("factor", h)], split_rows=16, dag_slot_ns=slot_us * 1000)
+    assert dag_check.violations(p) == []
