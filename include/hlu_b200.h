@@ -214,6 +214,24 @@ int hlu_schedule_create_chains(hlu_schedule **out, const hlu_ctx *ctx, const hlu
                                const hlu_term *terms, hlu_rkt_desc *rkt, const hlu_rkpart *parts,
                                const hlu_rkt_scratch *scratch, const int32_t *wait_dense, const int32_t *wait_rkt,
                                int64_t nlevels, int use_graph, void *stream);
+/* The DAG schedule (include/hlu_plan.h hlu_plan_build_dag) as one CUDA graph whose
+ * edges are the planner's launch dependencies: launch l waits for the launches
+ * dep_idx[dep_ptr[l] .. dep_ptr[l+1]) (all < l) and for nothing else, so launches of
+ * different time slots overlap where the level schedule put a barrier (the GPU
+ * analogue of the reference runtime's region dependencies, runtime.py:443-556).
+ * Truncation launches run concurrently, each in its own window of the scratch:
+ * scratch->list holds 7 ints per truncation descriptor (window at 7 * first,
+ * max_ops = descriptor count), scratch->items every row-block item (item0 / nitems:
+ * the window of each truncation launch, from hlu_rkt_items), scratch->counts 8 ints
+ * per truncation launch.  prio (may be NULL): 0 .. 2 per launch, kernels of
+ * higher-priority launches are scheduled first when SMs are contended. */
+int hlu_schedule_create_dag(hlu_schedule **out, const hlu_ctx *ctx, const hlu_launch *launches, int64_t nlaunch,
+                            const hlu_getrf_desc *getrf, const hlu_trsm_desc *trsm, const hlu_gemm_desc *gemm,
+                            const hlu_term *terms, hlu_rkt_desc *rkt, const hlu_rkpart *parts,
+                            const hlu_rkt_scratch *scratch, const int64_t *dep_ptr, const int32_t *dep_idx,
+                            const int64_t *item0, const int64_t *nitems, const int32_t *prio, void *stream);
+/* kernel nodes the DAG capture issued (diagnostics) */
+int64_t hlu_schedule_graph_nodes(const hlu_schedule *s);
 /* --- multi-GPU: owner-computes H-LU over a communicator (NCCL, NVLink) --- */
 typedef struct hlu_comm hlu_comm;
 struct hlu_xfer_s;

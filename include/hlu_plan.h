@@ -68,6 +68,25 @@ int hlu_plan_build_sharded(hlu_plan **out, const hlu_plan_node *nodes, int64_t n
                            int64_t ncmds, int32_t cap, int64_t ident_off, int64_t nslots, int32_t nrk,
                            int64_t arena_base, int32_t split_rows, const int32_t *slot_owner, int32_t nranks,
                            int32_t rank);
+/* DAG schedule (replaces the level barriers; the GPU analogue of the paper's
+ * task DAG with region dependencies, PAPER.md:598-670 / runtime.py:443-556): a
+ * hazard sweep in model time (per-op latency model) gives every op a start
+ * time; ops of one kernel class whose start falls into the same slot_ns window
+ * form a launch, and every launch lists the launches it depends on (RAW / WAR /
+ * WAW on skeleton slots and temps, arena-block hand-over).  hlu_launch.level is
+ * then the launch-group key in topological order (no barrier semantics) and
+ * truncation launches carry a route hint in smem_dim (bit 4: no op with
+ * max(m, n) <= 64, the register warp kernels are not launched).
+ * slot_ns <= 0 is hlu_plan_build. */
+int hlu_plan_build_dag(hlu_plan **out, const hlu_plan_node *nodes, int64_t nnodes, const hlu_plan_cmd *cmds,
+                       int64_t ncmds, int32_t cap, int64_t ident_off, int64_t nslots, int32_t nrk, int64_t arena_base,
+                       int32_t split_rows, int64_t slot_ns);
+/* dependency lists of a DAG plan: launch l waits for the launches
+ * idx[ptr[l] .. ptr[l+1]) (all < l); ptr has launches + 1 entries.  Returns the
+ * edge count (ptr / idx may be NULL), -1 for a level plan. */
+int64_t hlu_plan_dag(const hlu_plan *p, int64_t *ptr, int32_t *idx);
+/* per launch: model-time slack in ns (0 = on the model's critical path) */
+int hlu_plan_dag_slack(const hlu_plan *p, int64_t *slack_ns);
 const char *hlu_plan_error(const hlu_plan *p);
 /* sizes[14]: getrf, trsm, gemm, terms, rkt, parts, launches, ops, levels, arena doubles,
  *            log entries, rank slots, LU count, temps */

@@ -107,7 +107,7 @@ def lib():
     L.hlu_schedule_create_chains.argtypes = [ctypes.POINTER(vp), ctypes.POINTER(HluCtx), vp, i64,
                                              vp, vp, vp, vp, vp, vp, sp, vp, vp, i64, i32, vp]
     L.hlu_schedule_create_dag.argtypes = [ctypes.POINTER(vp), ctypes.POINTER(HluCtx), vp, i64,
-                                          vp, vp, vp, vp, vp, vp, sp, vp, vp, vp, vp, vp]
+                                          vp, vp, vp, vp, vp, vp, sp, vp, vp, vp, vp, vp, vp]
     L.hlu_schedule_create_dag.restype = ctypes.c_int
     L.hlu_schedule_graph_nodes.argtypes = [vp]
     L.hlu_schedule_graph_nodes.restype = i64

@@ -958,6 +958,7 @@ struct Planner {
   std::vector<int64_t> op_start, op_ready;  // model ns: start, and when dependants may start
   std::vector<int64_t> dag_ptr;             // per launch: [dag_ptr[l], dag_ptr[l+1]) into dag_idx
   std::vector<int32_t> dag_idx;             // predecessor launches
+  std::vector<int64_t> dag_slack;           // per launch: model-time slack (ns)
   std::vector<int32_t> op_rec[2];           // launch record(s) holding each op (-1: none)
 
   int rkt_class(const RktP &r) const {
@@ -1226,6 +1227,23 @@ struct Planner {
       }
       dag_ptr[l + 1] = (int64_t)dag_idx.size();
     }
+    // slack of every launch in model time (latest finish that keeps the model
+    // makespan - earliest finish): the runtime gives launches without slack a
+    // higher scheduling priority than the ones that can wait
+    std::vector<int64_t> dur(nlaunch, 0), est(nlaunch, 0), lft(nlaunch, 0);
+    for (int64_t l = 0; l < nlaunch; ++l)
+      for (int64_t q = lcount[l]; q < lcount[l + 1]; ++q) dur[l] = std::max(dur[l], op_cost_ns(ops[lops[q]]));
+    int64_t span = 0;
+    for (int64_t l = 0; l < nlaunch; ++l) {
+      for (int64_t e = dag_ptr[l]; e < dag_ptr[l + 1]; ++e) est[l] = std::max(est[l], est[dag_idx[e]] + dur[dag_idx[e]]);
+      span = std::max(span, est[l] + dur[l]);
+    }
+    std::fill(lft.begin(), lft.end(), span);
+    for (int64_t l = nlaunch - 1; l >= 0; --l)
+      for (int64_t e = dag_ptr[l]; e < dag_ptr[l + 1]; ++e)
+        lft[dag_idx[e]] = std::min(lft[dag_idx[e]], lft[l] - dur[l]);
+    dag_slack.assign(nlaunch, 0);
+    for (int64_t l = 0; l < nlaunch; ++l) dag_slack[l] = lft[l] - est[l] - dur[l];
   }
 
   // Diagnostics (HLU_PLAN_CP=1): weighted critical path of the op DAG under a
@@ -1859,7 +1877,9 @@ struct Planner {
       L.level = (int32_t)r.lv;
       if (r.kind == HLU_K_RKT32) {
         L.smem_dim = (r.dep ? 1 : 0) | (r.dim > RK_KMAX ? 2 : 0);  // bit 2: may take the wide path
-        if (dag_slot_ns && r.min_mn > 64) L.smem_dim |= 4;  // no op fits the register warp kernels
+        if (dag_slot_ns) {  // route hints of the DAG runtime (include/hlu_b200.h HLU_RKT_HINT_*)
+          if (r.min_mn > 64) L.smem_dim |= 4;      // no op fits the register warp kernels
+        }
         o_launch.push_back(L);
       } else {
         L.smem_dim = r.dim;
@@ -2066,6 +2086,13 @@ extern "C" int64_t hlu_plan_dag(const hlu_plan *p, int64_t *ptr, int32_t *idx) {
   if (ptr) std::memcpy(ptr, P.dag_ptr.data(), P.dag_ptr.size() * sizeof(int64_t));
   if (idx && !P.dag_idx.empty()) std::memcpy(idx, P.dag_idx.data(), P.dag_idx.size() * sizeof(int32_t));
   return (int64_t)P.dag_idx.size();
+}
+
+extern "C" int hlu_plan_dag_slack(const hlu_plan *p, int64_t *slack_ns) {
+  const Planner &P = p->P;
+  if (P.dag_ptr.empty()) return -1;
+  if (!P.dag_slack.empty()) std::memcpy(slack_ns, P.dag_slack.data(), P.dag_slack.size() * sizeof(int64_t));
+  return 0;
 }
 
 extern "C" const char *hlu_plan_error(const hlu_plan *p) { return p->error.c_str(); }

@@ -670,12 +670,10 @@ struct StackedR {  // the blocks' R factors stacked: block b at R + b K K (ld K)
 // routed: small ops (max(m, n) <= 64, K <= 16) to the warp kernels, the rest
 // (and the ADD shortcuts / empty recompressions) to the CTA phases, whose row
 // blocks become work items.
-__global__ void k_rkt_classify(hlu_ctx c, const hlu_rkt_desc *__restrict__ d, const hlu_rkpart *__restrict__ parts,
-                               int64_t first, int count, hlu_rkt_scratch s, int slot) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= count) return;
-  const int op = (int)(first + i);
-  const hlu_rkt_desc o = d[op];
+// the stacked rank of op o from the current ranks of its parts, logged as
+// (k1, k2) for ADD and (K, 0) for RECOMPRESS (one thread per op)
+__device__ __forceinline__ int log_stacked_rank(const hlu_ctx &c, const hlu_rkt_desc &o, const hlu_rkpart *parts,
+                                                int *k1o, int *k2o) {
   int K = 0, k1 = 0, k2 = 0;
   for (int p = 0; p < o.part_count; ++p) {
     const hlu_view v = parts[o.part_begin + p].a;
@@ -687,6 +685,20 @@ __global__ void k_rkt_classify(hlu_ctx c, const hlu_rkt_desc *__restrict__ d, co
   const bool add = o.mode == HLU_RK_ADD;
   c.log[o.log] = add ? k1 : K;
   c.log[o.log + 1] = add ? k2 : 0;
+  *k1o = k1;
+  *k2o = k2;
+  return K;
+}
+
+__global__ void k_rkt_classify(hlu_ctx c, const hlu_rkt_desc *__restrict__ d, const hlu_rkpart *__restrict__ parts,
+                               int64_t first, int count, hlu_rkt_scratch s, int slot) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= count) return;
+  const int op = (int)(first + i);
+  const hlu_rkt_desc o = d[op];
+  int k1, k2;
+  const int K = log_stacked_rank(c, o, parts, &k1, &k2);
+  const bool add = o.mode == HLU_RK_ADD;
   int32_t *cnt = s.counts + RK_CNT * slot;
   if ((add && (k1 == 0 || k2 == 0)) || K == 0) {
     s.list[RK_SEG_BIG * s.max_ops + atomicAdd(&cnt[RK_SEG_BIG], 1)] = op;
@@ -1196,12 +1208,11 @@ struct RkB {
   static size_t smem() { return (size_t)(2 * BUF + 2 * KM * KM + 3 * KM) * sizeof(double); }
 };
 
-template <int KM>
-__global__ void __launch_bounds__(RkB<KM>::NT)
-    k_rkt_b(hlu_ctx c, const hlu_rkt_desc *__restrict__ d, const hlu_rkpart *__restrict__ parts, hlu_rkt_scratch sc,
-            int slot) {
-  constexpr int BUF = RkB<KM>::BUF, NT = RkB<KM>::NT, NW = NT / 32;
-  extern __shared__ double sm[];
+// One op of the CTA path by one CTA of NT threads (sm: RkB<KM>::smem() bytes);
+// returns at once for the ops of the other core kernels (K range, k_rkt_bw).
+template <int KM, int NT>
+__device__ void rkt_b_op(const hlu_ctx &c, const hlu_rkt_desc &o, const hlu_rkpart *parts, double *sm) {
+  constexpr int BUF = RkB<KM>::BUF, NW = NT / 32;
   double *B0 = sm;              // BUF   side-A buffer, later G | V
   double *B1 = B0 + BUF;        // BUF   side-B buffer, later XT
   double *RA = B1 + BUF;        // KM*KM R_a, later W_a
@@ -1216,17 +1227,14 @@ __global__ void __launch_bounds__(RkB<KM>::NT)
   __shared__ unsigned char pairs_a[(KM - 1) * (KM / 2)], pairs_b[(KM - 1) * (KM / 2)];
   __shared__ int s_kk, s_ra, s_rb;
   const int tid = threadIdx.x, wq = tid >> 5;
-  const int nbig = sc.counts[RK_CNT * slot + RK_SEG_BIG];
-  const int32_t *lbig = sc.list + RK_SEG_BIG * sc.max_ops;
-  for (int idx = blockIdx.x; idx < nbig; idx += gridDim.x) {
-    const hlu_rkt_desc o = d[lbig[idx]];
+  {
     bool shortcut;
     const int K = logged_K(c, o, &shortcut);
     const int m = o.m, n = o.n;
     double *outA = c.pool + o.out_a;
     double *outB = c.pool + o.out_b;
     if (shortcut) {
-      if (KM != 32) continue;
+      if (KM != 32) return;
       load_parts(c, o, parts, P);
       const PartInfo &src = (P[1].k == 0) ? P[0] : P[1];
       int kk = src.k;
@@ -1245,17 +1253,17 @@ __global__ void __launch_bounds__(RkB<KM>::NT)
         c.log[o.log + 2] = kk;
       }
       __syncthreads();
-      continue;
+      return;
     }
     if (K == 0) {
       if (KM == 32 && tid == 0) {
         c.ranks[o.out_slot] = 0;
         c.log[o.log + 2] = 0;
       }
-      continue;
+      return;
     }
-    if ((KM == 32) != (K <= 32)) continue;
-    if (K <= 16 && m <= RK_BR && n <= RK_BR) continue;  // k_rkt_bw
+    if ((KM == 32) != (K <= 32)) return;
+    if (K <= 16 && m <= RK_BR && n <= RK_BR) return;  // k_rkt_bw
     BPROF_START();
     const rk_side_t sa = rk_side(m, K), sb = rk_side(n, K);
     double *wsA = c.pool + o.ws;
@@ -1397,6 +1405,20 @@ __global__ void __launch_bounds__(RkB<KM>::NT)
   }
 }
 
+template <int KM>
+__global__ void __launch_bounds__(RkB<KM>::NT)
+    k_rkt_b(hlu_ctx c, const hlu_rkt_desc *__restrict__ d, const hlu_rkpart *__restrict__ parts, hlu_rkt_scratch sc,
+            int slot) {
+  extern __shared__ double sm[];
+  const int nbig = sc.counts[RK_CNT * slot + RK_SEG_BIG];
+  const int32_t *lbig = sc.list + RK_SEG_BIG * sc.max_ops;
+  for (int idx = blockIdx.x; idx < nbig; idx += gridDim.x) {
+    const hlu_rkt_desc o = d[lbig[idx]];
+    rkt_b_op<KM, RkB<KM>::NT>(c, o, parts, sm);
+    __syncthreads();
+  }
+}
+
 // ---------------------------------------------------------------- phase B, one warp per op
 
 // CTA-path ops with K <= 16 and single-block factors: the core SVD of the two
@@ -1409,45 +1431,53 @@ struct BwCfg {
   static size_t smem() { return (size_t)WPC * PER * sizeof(double); }
 };
 
+// one op by one warp (sw: BwCfg<KB>::PER doubles, perm: KB ints)
+template <int KB>
+__device__ void rkt_bw_op(const hlu_ctx &c, const hlu_rkt_desc &o, double *sw, int *perm, int l) {
+  constexpr int LDW = BwCfg<KB>::LDW;
+  double *Rx = sw;
+  double *Ry = Rx + KB * KB;
+  double *Wx = Ry + KB * KB;
+  double *Wy = Wx + KB * LDW;
+  bool shortcut;
+  const int K = logged_K(c, o, &shortcut);
+  const rk_side_t sa = rk_side(o.m, K), sb = rk_side(o.n, K);
+  double *wsA = c.pool + o.ws;
+  double *wsB = wsA + sa.total;
+  for (int e = l; e < K * K; e += 32) {
+    Rx[e] = wsA[sa.off_R + e];
+    Ry[e] = wsB[sb.off_R + e];
+  }
+  __syncwarp();
+  const int kk = r_core<KB>(Rx, K, Ry, K, K, c, o.cap, Wx, Wy, perm, l);
+  double *Za = wsA + sa.off_Z, *Zb = wsB + sb.off_Z;
+  for (int e = l; e < sa.zrows * kk; e += 32) {
+    const int i = e % sa.zrows, j = e / sa.zrows;
+    Za[e] = Wx[perm[j] * LDW + i];
+  }
+  for (int e = l; e < sb.zrows * kk; e += 32) {
+    const int i = e % sb.zrows, j = e / sb.zrows;
+    Zb[e] = Wy[perm[j] * LDW + i];
+  }
+  if (l == 0) {
+    c.ranks[o.out_slot] = kk;
+    c.log[o.log + 2] = kk;
+  }
+}
+
 template <int KB>
 __global__ void __launch_bounds__(BwCfg<KB>::WPC * 32)
     k_rkt_bw(hlu_ctx c, const hlu_rkt_desc *__restrict__ d, hlu_rkt_scratch s, int slot) {
-  constexpr int WPC = BwCfg<KB>::WPC, LDW = BwCfg<KB>::LDW;
+  constexpr int WPC = BwCfg<KB>::WPC;
   extern __shared__ double sm[];
   __shared__ int perm[WPC][KB];
   const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
   double *Rx = sm + w * BwCfg<KB>::PER;
-  double *Ry = Rx + KB * KB;
-  double *Wx = Ry + KB * KB;
-  double *Wy = Wx + KB * LDW;
   const int n = s.counts[RK_CNT * slot + RK_SEG_C16];
   const int32_t *lst = s.list + RK_SEG_C16 * s.max_ops;
   for (int idx = blockIdx.x * WPC + w; idx < n; idx += gridDim.x * WPC) {
     const hlu_rkt_desc o = d[lst[idx]];
-    bool shortcut;
-    const int K = logged_K(c, o, &shortcut);
-    const rk_side_t sa = rk_side(o.m, K), sb = rk_side(o.n, K);
-    double *wsA = c.pool + o.ws;
-    double *wsB = wsA + sa.total;
-    for (int e = l; e < K * K; e += 32) {
-      Rx[e] = wsA[sa.off_R + e];
-      Ry[e] = wsB[sb.off_R + e];
-    }
-    __syncwarp();
-    const int kk = r_core<KB>(Rx, K, Ry, K, K, c, o.cap, Wx, Wy, perm[w], l);
-    double *Za = wsA + sa.off_Z, *Zb = wsB + sb.off_Z;
-    for (int e = l; e < sa.zrows * kk; e += 32) {
-      const int i = e % sa.zrows, j = e / sa.zrows;
-      Za[e] = Wx[perm[w][j] * LDW + i];
-    }
-    for (int e = l; e < sb.zrows * kk; e += 32) {
-      const int i = e % sb.zrows, j = e / sb.zrows;
-      Zb[e] = Wy[perm[w][j] * LDW + i];
-    }
-    if (l == 0) {
-      c.ranks[o.out_slot] = kk;
-      c.log[o.log + 2] = kk;
-    }
+    rkt_bw_op<KB>(c, o, Rx, perm[w], l);
     __syncwarp();
   }
 }
@@ -1705,23 +1735,19 @@ __global__ void __launch_bounds__(RW_NT)
 
 // BIG: the large-buffer row blocks (see k_rkt_a); their moving block holds
 // RK_TBUF doubles, so the kept columns go through in groups
+// one row block of phase C by one CTA of HLU_NT threads (sm: smem_c(BIG) bytes)
 template <bool BIG>
-__global__ void __launch_bounds__(HLU_NT)
-    k_rkt_c(hlu_ctx c, const hlu_rkt_desc *__restrict__ d, hlu_rkt_scratch s, int slot) {
+__device__ void rkt_c_item(const hlu_ctx &c, const hlu_rkt_desc &o, const hlu_rkt_item it, double *sm) {
   constexpr int TB = BIG ? RK_TBUF : RK_BUFS, VB = BIG ? RK_BUFA : RK_BUFS;
-  extern __shared__ double sm[];
   double *T = sm;        // TB moving block
   double *VS = T + TB;   // VB staged reflectors
   double *tq = VS + VB;  // RK_KMAX
   const int tid = threadIdx.x;
-  const int nitems = s.counts[RK_CNT * slot + (BIG ? RK_CNT_BIGITEMS : RK_CNT_ITEMS)];
-  for (int idx = blockIdx.x; idx < nitems; idx += gridDim.x) {
-    const hlu_rkt_item it = BIG ? s.items[s.max_items - 1 - idx] : s.items[idx];
-    const hlu_rkt_desc o = d[it.op];
+  {
     bool shortcut;
     const int K = logged_K(c, o, &shortcut);
     const int kk = c.log[o.log + 2];
-    if (kk <= 0) continue;
+    if (kk <= 0) return;
     const bool left = it.side == 0;
     const int M = left ? o.m : o.n;
     const rk_side_t sa = rk_side(o.m, K);
@@ -1737,6 +1763,17 @@ __global__ void __launch_bounds__(HLU_NT)
       apply_chain<true>(rows, K, sd.ch, min(grp, kk - c0), ws + sd.off_Z + it.block * K + (int64_t)c0 * sd.zrows,
                         sd.zrows, rb, T, VS, tq, ws + it.block * sd.blk, out + (int64_t)c0 * M, M, all);
     }
+  }
+}
+
+template <bool BIG>
+__global__ void __launch_bounds__(HLU_NT)
+    k_rkt_c(hlu_ctx c, const hlu_rkt_desc *__restrict__ d, hlu_rkt_scratch s, int slot) {
+  extern __shared__ double sm[];
+  const int nitems = s.counts[RK_CNT * slot + (BIG ? RK_CNT_BIGITEMS : RK_CNT_ITEMS)];
+  for (int idx = blockIdx.x; idx < nitems; idx += gridDim.x) {
+    const hlu_rkt_item it = BIG ? s.items[s.max_items - 1 - idx] : s.items[idx];
+    rkt_c_item<BIG>(c, d[it.op], it, sm);
   }
 }
 

@@ -7,6 +7,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <algorithm>
+#include <chrono>
 #include <cstring>
 #include <vector>
 
@@ -61,6 +62,10 @@ struct hlu_schedule {
   std::vector<int64_t> rkt_op0, rkt_item0, rkt_items;  // per launch (truncation launches only)
   int64_t dag_nodes = 0;
   unsigned long long *dag_join = nullptr;  // written by the graph's last node
+  std::vector<int32_t> dag_prio;           // per launch: index into dag_q
+  cudaStream_t dag_q[3] = {nullptr, nullptr, nullptr};  // capture streams by priority (0: the caller's)
+  cudaEvent_t dag_ev[2] = {nullptr, nullptr};
+  std::vector<cudaGraphExec_t> dag_exec;   // one graph per chunk of launches, replayed in order
 };
 
 __global__ void k_stamp(unsigned long long *slot) {
@@ -228,32 +233,54 @@ static int set_deps(cudaStream_t st, std::vector<cudaGraphNode_t> &deps) {
              : -21;
 }
 
-static int run_dag(hlu_schedule *s, cudaStream_t st) {
-  const size_t nl = s->launches.size();
+// Launches [l0, l1) as one captured graph.  The DAG is cut into chunks of
+// consecutive launches (launch order is topological), one CUDA graph each,
+// replayed back to back on the stream: instantiating one graph of several
+// hundred thousand nodes takes minutes (measured: 535k nodes, 117 s), a
+// chunk of ~10k nodes a fraction of a second.  Dependencies on launches of
+// earlier chunks are implied by the stream order; the only cost is one
+// drain of the in-flight launches per chunk boundary.
+static int run_dag_chunk(hlu_schedule *s, cudaStream_t st, size_t l0, size_t l1, int &slot) {
+  const size_t nl = l1 - l0;
   std::vector<cudaGraphNode_t> root, deps, tail, a_tail, b_tail, tmp;
-  cudaMemsetAsync(s->scratch.counts, 0, 8 * sizeof(int32_t) * std::max(s->nrkt, 1), st);
+  if (l0 == 0) cudaMemsetAsync(s->scratch.counts, 0, 8 * sizeof(int32_t) * std::max(s->nrkt, 1), st);
+  else k_stamp<<<1, 1, 0, st>>>(s->dag_join);
   int rc = capture_tail(st, root);
   if (rc) return rc;
+  // launches without slack are captured from higher-priority streams (their
+  // kernel nodes keep the stream's priority): when SMs are contended the block
+  // scheduler serves the critical chain first
+  cudaStream_t qs[3] = {st, s->dag_q[1] ? s->dag_q[1] : st, s->dag_q[2] ? s->dag_q[2] : st};
+  cudaEventRecord(s->fork, st);
+  for (int k = 1; k < 3; ++k)
+    if (qs[k] != st) cudaStreamWaitEvent(qs[k], s->fork, 0);
+  const cudaStream_t origin = st;
   std::vector<int64_t> tptr(nl + 1, 0);
   std::vector<cudaGraphNode_t> tails;
   tails.reserve(nl * 2);
   std::vector<char> has_succ(nl, 0);
-  int slot = 0;
   static const bool all_routes = getenv("HLU_RKT_ALL_ROUTES") && getenv("HLU_RKT_ALL_ROUTES")[0] == '1';
-  for (size_t l = 0; l < nl; ++l) {
+  for (size_t l = l0; l < l1; ++l) {
     const hlu_launch &L = s->launches[l];
     deps.clear();
     for (int64_t e = s->dag_ptr[l]; e < s->dag_ptr[l + 1]; ++e) {
       const int32_t p = s->dag_idx[e];
       if (p < 0 || (size_t)p >= l) return -22;
-      has_succ[p] = 1;
-      deps.insert(deps.end(), tails.begin() + tptr[p], tails.begin() + tptr[p + 1]);
+      if ((size_t)p < l0) continue;  // an earlier chunk: done before this graph starts
+      has_succ[p - l0] = 1;
+      deps.insert(deps.end(), tails.begin() + tptr[p - l0], tails.begin() + tptr[p - l0 + 1]);
     }
     if (deps.empty()) deps = root;
+    st = qs[s->dag_prio.empty() ? 0 : s->dag_prio[l]];
     if (L.count <= 0) {  // nothing to run: successors wait for the predecessors directly
       tails.insert(tails.end(), deps.begin(), deps.end());
-      tptr[l + 1] = (int64_t)tails.size();
+      tptr[l - l0 + 1] = (int64_t)tails.size();
       continue;
+    }
+    if (s->stamps) {  // diagnostics: when the launch became ready (its dependencies done)
+      if ((rc = set_deps(st, deps))) return rc;
+      k_stamp<<<1, 1, 0, st>>>(s->stamps + 2 * l);
+      if ((rc = capture_tail(st, deps))) return rc;
     }
     if (L.kind != HLU_K_RKT32) {
       if ((rc = set_deps(st, deps))) return rc;
@@ -287,35 +314,63 @@ static int run_dag(hlu_schedule *s, cudaStream_t st) {
       tail.clear();
       a_tail.clear();
       b_tail.clear();
-      if ((rc = K(0, deps, c))) return rc;
-      if (!no_warp) {
-        if ((rc = K(1, c, tail))) return rc;
-        if ((rc = K(2, c, tail))) return rc;
+      {
+        if ((rc = K(0, deps, c))) return rc;
+        if (!no_warp) {
+          if ((rc = K(1, c, tail))) return rc;
+          if ((rc = K(2, c, tail))) return rc;
+        }
+        if (wide && (rc = K(3, c, tail))) return rc;
+        if ((rc = K(4, c, a_tail))) return rc;
+        if ((rc = K(9, c, a_tail))) return rc;
+        if ((rc = K(5, a_tail, b_tail))) return rc;
+        if ((rc = K(6, a_tail, b_tail))) return rc;
+        if ((rc = K(7, a_tail, b_tail))) return rc;
+        if ((rc = K(8, b_tail, tail))) return rc;
+        if ((rc = K(10, b_tail, tail))) return rc;
       }
-      if (wide && (rc = K(3, c, tail))) return rc;
-      if ((rc = K(4, c, a_tail))) return rc;
-      if ((rc = K(9, c, a_tail))) return rc;
-      if ((rc = K(5, a_tail, b_tail))) return rc;
-      if ((rc = K(6, a_tail, b_tail))) return rc;
-      if ((rc = K(7, a_tail, b_tail))) return rc;
-      if ((rc = K(8, b_tail, tail))) return rc;
-      if ((rc = K(10, b_tail, tail))) return rc;
+    }
+    if (s->stamps) {  // ... and when its last kernel ended
+      if ((rc = set_deps(st, tail))) return rc;
+      k_stamp<<<1, 1, 0, st>>>(s->stamps + 2 * l + 1);
+      if ((rc = capture_tail(st, tail))) return rc;
     }
     tails.insert(tails.end(), tail.begin(), tail.end());
-    tptr[l + 1] = (int64_t)tails.size();
+    tptr[l - l0 + 1] = (int64_t)tails.size();
   }
   // join: the capturing stream ends behind every launch nothing else waits for
   deps.clear();
   for (size_t l = 0; l < nl; ++l)
     if (!has_succ[l]) deps.insert(deps.end(), tails.begin() + tptr[l], tails.begin() + tptr[l + 1]);
   if (deps.empty()) deps = root;
+  {  // a graph node takes a bounded number of dependencies comfortably: join the sinks through a tree
+    const size_t fan = 64;
+    while (deps.size() > fan) {
+      std::vector<cudaGraphNode_t> next;
+      for (size_t b = 0; b < deps.size(); b += fan) {
+        std::vector<cudaGraphNode_t> part(deps.begin() + b, deps.begin() + std::min(deps.size(), b + fan));
+        if ((rc = set_deps(origin, part))) return rc;
+        k_stamp<<<1, 1, 0, origin>>>(s->dag_join);
+        tmp.clear();
+        if ((rc = capture_tail(origin, tmp))) return rc;
+        next.insert(next.end(), tmp.begin(), tmp.end());
+      }
+      deps.swap(next);
+    }
+  }
+  st = origin;
+  for (int k = 1; k < 3; ++k) {  // the priority streams rejoin the origin behind the sinks
+    if (qs[k] == st) continue;
+    if ((rc = set_deps(qs[k], deps))) return rc;
+    cudaEventRecord(s->dag_ev[k - 1], qs[k]);
+    cudaStreamWaitEvent(st, s->dag_ev[k - 1], 0);
+  }
   if ((rc = set_deps(st, deps))) return rc;
   k_stamp<<<1, 1, 0, st>>>(s->dag_join);
   return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }
 
 static int run_launches(hlu_schedule *s, cudaStream_t st) {
-  if (!s->dag_ptr.empty()) return run_dag(s, st);
   if (s->comm) return run_sharded(s, st);
   if (!s->wait_d.empty() && !s->stamps) return run_chains(s, st);
   const size_t nl = s->launches.size();
@@ -375,6 +430,7 @@ struct DagArgs {
   const int64_t *dep_ptr;
   const int32_t *dep_idx;
   const int64_t *item0, *nitems;  // per launch: first row-block item and item count (truncation launches)
+  const int32_t *prio;            // per launch: 0 .. 2 scheduling priority (may be NULL)
 };
 
 struct ShardArgs {
@@ -422,9 +478,9 @@ extern "C" int hlu_schedule_create_dag(hlu_schedule **out, const hlu_ctx *ctx, c
                                        const hlu_gemm_desc *gemm, const hlu_term *terms, hlu_rkt_desc *rkt,
                                        const hlu_rkpart *parts, const hlu_rkt_scratch *scratch,
                                        const int64_t *dep_ptr, const int32_t *dep_idx, const int64_t *item0,
-                                       const int64_t *nitems, void *stream) {
+                                       const int64_t *nitems, const int32_t *prio, void *stream) {
   if (!dep_ptr || !item0 || !nitems) return -23;
-  const DagArgs dag{dep_ptr, dep_idx, item0, nitems};
+  const DagArgs dag{dep_ptr, dep_idx, item0, nitems, prio};
   return create(out, ctx, launches, nlaunch, getrf, trsm, gemm, terms, rkt, parts, scratch, nullptr, nullptr, 0, 1,
                 stream, nullptr, &dag);
 }
@@ -458,6 +514,15 @@ static int create(hlu_schedule **out, const hlu_ctx *ctx, const hlu_launch *laun
     for (int64_t i = 0; i < nlaunch; ++i) s->rkt_op0[i] = launches[i].first;
     if (s->dag_ptr.empty()) s->dag_ptr.push_back(0);
     cudaMalloc(&s->dag_join, sizeof(unsigned long long));
+    if (dag->prio) {
+      s->dag_prio.assign(dag->prio, dag->prio + nlaunch);
+      for (int32_t &v : s->dag_prio) v = std::min(2, std::max(0, v));
+      int least = 0, greatest = 0;
+      cudaDeviceGetStreamPriorityRange(&least, &greatest);
+      cudaStreamCreateWithPriority(&s->dag_q[1], cudaStreamNonBlocking, (least + greatest) / 2);
+      cudaStreamCreateWithPriority(&s->dag_q[2], cudaStreamNonBlocking, greatest);
+      for (int k = 0; k < 2; ++k) cudaEventCreateWithFlags(&s->dag_ev[k], cudaEventDisableTiming);
+    }
   }
   if (sh) {
     s->comm = sh->comm;
@@ -537,8 +602,9 @@ static int create(hlu_schedule **out, const hlu_ctx *ctx, const hlu_launch *laun
     if (e && e[0] == '1') {
       int64_t nr = 0;
       for (const hlu_launch &L : s->launches) nr += L.kind == HLU_K_RKT32;
-      cudaMalloc(&s->stamps, (s->launches.size() + 1 + 12 * nr) * sizeof(unsigned long long));
-      cudaMemset(s->stamps, 0, (s->launches.size() + 1 + 12 * nr) * sizeof(unsigned long long));
+      const size_t ns = dag ? 2 * s->launches.size() + 2 : s->launches.size() + 1 + 12 * nr;
+      cudaMalloc(&s->stamps, ns * sizeof(unsigned long long));
+      cudaMemset(s->stamps, 0, ns * sizeof(unsigned long long));
     }
   }
   cudaStream_t st = (cudaStream_t)stream;
@@ -547,6 +613,54 @@ static int create(hlu_schedule **out, const hlu_ctx *ctx, const hlu_launch *laun
   cudaStreamCreateWithFlags(&s->dense, cudaStreamNonBlocking);
   cudaEventCreateWithFlags(&s->fork, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&s->join, cudaEventDisableTiming);
+  if (dag) {
+    hlu_getrf_batched_f64(&s->ctx, s->getrf, 0, 0, st);
+    hlu_trsm_batched_f64(&s->ctx, s->trsm, 0, 0, st);
+    hlu_rk_update_batched_f64(&s->ctx, s->rkt, s->parts, 0, &s->scratch, st);
+    hlu_gemm_small_batched_f64(&s->ctx, s->gemm, s->terms, 0, st);
+    hlu_gemm_batched_f64(&s->ctx, s->gemm, s->terms, 0, st);
+    const bool timing = getenv("HLU_PLAN_TIMING") != nullptr;
+    auto now = [] { return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count(); };
+    const double t0 = now();
+    const int64_t budget = getenv("HLU_DAG_CHUNK_NODES") ? atoll(getenv("HLU_DAG_CHUNK_NODES")) : 12000;
+    // chunk boundaries by estimated kernel nodes (a truncation launch is ~10)
+    size_t l0 = 0;
+    int slot = 0;
+    const size_t nl = s->launches.size();
+    while (l0 < nl || s->dag_exec.empty()) {
+      size_t l1 = l0;
+      int64_t est = 0;
+      while (l1 < nl && (est < budget || l1 == l0)) est += s->launches[l1].kind == HLU_K_RKT32 ? 10 : 1, ++l1;
+      if (cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+        hlu_schedule_destroy(s);
+        return -10;
+      }
+      const int rc = run_dag_chunk(s, st, l0, l1, slot);
+      cudaGraph_t g = nullptr;
+      const cudaError_t e = cudaStreamEndCapture(st, &g);
+      cudaGraphExec_t ex = nullptr;
+      if (rc != 0 || e != cudaSuccess ||
+          cudaGraphInstantiate(&ex, g, s->dag_prio.empty() ? 0 : cudaGraphInstantiateFlagUseNodePriority) !=
+              cudaSuccess) {
+        if (timing) std::fprintf(stderr, "schedule: dag chunk [%zu, %zu) failed: rc %d, %s\n", l0, l1, rc,
+                                 cudaGetErrorString(e != cudaSuccess ? e : cudaGetLastError()));
+        if (g) cudaGraphDestroy(g);
+        hlu_schedule_destroy(s);
+        return rc != 0 ? rc : (e != cudaSuccess ? -11 : -12);
+      }
+      cudaGraphDestroy(g);
+      cudaGraphUpload(ex, st);
+      s->dag_exec.push_back(ex);
+      l0 = l1;
+      if (nl == 0) break;
+    }
+    cudaStreamSynchronize(st);
+    if (timing)
+      std::fprintf(stderr, "schedule: dag %zu launches, %lld kernel nodes in %zu graphs, capture + instantiate %.2fs\n",
+                   nl, (long long)s->dag_nodes, s->dag_exec.size(), now() - t0);
+    *out = s;
+    return 0;
+  }
   if (s->use_graph) {
     // make sure kernel attributes are set outside capture
     hlu_getrf_batched_f64(&s->ctx, s->getrf, 0, 0, st);
@@ -558,22 +672,31 @@ static int create(hlu_schedule **out, const hlu_ctx *ctx, const hlu_launch *laun
       delete s;
       return -10;
     }
-    if (s->stamps) hlu_rkt_set_phase_stamps(s->stamps + s->launches.size() + 1);
+    if (s->stamps && !dag) hlu_rkt_set_phase_stamps(s->stamps + s->launches.size() + 1);
+    const bool timing = getenv("HLU_PLAN_TIMING") != nullptr;
+    auto now = [] { return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count(); };
+    double t0 = now();
     const int rc = run_launches(s, st);
     hlu_rkt_set_phase_stamps(nullptr);
     cudaGraph_t g = nullptr;
     const cudaError_t e = cudaStreamEndCapture(st, &g);
+    if (timing) std::fprintf(stderr, "schedule: capture %.2fs (%lld dag nodes)\n", now() - t0, (long long)s->dag_nodes), t0 = now();
     if (rc != 0 || e != cudaSuccess) {
       if (g) cudaGraphDestroy(g);
       delete s;
       return rc != 0 ? rc : -11;
     }
     s->graph = g;
-    if (cudaGraphInstantiate(&s->exec, g, 0) != cudaSuccess) {
+    if (cudaGraphInstantiate(&s->exec, g, s->dag_prio.empty() ? 0 : cudaGraphInstantiateFlagUseNodePriority) !=
+        cudaSuccess) {
       cudaGraphDestroy(g);
       delete s;
       return -12;
     }
+    if (timing) std::fprintf(stderr, "schedule: instantiate %.2fs\n", now() - t0), t0 = now();
+    cudaGraphUpload(s->exec, st);
+    cudaStreamSynchronize(st);
+    if (timing) std::fprintf(stderr, "schedule: upload %.2fs\n", now() - t0);
   }
   *out = s;
   return 0;
@@ -581,6 +704,11 @@ static int create(hlu_schedule **out, const hlu_ctx *ctx, const hlu_launch *laun
 
 extern "C" int hlu_schedule_launch(hlu_schedule *s, void *stream) {
   cudaStream_t st = (cudaStream_t)stream;
+  if (!s->dag_exec.empty()) {
+    for (cudaGraphExec_t ex : s->dag_exec)
+      if (cudaGraphLaunch(ex, st) != cudaSuccess) return -13;
+    return 0;
+  }
   if (s->use_graph) return cudaGraphLaunch(s->exec, st) == cudaSuccess ? 0 : -13;
   return run_launches(s, st);
 }
@@ -588,9 +716,14 @@ extern "C" int hlu_schedule_launch(hlu_schedule *s, void *stream) {
 extern "C" int hlu_schedule_destroy(hlu_schedule *s) {
   if (!s) return 0;
   if (s->exec) cudaGraphExecDestroy(s->exec);
+  for (cudaGraphExec_t ex : s->dag_exec) cudaGraphExecDestroy(ex);
   if (s->graph) cudaGraphDestroy(s->graph);
   if (s->stamps) cudaFree(s->stamps);
   if (s->dag_join) cudaFree(s->dag_join);
+  for (int k = 1; k < 3; ++k)
+    if (s->dag_q[k]) cudaStreamDestroy(s->dag_q[k]);
+  for (int k = 0; k < 2; ++k)
+    if (s->dag_ev[k]) cudaEventDestroy(s->dag_ev[k]);
   for (int i = 0; i < 8; ++i) cudaEventDestroy((cudaEvent_t)s->aux.ev[i]);
   for (int i = 0; i < 4; ++i) cudaStreamDestroy((cudaStream_t)s->aux.side[i]);
   cudaEventDestroy(s->fork);
@@ -605,7 +738,8 @@ extern "C" int64_t hlu_schedule_stamps(hlu_schedule *s, unsigned long long *out)
   if (!s->stamps) return 0;
   int64_t nr = 0;
   for (const hlu_launch &L : s->launches) nr += L.kind == HLU_K_RKT32;
-  const int64_t n = (int64_t)s->launches.size() + 1 + 12 * nr;
+  // DAG mode: (ready, end) of every launch
+  const int64_t n = !s->dag_ptr.empty() ? 2 * (int64_t)s->launches.size() : (int64_t)s->launches.size() + 1 + 12 * nr;
   if (out && cudaMemcpy(out, s->stamps, n * sizeof(unsigned long long), cudaMemcpyDeviceToHost) != cudaSuccess)
     return -1;
   return n;

@@ -120,12 +120,21 @@ class DeviceCall:
                 self.chains = False
                 dp = np.ascontiguousarray(p.dag_ptr, dtype=np.int64)
                 di = np.ascontiguousarray(p.dag_idx if len(p.dag_idx) else np.zeros(1, np.int32), dtype=np.int32)
+                # launches without model-time slack get a higher scheduling priority
+                # (HLU_DAG_PRIO="t1,t2" in us: slack <= t1 high, <= t2 medium; "off": none)
+                prio = None
+                spec = os.environ.get("HLU_DAG_PRIO", "200,2000")
+                if spec != "off" and p.dag_slack is not None:
+                    t1, t2 = (float(x) * 1000.0 for x in spec.split(","))
+                    sl = np.asarray(p.dag_slack[: len(launches)], dtype=np.int64)
+                    prio = np.ascontiguousarray(np.where(sl <= t1, 2, np.where(sl <= t2, 1, 0)), dtype=np.int32)
                 rc = lib.hlu_schedule_create_dag(
                     ctypes.byref(handle), ctypes.byref(self.ctx), launches.ctypes.data, len(launches),
                     self.d_getrf.data_ptr(), self.d_trsm.data_ptr(), self.d_gemm.data_ptr(),
                     self.d_terms.data_ptr(), self.d_rkt.data_ptr(), self.d_parts.data_ptr(),
                     ctypes.byref(self.scratch), dp.ctypes.data, di.ctypes.data, item0.ctypes.data,
-                    nitems.ctypes.data, ctypes.c_void_p(self.stream.cuda_stream),
+                    nitems.ctypes.data, prio.ctypes.data if prio is not None else None,
+                    ctypes.c_void_p(self.stream.cuda_stream),
                 )
                 _native.check(rc, "hlu_schedule_create_dag")
             else:

@@ -64,6 +64,8 @@ def lib():
         L.hlu_plan_build_dag.restype = ctypes.c_int
         L.hlu_plan_dag.argtypes = [vp, vp, vp]
         L.hlu_plan_dag.restype = i64
+        L.hlu_plan_dag_slack.argtypes = [vp, vp]
+        L.hlu_plan_dag_slack.restype = ctypes.c_int
         L.hlu_host_pack.argtypes = [vp, i64, vp, ctypes.c_int]
         L.hlu_host_unpack.argtypes = [vp, i64, vp, ctypes.c_int]
         _lib = L
@@ -130,9 +132,9 @@ def cache_dir_default():
         return DEFAULT_CACHE
     return None if d in ("", "0") else d
 _PACKED_ARRAYS = ("getrf", "trsm", "gemm", "terms", "rkt", "parts", "launches", "flop_formula", "flop_coef",
-                  "flop_log", "lu_op_ids", "op_levels", "wait_dense", "wait_rkt", "dag_ptr", "dag_idx")
+                  "flop_log", "lu_op_ids", "op_levels", "wait_dense", "wait_rkt", "dag_ptr", "dag_idx", "dag_slack")
 _PACKED_INTS = ("nlevels", "arena_doubles", "nlog", "nranks")
-PLAN_FORMAT = 3  # bump when the packing (Python side) or the npz layout changes
+PLAN_FORMAT = 4  # bump when the packing (Python side) or the npz layout changes
 
 
 def plan_key(nodes, cmds, scalars):
@@ -292,13 +294,15 @@ def _build(layout, nodes, cmds, split_rows, shard=None, dag_slot_ns=0):
         wr = np.full(max(nlev, 1), -1, dtype=np.int32)
         if L.hlu_plan_level_waits(h, wd.ctypes.data, wr.ctypes.data) != 0:
             wd = wr = None
-        dag_ptr = dag_idx = None
+        dag_ptr = dag_idx = dag_slack = None
         ne = int(L.hlu_plan_dag(h, None, None))
         if ne >= 0:
             dag_ptr = np.zeros(nl + 1, dtype=np.int64)
             dag_idx = np.zeros(max(ne, 1), dtype=np.int32)
             L.hlu_plan_dag(h, dag_ptr.ctypes.data, dag_idx.ctypes.data)
             dag_idx = dag_idx[:ne]
+            dag_slack = np.zeros(max(nl, 1), dtype=np.int64)
+            L.hlu_plan_dag_slack(h, dag_slack.ctypes.data)
         xfer = mask = None
         if shard is not None:
             xfer = np.zeros(max(int(L.hlu_plan_xfer(h, None)), 1), dtype=ir.XFER)
@@ -320,5 +324,5 @@ def _build(layout, nodes, cmds, split_rows, shard=None, dag_slot_ns=0):
         nranks=max(nrank, 1), lu_op_ids=lu_ops[:nlu], lu_labels=labels, op_levels=lv,
         wait_dense=wd, wait_rkt=wr, xfer=xfer, op_mask=mask,
         shard=None if shard is None else (int(shard[1]), int(shard[2])),
-        dag_ptr=dag_ptr, dag_idx=dag_idx,
+        dag_ptr=dag_ptr, dag_idx=dag_idx, dag_slack=dag_slack,
     ), nops

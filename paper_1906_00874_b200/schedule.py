@@ -154,6 +154,7 @@ class Packed:
     # launches dag_idx[dag_ptr[l] : dag_ptr[l + 1]]; None = level schedule
     dag_ptr: np.ndarray = None
     dag_idx: np.ndarray = None
+    dag_slack: np.ndarray = None  # per launch: model-time slack in ns (scheduling priority)
 
 
 def _view_rec(v):
