@@ -622,6 +622,7 @@ static int create(hlu_schedule **out, const hlu_ctx *ctx, const hlu_launch *laun
     const bool timing = getenv("HLU_PLAN_TIMING") != nullptr;
     auto now = [] { return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count(); };
     const double t0 = now();
+    double t_cap = 0.0, t_inst = 0.0, t_up = 0.0;
     const int64_t budget = getenv("HLU_DAG_CHUNK_NODES") ? atoll(getenv("HLU_DAG_CHUNK_NODES")) : 12000;
     // chunk boundaries by estimated kernel nodes (a truncation launch is ~10)
     size_t l0 = 0;
@@ -635,29 +636,39 @@ static int create(hlu_schedule **out, const hlu_ctx *ctx, const hlu_launch *laun
         hlu_schedule_destroy(s);
         return -10;
       }
+      double tc = now();
       const int rc = run_dag_chunk(s, st, l0, l1, slot);
       cudaGraph_t g = nullptr;
       const cudaError_t e = cudaStreamEndCapture(st, &g);
+      t_cap += now() - tc;
+      tc = now();
       cudaGraphExec_t ex = nullptr;
-      if (rc != 0 || e != cudaSuccess ||
-          cudaGraphInstantiate(&ex, g, s->dag_prio.empty() ? 0 : cudaGraphInstantiateFlagUseNodePriority) !=
-              cudaSuccess) {
+      const cudaError_t ei =
+          (rc != 0 || e != cudaSuccess)
+              ? cudaErrorUnknown
+              : cudaGraphInstantiate(&ex, g, s->dag_prio.empty() ? 0 : cudaGraphInstantiateFlagUseNodePriority);
+      t_inst += now() - tc;
+      if (ei != cudaSuccess) {
         if (timing) std::fprintf(stderr, "schedule: dag chunk [%zu, %zu) failed: rc %d, %s\n", l0, l1, rc,
                                  cudaGetErrorString(e != cudaSuccess ? e : cudaGetLastError()));
         if (g) cudaGraphDestroy(g);
         hlu_schedule_destroy(s);
         return rc != 0 ? rc : (e != cudaSuccess ? -11 : -12);
       }
+      tc = now();
       cudaGraphDestroy(g);
       cudaGraphUpload(ex, st);
+      t_up += now() - tc;
       s->dag_exec.push_back(ex);
       l0 = l1;
       if (nl == 0) break;
     }
     cudaStreamSynchronize(st);
     if (timing)
-      std::fprintf(stderr, "schedule: dag %zu launches, %lld kernel nodes in %zu graphs, capture + instantiate %.2fs\n",
-                   nl, (long long)s->dag_nodes, s->dag_exec.size(), now() - t0);
+      std::fprintf(stderr,
+                   "schedule: dag %zu launches, %lld kernel nodes in %zu graphs, %.2fs (capture %.2fs, instantiate "
+                   "%.2fs, destroy + upload %.2fs)\n",
+                   nl, (long long)s->dag_nodes, s->dag_exec.size(), now() - t0, t_cap, t_inst, t_up);
     *out = s;
     return 0;
   }

@@ -126,8 +126,14 @@ def _run(roots, commands, ctl, capacity, device=None, use_graph=True, extras=Non
 
     cap = capacity
     while True:
+        import time
+
+        t0 = time.perf_counter()
         layout, packed = plan_call(roots, commands, cap, extras)
+        t1 = time.perf_counter()
         call = DeviceCall(layout, packed, ctl, device=device, use_graph=use_graph, extras=extras)
+        call.sync()
+        call.plan_s, call.setup_s = t1 - t0, time.perf_counter() - t1  # diagnostics (bench.py)
         call.launch()
         try:
             call.check_errors()

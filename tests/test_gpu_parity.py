@@ -367,3 +367,49 @@ def test_sharded_runtime_one_gpu():
         comm.close()
     y = forward_solve(h, g["rhs"])
     assert np.linalg.norm(y - g["y_forward"]) <= 1e-8 * np.linalg.norm(g["y_forward"])
+
+
+# ---- DAG schedule vs level schedule ------------------------------------------------
+
+
+@pytest.mark.parametrize("name,slot_us", [("mixed_192", 5), ("bem1d_1024", 20), ("sphere_1024", 5),
+                                          ("sphere_2048_l64", 20), ("cfg1", 20)])
+def test_dag_schedule_bit_identical_to_levels(name, slot_us):
+    """The launch DAG (no level barriers; overlapping launches, per-launch scratch
+    windows, arena hand-over edges) runs the same ops in the same
+    per-destination order as the level schedule: factors, ranks and the flop
+    log must be bit-identical, on repeated replays of the same graphs."""
+    import torch
+
+    from paper_1906_00874_b200 import native_plan
+    from paper_1906_00874_b200.device import DeviceCall
+    from paper_1906_00874_b200.planner import Layout
+
+    build, ctl = cases.CASES[name]
+    h, _ = build()
+    out = []
+    for slot in (0, slot_us * 1000):
+        L = Layout([h], cap=32)
+        packed, _ = native_plan.plan(L, [("factor", h)], cache_dir=None, dag_slot_ns=slot)
+        call = DeviceCall(L, packed, TruncationControl(*ctl), use_graph=True)
+        assert bool(call.dag) == (slot > 0)
+        call.snapshot()
+        runs = []
+        for _ in range(2 if slot else 1):
+            call.restore()
+            call.launch()
+            call.check_errors()
+            n = L.payload_doubles
+            runs.append((call.pool[:n].cpu().numpy().copy(), call.ranks.cpu().numpy().copy(),
+                         call.log.cpu().numpy().copy()))
+        if slot:
+            assert int(call.lib.hlu_schedule_graph_nodes(call.handle)) >= len(packed.launches)
+            assert runs[0][0].tobytes() == runs[1][0].tobytes()
+        out.append(runs[-1])
+        call.close()
+        del call
+        torch.cuda.empty_cache()
+    (p0, r0, l0), (p1, r1, l1) = out
+    assert np.array_equal(r0, r1)
+    assert p0.tobytes() == p1.tobytes()
+    assert np.array_equal(l0, l1)
