@@ -134,6 +134,14 @@ typedef struct {
 int hlu_host_pack(const hlu_pack_rec *recs, int64_t n, double *pool, int threads);
 int hlu_host_unpack(const hlu_pack_rec *recs, int64_t n, const double *pool, int threads);
 
+/* Effective-flop total of one call: the reference's FlopCounter (hlu.py:46-55,
+ * incremented at hlu.py:408-637) evaluated from the planner's per-op formulas
+ * (formula 0: coef; 1: coef k; 3: coef k^2; 2: 2 (kc + kp + 1) coef (kp + 1),
+ * with k / kp / kc = log[flog], log[flog + 1], log[flog + 2]) and the ranks the
+ * kernels logged.  Deterministic for any thread count. */
+double hlu_effective_flops(const int64_t *formula, const double *coef, const int64_t *flog, int64_t nops,
+                           const int32_t *log, int64_t nlog, int threads);
+
 #ifdef __cplusplus
 }
 #endif

@@ -82,3 +82,43 @@ extern "C" int hlu_host_unpack(const hlu_pack_rec *recs, int64_t n, const double
   parallel(n, threads, recs, [pool](const hlu_pack_rec &r) { unpack_one(r, pool); });
   return 0;
 }
+
+// Reference FlopCounter total (hlu.py:46-55 and its call sites) from the
+// planner's static per-op formulas and the ranks the kernels logged: formula
+// 0 = c, 1 = c k, 3 = c k^2, 2 (Rk update) = 2 (kc + kp + 1) c (kp + 1) with
+// k = log[flog], kp = log[flog + 1], kc = log[flog + 2].  Fixed 64k-op chunks
+// summed in order, so the total does not depend on the thread count.
+extern "C" double hlu_effective_flops(const int64_t *formula, const double *coef, const int64_t *flog,
+                                      int64_t nops, const int32_t *log, int64_t nlog, int threads) {
+  constexpr int64_t CH = 65536;
+  const int64_t nch = (nops + CH - 1) / CH;
+  std::vector<double> part((size_t)std::max<int64_t>(nch, 1), 0.0);
+  if (threads <= 0) threads = (int)std::max(1u, std::thread::hardware_concurrency());
+  threads = (int)std::min<int64_t>(threads, std::max<int64_t>(nch, 1));
+  auto at = [&](int64_t i) -> double {
+    if (nlog <= 0) return 0.0;
+    return (double)log[std::min<int64_t>(std::max<int64_t>(i, 0), nlog - 1)];
+  };
+  auto work = [&](int t) {
+    for (int64_t c = t; c < nch; c += threads) {
+      double s = 0.0;
+      const int64_t e = std::min(nops, (c + 1) * CH);
+      for (int64_t i = c * CH; i < e; ++i) {
+        const int64_t f = formula[i];
+        const int64_t ix = std::max<int64_t>(flog[i], 0);
+        const double cf = coef[i];
+        if (f == 0) s += cf;
+        else if (f == 1) s += cf * at(ix);
+        else if (f == 3) { const double k = at(ix); s += cf * k * k; }
+        else if (f == 2) { const double kp = at(ix + 1), kc = at(ix + 2); s += 2.0 * (kc + kp + 1.0) * cf * (kp + 1.0); }
+      }
+      part[(size_t)c] = s;
+    }
+  };
+  std::vector<std::thread> pool;
+  for (int t = 0; t < threads; ++t) pool.emplace_back(work, t);
+  for (auto &th : pool) th.join();
+  double tot = 0.0;
+  for (double v : part) tot += v;
+  return tot;
+}

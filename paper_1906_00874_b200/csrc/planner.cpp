@@ -1632,18 +1632,30 @@ struct Planner {
     return true;
   }
 
-  // Exchange records: after level lv, rank w broadcasts every slot it wrote in
-  // lv that an op of another rank reads (at any level: a superset of what the
-  // later levels need); a final step (level nlevels) ships every written slot
-  // from its owner, so each rank ends with the whole factorization.  Records
-  // are grouped by (level, src), groups capped at XFER_GROUP doubles, with
-  // their offsets in the group's staging buffer (payload, then the rank).
+  // Exchange records: after level lv, rank w broadcasts the slots it wrote in
+  // lv whose value an op of another rank reads before the slot's next write
+  // (a slot is written by its owner only; intermediate values nobody else
+  // reads stay local, so in an H-LU mostly the final factor blocks travel);
+  // a final step (level nlevels) ships every written slot from its owner, so
+  // each rank ends with the whole factorization.  Records are grouped by
+  // (level, src), groups capped at XFER_GROUP doubles, with their offsets in
+  // the group's staging buffer (payload, then the rank).
+  // HLU_XFER_EVERY_WRITE=1 restores the superset (every write of a slot that
+  // has a remote reader at any level), for comparison.
   static constexpr int64_t XFER_GROUP = int64_t(1) << 26;  // 512 MB
   void exchange(const std::vector<int64_t> &order) {
     slot_nodes();
     const int64_t S = nslots;
-    std::vector<uint64_t> readers(S, 0);
-    {
+    struct X {
+      int64_t lv;
+      int32_t src;
+      int64_t sl;
+    };
+    std::vector<X> xs;
+    std::vector<char> written(S, 0);
+    const char *ev = std::getenv("HLU_XFER_EVERY_WRITE");
+    if (ev && ev[0] == '1') {
+      std::vector<uint64_t> readers(S, 0);
       std::vector<int32_t> diff((size_t)(S + 1) * nranks, 0);
       for (size_t i = 0; i < ops.size(); ++i) {
         const Op &o = ops[i];
@@ -1664,25 +1676,67 @@ struct Planner {
           run[b] += diff[(size_t)sl * nranks + b];
           if (run[b] > 0) readers[sl] |= 1ull << b;
         }
-    }
-    std::vector<char> written(S, 0);
-    struct X {
-      int64_t lv;
-      int32_t src;
-      int64_t sl;
-    };
-    std::vector<X> xs;
-    for (int64_t i : order) {  // level order
-      const Op &o = ops[i];
-      for (int64_t w = o.w_begin; w < o.w_end; ++w) {
-        const Iv &v = ivs[w];
-        if (v.lo >= S) continue;
-        for (int64_t sl = v.lo; sl < std::min<int64_t>(v.hi, S); ++sl) {
-          written[sl] = 1;
-          const int32_t src = slot_owner[sl];
-          if (readers[sl] & ~(1ull << src)) xs.push_back(X{levels[i], src, sl});
+      for (int64_t i : order) {  // level order
+        const Op &o = ops[i];
+        for (int64_t w = o.w_begin; w < o.w_end; ++w) {
+          const Iv &v = ivs[w];
+          if (v.lo >= S) continue;
+          for (int64_t sl = v.lo; sl < std::min<int64_t>(v.hi, S); ++sl) {
+            written[sl] = 1;
+            const int32_t src = slot_owner[sl];
+            if (readers[sl] & ~(1ull << src)) xs.push_back(X{levels[i], src, sl});
+          }
         }
       }
+    } else {
+      // Backward sweep in level order: pending(sl) = the ranks that read slot sl
+      // after the current position and before its next write.  Reads cover slot
+      // intervals (partitioned operands), so pending lives in a segment tree of
+      // OR tags: range OR, point query (OR over the root path), point clear
+      // (tags pushed down along the path first).
+      int64_t size = 1;
+      while (size < std::max<int64_t>(S, 1)) size <<= 1;
+      std::vector<uint64_t> tag((size_t)2 * size, 0);
+      auto range_or = [&](int64_t lo, int64_t hi, uint64_t m) {
+        for (lo += size, hi += size; lo < hi; lo >>= 1, hi >>= 1) {
+          if (lo & 1) tag[lo++] |= m;
+          if (hi & 1) tag[--hi] |= m;
+        }
+      };
+      auto take = [&](int64_t sl) {  // query + clear
+        int64_t node = 1;
+        for (int64_t half = size >> 1; half >= 1; half >>= 1) {
+          const uint64_t t = tag[node];
+          if (t) {
+            tag[2 * node] |= t;
+            tag[2 * node + 1] |= t;
+            tag[node] = 0;
+          }
+          node = 2 * node + (((sl & half) != 0) ? 1 : 0);
+        }
+        const uint64_t m = tag[node];
+        tag[node] = 0;
+        return m;
+      };
+      for (size_t q = order.size(); q-- > 0;) {
+        const int64_t i = order[q];
+        const Op &o = ops[i];
+        for (int64_t w = o.w_begin; w < o.w_end; ++w) {
+          const Iv &v = ivs[w];
+          if (v.lo >= S) continue;
+          for (int64_t sl = v.lo; sl < std::min<int64_t>(v.hi, S); ++sl) {
+            written[sl] = 1;
+            const int32_t src = slot_owner[sl];
+            if (take(sl) & ~(1ull << src)) xs.push_back(X{levels[i], src, sl});
+          }
+        }
+        for (int64_t r = o.r_begin; r < o.r_end; ++r) {
+          const Iv &v = ivs[r];
+          if (v.lo >= S) continue;
+          range_or(v.lo, std::min<int64_t>(v.hi, S), op_mask[i]);
+        }
+      }
+      std::reverse(xs.begin(), xs.end());
     }
     for (int64_t sl = 0; sl < S; ++sl)
       if (written[sl]) xs.push_back(X{nlevels, slot_owner[sl], sl});

@@ -21,10 +21,11 @@ import numpy as np
 from . import _native
 from .hmatrix import StructureError  # noqa: F401  (re-exported for callers)
 from .lowrank import SingularBlockError
-from .pool import fill_pool, read_extra, read_pool
+from .pool import fill_pool, leaf_chunks, read_extra, read_pool
 from .schedule import Packed, effective_flops, pack
 
 INT32_MAX = np.iinfo(np.int32).max
+XFER_CHUNKS = 16  # pool ranges of the pipelined upload / download
 
 
 class RankOverflow(RuntimeError):
@@ -69,7 +70,6 @@ class DeviceCall:
             # pinned staging buffers (payloads packed natively, hlu_host_pack)
             self.host_pool = torch.zeros(layout.payload_doubles, dtype=torch.float64, pin_memory=True)
             self.host_ranks = torch.zeros(p.nranks, dtype=torch.int32, pin_memory=True)
-            fill_pool(layout, self.host_pool.numpy(), self.host_ranks.numpy(), extras)
             self.ranks = torch.empty(p.nranks, dtype=torch.int32, device=self.device)
             self.log = torch.zeros(p.nlog, dtype=torch.int32, device=self.device)
             self.err = torch.tensor([0, INT32_MAX, 0, 0], dtype=torch.int32, device=self.device)
@@ -87,7 +87,7 @@ class DeviceCall:
                     torch, self.device, p.rkt, p.launches)
             else:
                 self.scratch, self._scratch_keep = _native.rkt_scratch(torch, self.device, p.rkt, p.launches)
-            self.upload()
+            self.refill_upload(extras)
             self.ctx = _native.HluCtx(
                 self.pool.data_ptr(), self.ranks.data_ptr(), self.log.data_ptr(), self.err.data_ptr(),
                 self.dlog.data_ptr(), float(ctl.eps), -1 if ctl.kmax is None else int(ctl.kmax), 0,
@@ -163,15 +163,33 @@ class DeviceCall:
         pinned staging buffers (same structure; the next ``upload`` sends them)."""
         fill_pool(self.L, self.host_pool.numpy(), self.host_ranks.numpy(), extras)
 
+    def _reset_err(self):
+        self.err[0] = 0
+        self.err[1] = INT32_MAX
+        self.err[2] = 0
+
     def upload(self):
         """Host (pinned) -> device copy of payloads and ranks; resets error words."""
         n = self.L.payload_doubles
         with self.torch.cuda.device(self.device), self.torch.cuda.stream(self.stream):
             self.pool[:n].copy_(self.host_pool, non_blocking=True)
             self.ranks.copy_(self.host_ranks, non_blocking=True)
-            self.err[0] = 0
-            self.err[1] = INT32_MAX
-            self.err[2] = 0
+            self._reset_err()
+
+    def refill_upload(self, extras=None, nchunks=None):
+        """``refill`` + ``upload`` pipelined: the leaves are packed group by
+        group into the pinned buffer and every finished pool range starts its
+        host-to-device copy while the next group is being packed."""
+        nchunks = XFER_CHUNKS if nchunks is None else nchunks
+        hp = self.host_pool
+        with self.torch.cuda.device(self.device), self.torch.cuda.stream(self.stream):
+
+            def send(lo, hi):
+                self.pool[lo:hi].copy_(hp[lo:hi], non_blocking=True)
+
+            fill_pool(self.L, hp.numpy(), self.host_ranks.numpy(), extras, nchunks=nchunks, on_chunk=send)
+            self.ranks.copy_(self.host_ranks, non_blocking=True)
+            self._reset_err()
 
     def snapshot(self):
         """Device-resident pristine copy, for repeated timed runs."""
@@ -250,17 +268,30 @@ class DeviceCall:
         if err[0]:
             raise RankOverflow(f"{int(err[0])} Rk results exceeded capacity {self.L.cap}")
 
-    def download(self):
+    def download(self, nchunks=None):
         """Device -> host (into the pinned staging buffers): install results
-        into the H-matrix; returns d2h bytes."""
-        n = self.L.payload_doubles
-        with self.torch.cuda.device(self.device), self.torch.cuda.stream(self.stream):
-            self.host_pool.copy_(self.pool[:n], non_blocking=True)
+        into the H-matrix; returns d2h bytes.  The pool comes back in ranges
+        (pool.leaf_chunks), each unpacked into the H-matrix as soon as its
+        copy has landed, while the later ranges are still in flight."""
+        nchunks = XFER_CHUNKS if nchunks is None else nchunks
+        torch = self.torch
+        _, offs = leaf_chunks(self.L, nchunks)
+        events = []
+        with torch.cuda.device(self.device), torch.cuda.stream(self.stream):
             self.host_ranks.copy_(self.ranks, non_blocking=True)
-        self.sync()
+            ev_r = torch.cuda.Event()
+            ev_r.record(self.stream)
+            for c in range(len(offs) - 1):
+                lo, hi = int(offs[c]), int(offs[c + 1])
+                self.host_pool[lo:hi].copy_(self.pool[lo:hi], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(self.stream)
+                events.append(ev)
+        ev_r.synchronize()
         pool = self.host_pool.numpy()
         ranks = self.host_ranks.numpy()
-        read_pool(self.L, pool, ranks)
+        read_pool(self.L, pool, ranks, nchunks=nchunks, wait_chunk=lambda c: events[c].synchronize())
+        self.sync()
         self._last_pool = pool
         return pool.nbytes + ranks.nbytes
 

@@ -65,9 +65,11 @@ def make_plan(h: HMatrix, truncation: TruncationControl | None = None, mode: str
               workers: int = 1, wd_er: bool = True, seed: int = 0, capacity: int | None = None,
               device=None, use_graph: bool = True, keep_schedule: bool = False) -> HluPlan:
     """Reference ``make_plan`` (hlu.py:72-90).  ``keep_schedule=True`` keeps the
-    planned device schedule (pools, descriptors, CUDA graph) on the plan, so
+    planned device schedule (pools, descriptors, CUDA graphs) on the plan, so
     later ``hlu_factorize(plan)`` calls on the same structure only re-pack the
-    host payloads, upload, replay and download (plan once, factorize many)."""
+    host payloads, upload, replay and download (plan once, factorize many); it
+    also selects the launch-DAG schedule, whose longer setup the replays repay.
+    Without it every call plans the level schedule (fast setup) and frees it."""
     if mode not in (SEQUENTIAL, PARALLEL):
         raise ValueError(f"unknown mode {mode!r}")
     return HluPlan(
@@ -96,15 +98,22 @@ def _auto_capacity(roots, ctl):
 _TRI = {"lower_matvec": 1, "upper_matvec": 2}
 
 
-def plan_call(roots, commands, capacity, extras=None, planner="native"):
+def plan_call(roots, commands, capacity, extras=None, planner="native", replay=True):
     """Layout + packed schedule for a list of planner commands, e.g.
     ``[("factor", h)]``; ``planner`` = "native" (C++) or "python" (the
-    reference-order specification the native planner is tested against)."""
+    reference-order specification the native planner is tested against).
+    ``replay`` picks the schedule: True = the launch DAG (finest overlap, but
+    its CUDA graphs take minutes to instantiate at n = 131072, so it pays off
+    when the schedule is kept and replayed); False = the level schedule
+    (seconds to set up; one-shot calls).  ``HLU_DAG_SLOT_US`` overrides both."""
     layout = Layout(roots, cap=capacity, extra=[(k, v.shape[0], v.shape[1]) for k, v in (extras or {}).items()])
     if planner == "native":
+        import os
+
         from . import native_plan
 
-        packed, _ = native_plan.plan(layout, commands)
+        slot = None if (replay or os.environ.get(native_plan.DAG_SLOT_ENV)) else 0
+        packed, _ = native_plan.plan(layout, commands, dag_slot_ns=slot)
         return layout, packed
     pl = Planner(layout)
     for cmd in commands:
@@ -118,10 +127,11 @@ def plan_call(roots, commands, capacity, extras=None, planner="native"):
     return layout, pack(pl, layout.payload_doubles)
 
 
-def _run(roots, commands, ctl, capacity, device=None, use_graph=True, extras=None, keep=False):
+def _run(roots, commands, ctl, capacity, device=None, use_graph=True, extras=None, keep=False, replay=False):
     """Plan + run one H-arithmetic call on the GPU, re-planning with a doubled
     capacity (clamped to MAX_CAP) if any Rk result overflows.  Returns the
-    DeviceCall; ``call.capacity`` is the capacity that succeeded."""
+    DeviceCall; ``call.capacity`` is the capacity that succeeded.  ``replay``:
+    the call's schedule will be kept and replayed (see ``plan_call``)."""
     from .device import DeviceCall, RankOverflow
 
     cap = capacity
@@ -129,7 +139,7 @@ def _run(roots, commands, ctl, capacity, device=None, use_graph=True, extras=Non
         import time
 
         t0 = time.perf_counter()
-        layout, packed = plan_call(roots, commands, cap, extras)
+        layout, packed = plan_call(roots, commands, cap, extras, replay=replay)
         t1 = time.perf_counter()
         call = DeviceCall(layout, packed, ctl, device=device, use_graph=use_graph, extras=extras)
         call.sync()
@@ -160,19 +170,32 @@ def hlu_factorize(plan: HluPlan):
     if call is not None and getattr(call, "handle", None) and call.L.roots[0] is h:
         from .device import RankOverflow
 
-        call.refill()  # the structure is unchanged: new payloads through the kept schedule
-        call.upload()
+        import os
+        import time
+
+        t = [time.perf_counter()]
+        call.refill_upload()  # the structure is unchanged: new payloads through the kept schedule
+        t.append(time.perf_counter())
         call.launch()
         try:
             call.check_errors()
+            t.append(time.perf_counter())
             call.download()
+            t.append(time.perf_counter())
             plan.flops.add(call.flops())
+            t.append(time.perf_counter())
+            if os.environ.get("HLU_E2E_TIMING") == "1":
+                import sys
+
+                print("hlu_factorize (kept schedule): pack+upload issue %.3f s, factorization (sync) %.3f s, "
+                      "download+install %.3f s, flop counter %.3f s" % tuple(b - a for a, b in zip(t, t[1:])),
+                      file=sys.stderr)
             return None
         except RankOverflow:
             call.close()
             plan.capacity = min(2 * plan.capacity, MAX_CAP)
     call = _run([h], [("factor", h)], plan.truncation, plan.capacity, plan.device, plan.use_graph,
-                keep=plan.keep_schedule)
+                keep=plan.keep_schedule, replay=plan.keep_schedule)
     plan.capacity = call.capacity  # later calls start from the capacity that fitted
     plan.flops.add(call.flops())
     plan.last_call = call

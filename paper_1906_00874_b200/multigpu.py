@@ -2,16 +2,16 @@
 (SURVEY.md §8e).
 
 * Every leaf (skeleton slot) gets an owner rank from a 2-D block-cyclic grid
-  over the index space (block size ~ n / (4 * grid side), i.e. about four
-  block rows/columns per rank, the balance point the survey measured).
+  over square index blocks of n / (4 * nranks) rows and columns (the balance
+  point the survey measured).
 * Every op runs on the owner of the slot it writes; a temp producer (product
   GEMM, accumulated/merged Rk temp, hoisted inner product) runs on every rank
   that consumes the temp (replicated when consumers live on several ranks),
   so temps never cross ranks.  The per-destination op order — and therefore
   every rank decision — is the single-GPU one.
 * After each level, every rank ships the slots it wrote in that level
-  (payload region + rank) to the ranks that will read them: the exchange
-  list is static, computed here from the plan.
+  (payload region + rank) whose value another rank reads before the slot's
+  next write: the exchange list is static, computed from the plan.
 
 ``run_level_exchange`` drives any per-rank executor with a
 ``torch.distributed`` process group (the readable specification, gloo on CPU
@@ -42,16 +42,22 @@ def grid_shape(nranks):
 
 
 def owner_map(layout, nranks, n=None, blocks_per_rank=4):
-    """Owner rank of every skeleton slot (leaves, then extra objects -> rank 0)."""
+    """Owner rank of every skeleton slot (leaves, then extra objects -> rank 0):
+    2-D block-cyclic over SQUARE index blocks of n / (blocks_per_rank * nranks)
+    rows and columns (32 x 32 blocks for 8 ranks, the level-5 clusters SURVEY
+    8e measured as the balance point).  Square blocks matter: the work of an
+    H-LU sits near the diagonal, and with different row / column block sizes a
+    pr x pc grid aliases the diagonal onto a few ranks (measured at cfg3, 8
+    ranks: ops per rank max / mean 1.69 with n/8 x n/16 blocks, 1.06 with
+    square n/32 blocks)."""
     pr, pc = grid_shape(nranks)
     if n is None:
         n = max(lf.row_range[1] for lf in layout.leaves)
-    bs_r = max(1, n // (blocks_per_rank * pr))
-    bs_c = max(1, n // (blocks_per_rank * pc))
+    bs = max(1, n // (blocks_per_rank * nranks))
     own = np.zeros(layout.nslots, dtype=np.int64)
     for s, lf in enumerate(layout.leaves):
-        r = (lf.row_range[0] // bs_r) % pr
-        c = (lf.col_range[0] // bs_c) % pc
+        r = (lf.row_range[0] // bs) % pr
+        c = (lf.col_range[0] // bs) % pc
         own[s] = r * pc + c
     return own
 

@@ -50,15 +50,35 @@ def _records(host, off, rows, cols):
     return recs
 
 
-def fill_pool(layout, pool, ranks, extras=None):
-    """Write every leaf payload into ``pool`` (float64, column-major slabs) and
-    the ranks (int32): one threaded native transpose-copy pass
-    (``hlu_host_pack``, include/hlu_plan.h)."""
+def leaf_chunks(layout, nchunks):
+    """Cut the leaves (pool offsets ascend in leaf order) into ``nchunks``
+    contiguous groups of about equal payload: returns (leaf index bounds,
+    pool offset bounds), both of length nchunks + 1; the last offset bound is
+    ``payload_doubles`` (identity block and extras ride with the last chunk).
+    Cached on the layout."""
+    key = ("_leaf_chunks", int(nchunks))
+    got = layout.__dict__.get(key)
+    if got is not None:
+        return got
+    starts = np.fromiter(
+        (layout.dense_off[id(lf)] if lf.kind == DENSE else layout.rk[id(lf)][0] for lf in layout.leaves),
+        dtype=np.int64, count=len(layout.leaves))
+    n = max(1, min(int(nchunks), len(starts)))
+    total = layout.ident_off
+    li = np.searchsorted(starts, total * np.arange(1, n) // n, side="left") if len(starts) else np.zeros(0, int)
+    li = np.unique(np.concatenate([[0], li, [len(starts)]])).astype(np.int64)
+    offs = np.concatenate([[0], starts[li[1:-1]], [layout.payload_doubles]]).astype(np.int64)
+    layout.__dict__[key] = (li, offs)
+    return li, offs
+
+
+def _pack_records(layout, leaves, ranks):
+    """Pack records of a group of leaves; sets their ranks; returns (recs, keep-alive list)."""
     cap = layout.cap
     host, off, rows, cols, keep = [], [], [], [], []
     slots, ks = [], []
     dense_off, rk = layout.dense_off, layout.rk
-    for lf in layout.leaves:
+    for lf in leaves:
         if lf.kind == DENSE:
             d = _c_order(lf.data)
             keep.append(d)
@@ -83,16 +103,31 @@ def fill_pool(layout, pool, ranks, extras=None):
             cols.extend((k, k))
     if slots:
         ranks[np.asarray(slots)] = np.asarray(ks, dtype=np.int32)
-    recs = _records(host, off, rows, cols)
+    return _records(host, off, rows, cols), keep
+
+
+def fill_pool(layout, pool, ranks, extras=None, nchunks=1, on_chunk=None):
+    """Write every leaf payload into ``pool`` (float64, column-major slabs) and
+    the ranks (int32) by threaded native transpose-copies (``hlu_host_pack``,
+    include/hlu_plan.h).  With ``nchunks`` > 1 the leaves are packed group by
+    group and ``on_chunk(lo, hi)`` is called as soon as the pool range
+    [lo, hi) is complete, so the caller can start its host-to-device copy
+    while the next group is being packed."""
     assert pool.dtype == np.float64 and pool.flags.c_contiguous
-    _native().hlu_host_pack(recs.ctypes.data, len(recs), pool.ctypes.data, 0)
-    del keep
     from .planner import IDENT
 
     pool[layout.ident_off : layout.ident_off + IDENT * IDENT] = np.eye(IDENT).ravel()
     for name, arr in (extras or {}).items():
         off, rows, cols, _ = layout.extra[name]
         pool[off : off + rows * cols] = np.asarray(arr, dtype=float).reshape(rows, cols).ravel(order="F")
+    li, offs = leaf_chunks(layout, nchunks)
+    pack = _native().hlu_host_pack
+    for c in range(len(li) - 1):
+        recs, keep = _pack_records(layout, layout.leaves[li[c] : li[c + 1]], ranks)
+        pack(recs.ctypes.data, len(recs), pool.ctypes.data, 0)
+        del keep
+        if on_chunk is not None:
+            on_chunk(int(offs[c]), int(offs[c + 1]))
 
 
 def fill_pool_numpy(layout, pool, ranks, extras=None):
@@ -119,37 +154,45 @@ def fill_pool_numpy(layout, pool, ranks, extras=None):
         pool[off : off + rows * cols] = np.asarray(arr, dtype=float).reshape(rows, cols).ravel(order="F")
 
 
-def read_pool(layout, pool, ranks):
+def read_pool(layout, pool, ranks, nchunks=1, wait_chunk=None):
     """Install the pool contents back into the layout's H-matrix: dense
-    payloads in place, fresh LowRank factors for Rk leaves (one threaded native
-    transpose-copy pass, ``hlu_host_unpack``)."""
-    host, off, rows, cols = [], [], [], []
+    payloads in place, fresh LowRank factors for Rk leaves (threaded native
+    transpose-copies, ``hlu_host_unpack``).  With ``nchunks`` > 1 the leaves
+    are read group by group (``leaf_chunks``) and ``wait_chunk(c)`` is called
+    before group ``c`` is touched (the caller waits for that range's
+    device-to-host copy there)."""
     dense_off, rk = layout.dense_off, layout.rk
     ranks = np.asarray(ranks).tolist()
     empty = np.empty
-    for lf in layout.leaves:
-        if lf.kind == DENSE:
-            d = lf.data
-            if not (d.flags.c_contiguous and d.dtype == np.float64 and d.flags.writeable):
-                lf.data = d = np.array(d, dtype=np.float64, order="C")
-            host.append(_addr(d))
-            off.append(dense_off[id(lf)])
-            rows.append(lf.rows)
-            cols.append(lf.cols)
-        else:
-            a_off, b_off, slot = rk[id(lf)]
-            k = ranks[slot]
-            a = empty((lf.rows, k))
-            b = empty((lf.cols, k))
-            lf.data = LowRank(a, b)
-            if k:
-                host.extend((_addr(a), _addr(b)))
-                off.extend((a_off, b_off))
-                rows.extend((lf.rows, lf.cols))
-                cols.extend((k, k))
-    recs = _records(host, off, rows, cols)
-    pool = np.ascontiguousarray(pool, dtype=np.float64)
-    _native().hlu_host_unpack(recs.ctypes.data, len(recs), pool.ctypes.data, 0)
+    assert pool.dtype == np.float64 and pool.flags.c_contiguous
+    unpack = _native().hlu_host_unpack
+    li, _ = leaf_chunks(layout, nchunks)
+    for c in range(len(li) - 1):
+        host, off, rows, cols = [], [], [], []
+        for lf in layout.leaves[li[c] : li[c + 1]]:
+            if lf.kind == DENSE:
+                d = lf.data
+                if not (d.flags.c_contiguous and d.dtype == np.float64 and d.flags.writeable):
+                    lf.data = d = np.array(d, dtype=np.float64, order="C")
+                host.append(_addr(d))
+                off.append(dense_off[id(lf)])
+                rows.append(lf.rows)
+                cols.append(lf.cols)
+            else:
+                a_off, b_off, slot = rk[id(lf)]
+                k = ranks[slot]
+                a = empty((lf.rows, k))
+                b = empty((lf.cols, k))
+                lf.data = LowRank(a, b)
+                if k:
+                    host.extend((_addr(a), _addr(b)))
+                    off.extend((a_off, b_off))
+                    rows.extend((lf.rows, lf.cols))
+                    cols.extend((k, k))
+        recs = _records(host, off, rows, cols)
+        if wait_chunk is not None:
+            wait_chunk(c)
+        unpack(recs.ctypes.data, len(recs), pool.ctypes.data, 0)
 
 
 def read_pool_numpy(layout, pool, ranks):

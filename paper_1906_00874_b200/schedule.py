@@ -253,7 +253,21 @@ def pack(pl: Planner, arena_base: int):
 
 
 def effective_flops(p: Packed, log):
-    """Reference FlopCounter total from the static formulas and logged ranks."""
+    """Reference FlopCounter total from the static formulas and logged ranks
+    (threaded native evaluation, ``hlu_effective_flops`` in include/hlu_plan.h;
+    cfg3 has 9.6 M ops)."""
+    from . import native_plan
+
+    f = np.ascontiguousarray(p.flop_formula, dtype=np.int64)
+    c = np.ascontiguousarray(p.flop_coef, dtype=np.float64)
+    fl = np.ascontiguousarray(p.flop_log, dtype=np.int64)
+    lg = np.ascontiguousarray(log, dtype=np.int32)
+    return float(native_plan.lib().hlu_effective_flops(f.ctypes.data, c.ctypes.data, fl.ctypes.data, len(f),
+                                                       lg.ctypes.data, len(lg), 0))
+
+
+def effective_flops_numpy(p: Packed, log):
+    """numpy statement of ``effective_flops`` (tests compare the two)."""
     f = p.flop_formula
     c = p.flop_coef
     idx = np.maximum(p.flop_log, 0)

@@ -133,3 +133,51 @@ def test_singular_block_label_in_plan():
     first = int(M.err[1])
     idx = int(np.nonzero(p.lu_op_ids == first)[0][0])
     assert p.lu_labels[idx] == "lu[0:4)x[0:4)"
+
+
+@pytest.mark.parametrize("nchunks", [1, 3, 16])
+def test_chunked_pack_and_unpack_match_numpy(nchunks):
+    """The pipelined upload / download packs and installs the leaves group by
+    group (pool.leaf_chunks): every pool range is complete when its callback
+    fires, the ranges tile the payload, and the result equals the per-leaf
+    numpy statement."""
+    from paper_1906_00874_b200.pool import fill_pool_numpy, leaf_chunks, read_pool_numpy
+
+    build, _ = cases.CASES["bem1d_1024"]
+    h, _ = build()
+    x = np.arange(h.rows, dtype=float).reshape(-1, 1)
+    L = Layout([h], cap=32, extra=[("x", h.rows, 1)])
+    want = np.zeros(L.payload_doubles)
+    want_r = np.zeros(L.nrk, np.int32)
+    fill_pool_numpy(L, want, want_r, extras={"x": x})
+    pool = np.full(L.payload_doubles, np.nan)
+    ranks = np.zeros(L.nrk, np.int32)
+    seen = []
+
+    def on_chunk(lo, hi):
+        seen.append((lo, hi))
+        m = ~np.isnan(want[lo:hi]) & (want[lo:hi] != 0)
+        assert np.array_equal(pool[lo:hi][m], want[lo:hi][m])  # the range is final when announced
+
+    fill_pool(L, pool, ranks, extras={"x": x}, nchunks=nchunks, on_chunk=on_chunk)
+    li, offs = leaf_chunks(L, nchunks)
+    assert seen == list(zip(offs[:-1].tolist(), offs[1:].tolist()))
+    assert seen[0][0] == 0 and seen[-1][1] == L.payload_doubles and len(li) == len(offs)
+    written = ~np.isnan(pool)
+    assert np.array_equal(pool[written], want[written]) and np.array_equal(ranks, want_r)
+    assert not np.any(want[~written])  # only capacity padding stays untouched
+    # install back group by group, in order, each after its wait callback
+    h2, h3 = h.copy(), h.copy()
+    order = []
+    read_pool(Layout([h2], cap=32, extra=[("x", h.rows, 1)]), want, want_r, nchunks=nchunks, wait_chunk=order.append)
+    read_pool_numpy(Layout([h3], cap=32, extra=[("x", h.rows, 1)]), want, want_r)
+    assert order == list(range(len(offs) - 1))
+    assert cases.payload_sha(h2) == cases.payload_sha(h3) == cases.payload_sha(h)
+
+
+def test_native_flop_counter_matches_numpy():
+    from paper_1906_00874_b200.schedule import effective_flops_numpy
+
+    h, p, M, _ = _run_ir("bem1d_1024")
+    a, b = effective_flops(p, M.log), effective_flops_numpy(p, M.log)
+    assert abs(a - b) <= 1e-13 * b and a > 0
