@@ -12,9 +12,9 @@ with the inputs resident in HBM (a device-to-device restore of the pristine
 payload precedes every step, outside the events; L2 is flushed between steps);
 ``e2e`` goes through the public plugin path with pinned host buffers
 (host->device upload, factorization, device->host download inside the timed
-region).  H-LU does not shard into independent units; with --gpus N every
-rank factorizes its own replica ("replicas only") and the
-aggregate is reported.
+region).  H-LU does not shard into independent units; under torchrun with N
+ranks ONE factorization runs owner-computes over the N GPUs with NCCL slot
+exchanges (strong scaling).
 """
 
 from __future__ import annotations
@@ -149,7 +149,7 @@ def time_rkt_launches(call, torch):
 
 def run_sharded(args, world, rank, local, dev, dist):
     """One H-LU factorization on WORLD_SIZE GPUs (one process each): owner
-    computes over a 2-D block-cyclic slot map, the native sharded plan per
+    computes over a skewed cyclic slot map (square index blocks), the native sharded plan per
     rank, slot exchanges as gather -> ncclBroadcast -> scatter inside each
     rank's CUDA graph, final gather (every rank ends with the whole factor).
     Timed on the device with CUDA events, max over ranks; total work is fixed
@@ -240,7 +240,7 @@ def run_sharded(args, world, rank, local, dev, dist):
         "data": "synthetic (BASELINE BEM sphere geometry, Laplace kernel; seeded)",
         "config": bench_config(cfg),
         "details": {"factor_time_s": t_step, "effective_flops": flops,
-                    "parallelism": f"owner computes over {world} GPUs (2-D block-cyclic slot owners), "
+                    "parallelism": f"owner computes over {world} GPUs (skewed cyclic slot owners over square index blocks), "
                                    "NCCL slot exchanges per level, final gather",
                     "ops_per_rank": share, "exchange_bytes_per_rank_broadcast_total": xfer_bytes,
                     "levels": int(packed.nlevels), "assembly_s": t_asm, "plan_s": t_plan, "rank_capacity": cap},

@@ -1,9 +1,8 @@
 """Owner-computes decomposition of the H-LU op DAG over several GPUs
 (SURVEY.md §8e).
 
-* Every leaf (skeleton slot) gets an owner rank from a 2-D block-cyclic grid
-  over square index blocks of n / (4 * nranks) rows and columns (the balance
-  point the survey measured).
+* Every leaf (skeleton slot) gets an owner rank from a skewed cyclic map over
+  square index blocks of n / (4 * nranks) rows and columns (``owner_map``).
 * Every op runs on the owner of the slot it writes; a temp producer (product
   GEMM, accumulated/merged Rk temp, hoisted inner product) runs on every rank
   that consumes the temp (replicated when consumers live on several ranks),
@@ -34,31 +33,33 @@ import numpy as np
 from .hmatrix import DENSE
 
 
-def grid_shape(nranks):
-    pr = int(math.isqrt(nranks))
-    while nranks % pr:
-        pr -= 1
-    return pr, nranks // pr
+def skew_stride(nranks):
+    """Column stride b of the skewed cyclic owner map: the smallest b >= 2 with
+    gcd(1 + b, nranks) == 1, so the block diagonal (i, i) -> (1 + b) i mod
+    nranks visits every rank."""
+    b = 2
+    while math.gcd(1 + b, nranks) != 1:
+        b += 1
+    return b
 
 
 def owner_map(layout, nranks, n=None, blocks_per_rank=4):
     """Owner rank of every skeleton slot (leaves, then extra objects -> rank 0):
-    2-D block-cyclic over SQUARE index blocks of n / (blocks_per_rank * nranks)
+    skewed cyclic over SQUARE index blocks of n / (blocks_per_rank * nranks)
     rows and columns (32 x 32 blocks for 8 ranks, the level-5 clusters SURVEY
-    8e measured as the balance point).  Square blocks matter: the work of an
-    H-LU sits near the diagonal, and with different row / column block sizes a
-    pr x pc grid aliases the diagonal onto a few ranks (measured at cfg3, 8
-    ranks: ops per rank max / mean 1.69 with n/8 x n/16 blocks, 1.06 with
-    square n/32 blocks)."""
-    pr, pc = grid_shape(nranks)
+    8e measured as the balance point): block (i, j) -> (i + b j) mod nranks.
+    The work of an H-LU sits on and next to the block diagonal, and a plain
+    pr x pc block-cyclic grid aliases the diagonal onto few ranks (cfg3, 8
+    ranks, ops per rank max / mean: 1.69 for a 2 x 4 grid, over n/8 x n/16 or
+    square n/32 blocks alike; 1.08 skewed).  Every block diagonal j - i = d
+    cycles through all ranks here."""
     if n is None:
         n = max(lf.row_range[1] for lf in layout.leaves)
     bs = max(1, n // (blocks_per_rank * nranks))
+    b = skew_stride(nranks)
     own = np.zeros(layout.nslots, dtype=np.int64)
     for s, lf in enumerate(layout.leaves):
-        r = (lf.row_range[0] // bs) % pr
-        c = (lf.col_range[0] // bs) % pc
-        own[s] = r * pc + c
+        own[s] = (lf.row_range[0] // bs + b * (lf.col_range[0] // bs)) % nranks
     return own
 
 
