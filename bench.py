@@ -318,6 +318,10 @@ def run_ours(args):
     oneshot = time.perf_counter() - t0
     cap = once.capacity
     del once
+    import gc
+
+    gc.collect()
+    torch.cuda.empty_cache()
     _restore_payloads(h, template)
     # Plan once, factorize many: keep_schedule selects the launch-DAG schedule
     # (its CUDA graphs take about two minutes to instantiate at cfg3) and keeps

@@ -63,6 +63,9 @@ class DeviceCall:
         self.total = layout.payload_doubles + p.arena_doubles
         self.h2d_bytes = layout.payload_doubles * 8 + p.nranks * 4
         with torch.cuda.device(self.device):
+            # blocks an earlier call freed stay in torch's caching allocator: hand
+            # them back, the CUDA graphs below take driver memory beside the pools
+            torch.cuda.empty_cache()
             # a dedicated stream: the legacy default stream cannot be graph-captured
             self.stream = torch.cuda.Stream(self.device)
         with torch.cuda.device(self.device), torch.cuda.stream(self.stream):
@@ -307,6 +310,15 @@ class DeviceCall:
             with self.torch.cuda.device(self.device):
                 self.lib.hlu_schedule_destroy(self.handle)
             self.handle = None
+
+    def release(self):
+        """``close`` and drop the device pools (results already downloaded stay
+        readable through ``extra``)."""
+        self.close()
+        for name in ("pool", "_pristine", "staging", "scratch", "_scratch_keep", "d_getrf", "d_trsm", "d_gemm",
+                     "d_terms", "d_rkt", "d_parts", "d_xfer"):
+            if hasattr(self, name):
+                setattr(self, name, None)
 
     def __del__(self):
         try:

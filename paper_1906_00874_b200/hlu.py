@@ -148,7 +148,7 @@ def _run(roots, commands, ctl, capacity, device=None, use_graph=True, extras=Non
         try:
             call.check_errors()
         except RankOverflow:
-            call.close()
+            call.release()
             if cap >= MAX_CAP:
                 raise
             cap = min(2 * cap, MAX_CAP)
@@ -156,7 +156,7 @@ def _run(roots, commands, ctl, capacity, device=None, use_graph=True, extras=Non
         call.capacity = cap
         call.download()
         if not keep:
-            call.close()
+            call.release()
         return call
 
 
@@ -192,7 +192,7 @@ def hlu_factorize(plan: HluPlan):
                       file=sys.stderr)
             return None
         except RankOverflow:
-            call.close()
+            call.release()
             plan.capacity = min(2 * plan.capacity, MAX_CAP)
     call = _run([h], [("factor", h)], plan.truncation, plan.capacity, plan.device, plan.use_graph,
                 keep=plan.keep_schedule, replay=plan.keep_schedule)

@@ -91,6 +91,52 @@ def main():
         l = int(via[l])
     print(f"releasing chain of the last launch: {hops} launches, gaps {gaps / 1e3:.2f} ms; " +
           ", ".join(f"{k} {v[0]}/{v[1] / 1e3:.1f}ms" for k, v in comp.items()))
+    # GEMM launches on that chain: serial tile steps of their longest CTA (static
+    # dimension bounds: 64 x 64 output tiles, 32-deep k-steps, triple terms both products)
+    g, t = p.gemm, p.terms
+
+    def steps(rows, cols, inner):
+        return -(-rows // 64) * -(-cols // 64) * -(-inner // 32)
+
+    chain = []
+    l = int(np.argmax(end))
+    while l >= 0:
+        chain.append(l)
+        l = int(via[l])
+    rows_out = []
+    for l in chain:
+        if int(kind[l]) not in (ir.K_GEMM, ir.K_GEMM_SMALL):
+            continue
+        f, c = int(Ls["first"][l]), int(Ls["count"][l])
+        best, desc = 0, None
+        for ch in range(f, f + c):
+            tb, n = int(g["term_begin"][ch]), int(g["term_count"][ch])
+            w = 0
+            big = None
+            for tm in t[tb:tb + n]:
+                if tm["kind"] == ir.TERM_GEMM:
+                    x = steps(int(tm["c"]["rows"]), int(tm["c"]["cols"]), int(tm["a"]["cols"]))
+                elif tm["kind"] == ir.TERM_TRIPLE:
+                    x = (steps(int(tm["m"]["rows"]), int(tm["c"]["cols"]), int(tm["m"]["cols"])) +
+                         steps(int(tm["c"]["rows"]), int(tm["c"]["cols"]), int(tm["m"]["rows"])))
+                else:
+                    x = 0
+                w += x
+                if big is None or x > big[0]:
+                    big = (x, int(tm["kind"]), int(tm["c"]["rows"]), int(tm["c"]["cols"]), int(tm["a"]["cols"]),
+                           int(tm["m"]["rows"]), int(tm["m"]["cols"]))
+            if w > best:
+                best, desc = w, (n, big)
+        rows_out.append((dur[l], best, c, desc))
+    if rows_out:
+        d = np.array([r[0] for r in rows_out])
+        w = np.array([r[1] for r in rows_out], dtype=float)
+        print(f"gemm launches on the chain: {len(d)}, duration mean {d.mean():.1f} us; serial tile steps of the longest "
+              f"CTA: p50 {np.percentile(w, 50):.0f}, p90 {np.percentile(w, 90):.0f}, max {w.max():.0f}; "
+              f"corr(duration, steps) {np.corrcoef(d, w)[0, 1]:.2f}; us per step (fit) {np.polyfit(w, d, 1)[0]:.2f}")
+        for r in sorted(rows_out, key=lambda r: -r[0])[:12]:
+            print(f"   dur {r[0]:8.1f} us, chains {r[2]:5d}, longest CTA {r[1]:5d} steps: terms {r[3][0]}, biggest term "
+                  f"(steps, kind, Crows, Ccols, inner, Mrows, Mcols) {r[3][1]}")
     # in-flight profile
     ev = np.concatenate([np.stack([ready, np.ones(nl)], 1), np.stack([end, -np.ones(nl)], 1)])
     ev = ev[np.argsort(ev[:, 0], kind="stable")]
