@@ -134,6 +134,13 @@ typedef struct {
 int hlu_host_pack(const hlu_pack_rec *recs, int64_t n, double *pool, int threads);
 int hlu_host_unpack(const hlu_pack_rec *recs, int64_t n, const double *pool, int threads);
 
+/* The same copies with recs[i].host = the numpy array OBJECT (id(array)): the
+ * data pointers are read from numpy's PyArrayObject and every array is checked
+ * to be a C-contiguous float64 rows x cols array (writeable when unpack != 0).
+ * recs[i].host is replaced by the data pointer.  Returns 0, or -(i + 1) for the
+ * first array failing the check (nothing is copied then). */
+int64_t hlu_host_pack_np(hlu_pack_rec *recs, int64_t n, double *pool, int threads, int unpack);
+
 /* Effective-flop total of one call: the reference's FlopCounter (hlu.py:46-55,
  * incremented at hlu.py:408-637) evaluated from the planner's per-op formulas
  * (formula 0: coef; 1: coef k; 3: coef k^2; 2: 2 (kc + kp + 1) coef (kp + 1),

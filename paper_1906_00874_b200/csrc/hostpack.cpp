@@ -73,6 +73,54 @@ void parallel(int64_t n, int threads, const hlu_pack_rec *recs, F f) {
 
 }  // namespace
 
+// --- numpy arrays addressed through their PyObject (id(array)) -----------------
+// The per-leaf Python cost of asking numpy for a data pointer
+// (__array_interface__: ~2 us, 240 k arrays at cfg3) is the bulk of a
+// pack / unpack, so the *_np entry points take the array objects themselves
+// and read the fields of numpy's PyArrayObject (ABI-stable head of the struct:
+// PyObject_HEAD, data, nd, dimensions, strides, base, descr, flags; descr:
+// PyObject_HEAD, typeobj, kind, type, byteorder, flags, type_num).  Every
+// array is validated (float64, 2-d, the expected shape, C-contiguous rows,
+// writeable for unpack); the Python side self-tests the layout at import and
+// falls back to hlu_host_pack / hlu_host_unpack if it does not hold.
+namespace {
+struct NpView {
+  const char *data;
+  bool ok;
+};
+constexpr int NPY_DOUBLE_NUM = 12;
+constexpr int NPY_WRITEABLE = 0x0400;
+NpView np_view(uint64_t obj, int64_t rows, int64_t cols, bool writeable) {
+  const char *o = reinterpret_cast<const char *>(obj);
+  const char *data = *reinterpret_cast<const char *const *>(o + 16);
+  const int nd = *reinterpret_cast<const int *>(o + 24);
+  const int64_t *dims = *reinterpret_cast<const int64_t *const *>(o + 32);
+  const int64_t *strides = *reinterpret_cast<const int64_t *const *>(o + 40);
+  const char *descr = *reinterpret_cast<const char *const *>(o + 56);
+  const int flags = *reinterpret_cast<const int *>(o + 64);
+  bool ok = nd == 2 && descr && *reinterpret_cast<const int *>(descr + 28) == NPY_DOUBLE_NUM &&
+            descr[26] != '>';
+  if (ok) ok = dims[0] == rows && dims[1] == cols;
+  if (ok && rows > 0 && cols > 0)
+    ok = (cols == 1 || strides[1] == 8) && (rows == 1 || strides[0] == cols * 8);
+  if (ok && writeable) ok = (flags & NPY_WRITEABLE) != 0;
+  return NpView{data, ok};
+}
+}  // namespace
+
+// recs[i].host holds id(array); returns 0, or -(i + 1) for the first array
+// that is not a C-contiguous float64 (rows x cols) array (nothing is copied then)
+extern "C" int64_t hlu_host_pack_np(hlu_pack_rec *recs, int64_t n, double *pool, int threads, int unpack) {
+  for (int64_t i = 0; i < n; ++i) {
+    const NpView v = np_view((uint64_t)recs[i].host, recs[i].rows, recs[i].cols, unpack != 0);
+    if (!v.ok) return -(i + 1);
+    recs[i].host = const_cast<char *>(v.data);
+  }
+  if (unpack) parallel(n, threads, recs, [pool](const hlu_pack_rec &r) { unpack_one(r, pool); });
+  else parallel(n, threads, recs, [pool](const hlu_pack_rec &r) { pack_one(r, pool); });
+  return 0;
+}
+
 extern "C" int hlu_host_pack(const hlu_pack_rec *recs, int64_t n, double *pool, int threads) {
   parallel(n, threads, recs, [pool](const hlu_pack_rec &r) { pack_one(r, pool); });
   return 0;

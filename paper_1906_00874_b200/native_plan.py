@@ -68,6 +68,8 @@ def lib():
         L.hlu_plan_dag_slack.restype = ctypes.c_int
         L.hlu_host_pack.argtypes = [vp, i64, vp, ctypes.c_int]
         L.hlu_host_unpack.argtypes = [vp, i64, vp, ctypes.c_int]
+        L.hlu_host_pack_np.argtypes = [vp, i64, vp, ctypes.c_int, ctypes.c_int]
+        L.hlu_host_pack_np.restype = i64
         L.hlu_effective_flops.argtypes = [vp, vp, vp, i64, vp, i64, ctypes.c_int]
         L.hlu_effective_flops.restype = ctypes.c_double
         _lib = L

@@ -181,3 +181,37 @@ def test_native_flop_counter_matches_numpy():
     h, p, M, _ = _run_ir("bem1d_1024")
     a, b = effective_flops(p, M.log), effective_flops_numpy(p, M.log)
     assert abs(a - b) <= 1e-13 * b and a > 0
+
+
+def test_pack_unpack_general_path_for_odd_arrays():
+    """Leaves that are not C-contiguous float64 arrays (or are read-only on the
+    way back) fail the native array check and take the general path; the
+    result is the same."""
+    from paper_1906_00874_b200.hmatrix import DENSE
+    from paper_1906_00874_b200.pool import fill_pool_numpy, np_fast_path, read_pool_numpy
+
+    assert np_fast_path()  # numpy's array struct is readable natively in this environment
+    build, _ = cases.CASES["mixed_192"]
+    h, _ = build()
+    dense = [lf for lf in h.leaves() if lf.kind == DENSE]
+    rk = [lf for lf in h.leaves() if lf.kind != DENSE]
+    dense[0].data = np.asfortranarray(dense[0].data)
+    dense[1].data = dense[1].data.astype(np.float32).astype(np.float64)[:, :]  # still fine (control)
+    rk[0].data.a = np.asfortranarray(rk[0].data.a) if rk[0].data.k > 1 else rk[0].data.a
+    L = Layout([h], cap=32)
+    want = np.zeros(L.payload_doubles)
+    want_r = np.zeros(L.nrk, np.int32)
+    fill_pool_numpy(L, want, want_r)
+    pool = np.zeros(L.payload_doubles)
+    ranks = np.zeros(L.nrk, np.int32)
+    fill_pool(L, pool, ranks, nchunks=4)
+    assert np.array_equal(pool, want) and np.array_equal(ranks, want_r)
+    h2, h3 = h.copy(), h.copy()
+    d2 = [lf for lf in h2.leaves() if lf.kind == DENSE]
+    d2[2].data.flags.writeable = False
+    d2[3].data = np.asfortranarray(d2[3].data)
+    want2 = want * 2.0
+    read_pool(Layout([h2], cap=32), want2, want_r, nchunks=4)
+    read_pool_numpy(Layout([h3], cap=32), want2, want_r)
+    assert cases.payload_sha(h2) == cases.payload_sha(h3)
+    assert d2[2].data.flags.writeable and d2[3].data.flags.c_contiguous
