@@ -260,6 +260,7 @@ static int run_dag_chunk(hlu_schedule *s, cudaStream_t st, size_t l0, size_t l1,
   tails.reserve(nl * 2);
   std::vector<char> has_succ(nl, 0);
   static const bool all_routes = getenv("HLU_RKT_ALL_ROUTES") && getenv("HLU_RKT_ALL_ROUTES")[0] == '1';
+  static const bool join_tails = getenv("HLU_DAG_JOIN") && getenv("HLU_DAG_JOIN")[0] == '1';
   for (size_t l = l0; l < l1; ++l) {
     const hlu_launch &L = s->launches[l];
     deps.clear();
@@ -329,6 +330,16 @@ static int run_dag_chunk(hlu_schedule *s, cudaStream_t st, size_t l0, size_t l1,
         if ((rc = K(8, b_tail, tail))) return rc;
         if ((rc = K(10, b_tail, tail))) return rc;
       }
+    }
+    if (join_tails && tail.size() > 1) {
+      // one empty node behind the launch's tail kernels: successors take one edge
+      // instead of one per tail (no GPU work; fewer edges to instantiate)
+      cudaStreamCaptureStatus status;
+      cudaGraph_t graph = nullptr;
+      if (cudaStreamGetCaptureInfo(st, &status, nullptr, &graph, nullptr, nullptr) != cudaSuccess || !graph) return -23;
+      cudaGraphNode_t join = nullptr;
+      if (cudaGraphAddEmptyNode(&join, graph, tail.data(), tail.size()) != cudaSuccess) return -23;
+      tail.assign(1, join);
     }
     if (s->stamps) {  // ... and when its last kernel ended
       if ((rc = set_deps(st, tail))) return rc;

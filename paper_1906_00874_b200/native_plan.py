@@ -193,7 +193,11 @@ def load_packed(path):
 
 
 DAG_SLOT_ENV = "HLU_DAG_SLOT_US"  # time-slot width of the DAG schedule in us; "0": level schedule
-DAG_SLOT_US_DEFAULT = 20.0
+# Finer slots = fewer false dependencies between launches = shorter runs, but more
+# CUDA-graph nodes, whose instantiation time grows faster than linearly (cfg3:
+# 20 us 3.35 s / 536 k nodes / 121 s set-up, 10 us 3.14 s / 683 k / 165-190 s,
+# 5 us 2.99 s / 776 k / 222-240 s; profiles/r02/dag_slot_sweep.txt)
+DAG_SLOT_US_DEFAULT = 5.0
 
 
 def dag_slot_ns_default():
