@@ -318,42 +318,108 @@ __device__ void trsm_shared(double *sm, const Mat &T, const Mat &X, int mode) {
       xs[i + v * ld] = (mode == 1) ? X.get(v0 + v, i) : X.get(i, v0 + v);
     }
     __syncthreads();
-    if (mode == 0) {
-      for (int j = 0; j < n - 1; ++j) {
-        const int r = n - j - 1;
-        for (int e = tid; e < r * nv; e += HLU_NT) {
-          const int i = j + 1 + e % r, v = e / r;
-          xs[i + v * ld] -= ts[i + j * ld] * xs[j + v * ld];
+    // Substitution with the right-hand sides in registers: warp w owns the
+    // columns v = w, w + 8, ... of the chunk (<= 8 of them), lane l the solve
+    // indices l, l + 32, ... (n <= 128: 4 per lane).  A column never leaves its
+    // warp, so the n elimination steps need no CTA barrier: the pivot element
+    // is broadcast by a shuffle and the coefficient column / row of T is read
+    // from shared memory once for all of the warp's columns.  Same operations
+    // per element, in the same order, as the textbook loops they replace.
+    {
+      const int lane = tid & 31, wid = tid >> 5;
+      const int ncol = nv > wid ? (nv - wid + HLU_NWARP - 1) / HLU_NWARP : 0;  // warp-uniform
+      double x[TRSM_CHUNK / HLU_NWARP][4];
+#pragma unroll
+      for (int c = 0; c < TRSM_CHUNK / HLU_NWARP; ++c)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int i = lane + 32 * q;
+          x[c][q] = (c < ncol && i < n) ? xs[i + (wid + HLU_NWARP * c) * ld] : 0.0;
         }
-        __syncthreads();
-      }
-    } else if (mode == 1) {
-      for (int j = 0; j < n; ++j) {
-        const double ujj = ts[j + j * ld];
-        const int r = n - j - 1;
-        for (int e = tid; e < r * nv; e += HLU_NT) {
-          const int l = j + 1 + e % r, v = e / r;
-          xs[l + v * ld] -= (xs[j + v * ld] / ujj) * ts[j + l * ld];
+      if (mode == 0) {
+#pragma unroll
+        for (int q0 = 0; q0 < 4; ++q0) {
+          if (q0 * 32 < n - 1) {
+            for (int jl = 0; jl < 32 && q0 * 32 + jl < n - 1; ++jl) {
+              const int j = q0 * 32 + jl;
+              double l[4];
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                const int i = lane + 32 * q;
+                l[q] = (q >= q0 && i > j && i < n) ? ts[i + j * ld] : 0.0;
+              }
+#pragma unroll
+              for (int c = 0; c < TRSM_CHUNK / HLU_NWARP; ++c) {
+                if (c < ncol) {
+                  const double xj = __shfl_sync(0xffffffffu, x[c][q0], jl);
+#pragma unroll
+                  for (int q = 0; q < 4; ++q)
+                    if (q >= q0 && lane + 32 * q > j) x[c][q] -= l[q] * xj;
+                }
+              }
+            }
+          }
         }
-        __syncthreads();
-      }
-      for (int e = tid; e < n * nv; e += HLU_NT) {
-        const int i = e % n, v = e / n;
-        xs[i + v * ld] /= ts[i + i * ld];
-      }
-    } else {
-      for (int j = n - 1; j >= 0; --j) {
-        const double ujj = ts[j + j * ld];
-        for (int e = tid; e < j * nv; e += HLU_NT) {
-          const int i = e % j, v = e / j;
-          xs[i + v * ld] -= ts[i + j * ld] * (xs[j + v * ld] / ujj);
+      } else if (mode == 1) {
+#pragma unroll
+        for (int q0 = 0; q0 < 4; ++q0) {
+          if (q0 * 32 < n) {
+            for (int jl = 0; jl < 32 && q0 * 32 + jl < n; ++jl) {
+              const int j = q0 * 32 + jl;
+              const double ujj = ts[j + j * ld];
+              double u[4];
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                const int i = lane + 32 * q;
+                u[q] = (q >= q0 && i > j && i < n) ? ts[j + i * ld] : 0.0;
+              }
+#pragma unroll
+              for (int c = 0; c < TRSM_CHUNK / HLU_NWARP; ++c) {
+                if (c < ncol) {
+                  const double xd = __shfl_sync(0xffffffffu, x[c][q0], jl) / ujj;
+#pragma unroll
+                  for (int q = 0; q < 4; ++q)
+                    if (q >= q0 && lane + 32 * q > j) x[c][q] -= xd * u[q];
+                  if (lane == jl) x[c][q0] = xd;
+                }
+              }
+            }
+          }
         }
-        __syncthreads();
+      } else {
+#pragma unroll
+        for (int q0 = 3; q0 >= 0; --q0) {
+          if (q0 * 32 < n) {
+            for (int jl = min(31, n - 1 - q0 * 32); jl >= 0; --jl) {
+              const int j = q0 * 32 + jl;
+              const double ujj = ts[j + j * ld];
+              double u[4];
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                const int i = lane + 32 * q;
+                u[q] = (q <= q0 && i < j) ? ts[i + j * ld] : 0.0;
+              }
+#pragma unroll
+              for (int c = 0; c < TRSM_CHUNK / HLU_NWARP; ++c) {
+                if (c < ncol) {
+                  const double xd = __shfl_sync(0xffffffffu, x[c][q0], jl) / ujj;
+#pragma unroll
+                  for (int q = 0; q < 4; ++q)
+                    if (q <= q0 && lane + 32 * q < j) x[c][q] -= u[q] * xd;
+                  if (lane == jl) x[c][q0] = xd;
+                }
+              }
+            }
+          }
+        }
       }
-      for (int e = tid; e < n * nv; e += HLU_NT) {
-        const int i = e % n, v = e / n;
-        xs[i + v * ld] /= ts[i + i * ld];
-      }
+#pragma unroll
+      for (int c = 0; c < TRSM_CHUNK / HLU_NWARP; ++c)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int i = lane + 32 * q;
+          if (c < ncol && i < n) xs[i + (wid + HLU_NWARP * c) * ld] = x[c][q];
+        }
     }
     __syncthreads();
     for (int e = tid; e < n * nv; e += HLU_NT) {
