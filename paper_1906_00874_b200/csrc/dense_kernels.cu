@@ -71,18 +71,40 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 // C += alpha * A B.  Double-buffered k-tiles: the next tile streams into the
 // other shared buffers by cp.async while the tensor cores consume this one.
 // sA / sB hold two GTILE buffers each.
+//
+// The operand geometry is copied into registers first: the Mats arrive by
+// reference (they live in the caller's stack frame) and every cp.async is an
+// asm with a memory clobber, so reading A.p / A.rs / ... inside the staging
+// loop would reload them from local memory after each copy (measured: 2.6 k
+// instructions and a local-load stall per copy for one 64^3 tile).  Element u
+// of a thread's staging list sits at a fixed offset from element 0 (row or
+// depth advances linearly with u), so the addresses are one base plus u
+// strides, advanced by a constant per k-tile.
 __device__ __noinline__ void tile_gemm(const Mat &C, const Mat &A, const Mat &B, double alpha, double *sA,
                                        double *sB, int tri = HLU_TRI_NONE) {
   const int m = C.rows, n = C.cols, k = A.cols;
+  double *const Cp = C.p;
+  const double *const Ap = A.p, *const Bp = B.p;
+  // strides and element offsets of one operand fit 32 bits (an operand is a window of one leaf / temp)
+  const int Crs = (int)C.rs, Ccs = (int)C.cs, Ars = (int)A.rs, Acs = (int)A.cs, Brs = (int)B.rs, Bcs = (int)B.cs;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int g = lane >> 2, t = lane & 3;
   const int wm = (wid & 3) * 16, wn = (wid >> 2) * 32;
   // coalescing: walk each operand's unit-stride dimension fastest
-  const bool a_rf = A.rs == 1, b_rf = B.rs == 1;
-  const bool a_sh = __isShared(A.p), b_sh = __isShared(B.p);
+  const bool a_rf = Ars == 1, b_rf = Brs == 1;
+  const bool a_sh = __isShared(Ap), b_sh = __isShared(Bp);
   // element (row r, depth q) of the A tile / (depth q, col c) of the B tile
   const int am = a_rf ? 1 : GL32, ak = a_rf ? GL64 : 1;
   const int bk = b_rf ? 1 : GL64, bn = b_rf ? GL32 : 1;
+  // staging list of this thread: element u = (row ar0 + u adr, depth aq0 + u adq) of A,
+  // (depth bq0 + u bdq, col bc0 + u bdc) of B
+  const int ar0 = a_rf ? tid % GB : tid / GK, aq0 = a_rf ? tid / GB : tid % GK;
+  const int adr = a_rf ? 0 : HLU_NT / GK, adq = a_rf ? HLU_NT / GB : 0;
+  const int bq0 = b_rf ? tid % GK : tid / GB, bc0 = b_rf ? tid / GK : tid % GB;
+  const int bdq = b_rf ? 0 : HLU_NT / GB, bdc = b_rf ? HLU_NT / GK : 0;
+  const int a_step = adr * Ars + adq * Acs, b_step = bdq * Brs + bdc * Bcs;
+  const int ta_off = ar0 * am + aq0 * ak, ta_step = adr * am + adq * ak;
+  const int tb_off = bq0 * bk + bc0 * bn, tb_step = bdq * bk + bdc * bn;
   for (int i0 = 0; i0 < m; i0 += GB) {
     for (int j0 = 0; j0 < n; j0 += GB) {
       double acc[4][4];
@@ -90,32 +112,33 @@ __device__ __noinline__ void tile_gemm(const Mat &C, const Mat &A, const Mat &B,
       for (int f = 0; f < 4; ++f)
 #pragma unroll
         for (int v = 0; v < 4; ++v) acc[f][v] = 0.0;
+      const int a_base = (i0 + ar0) * Ars + aq0 * Acs, b_base = bq0 * Brs + (j0 + bc0) * Bcs;
+      // fragments of this warp inside C (warp-uniform): 0 when its rows or columns lie outside
+      const int nf = (i0 + wm < m) ? max(0, min(4, (n - j0 - wn + 7) >> 3)) : 0;
       auto issue = [&](int k0, int buf) {
-        double *ta = sA + buf * GTILE, *tb = sB + buf * GTILE;
-#pragma unroll 1
+        double *ta = sA + buf * GTILE + ta_off, *tb = sB + buf * GTILE + tb_off;
+        const double *pa = Ap + (a_base + k0 * Acs), *pb = Bp + (b_base + k0 * Brs);
+        int ai = i0 + ar0, aq = k0 + aq0, bq = k0 + bq0, bj = j0 + bc0;
+        const int kz = (k + 7) & ~7;  // depths [k, kz) are read by the last 8-deep step: zero-filled
+#pragma unroll 2
         for (int u = 0; u < GPF; ++u) {
-          const int e = tid + u * HLU_NT;
-          const int r = a_rf ? e % GB : e / GK, q = a_rf ? e / GB : e % GK;
-          const int gi = i0 + r, gk = k0 + q;
-          const bool oka = gi < m && gk < k;
-          cp_async8(ta + r * am + q * ak, oka ? &A.at(gi, gk) : A.p, oka, a_sh);
-          const int qq = b_rf ? e % GK : e / GB, cc = b_rf ? e / GK : e % GB;
-          const int bj = j0 + cc, bkk = k0 + qq;
-          const bool okb = bkk < k && bj < n;
-          cp_async8(tb + qq * bk + cc * bn, okb ? &B.at(bkk, bj) : B.p, okb, b_sh);
+          // rows of A past m and columns of B past n only feed accumulator entries that are
+          // never stored: nothing is staged for them
+          if (ai < m && aq < kz) cp_async8(ta, aq < k ? pa : Ap, aq < k, a_sh);
+          if (bj < n && bq < kz) cp_async8(tb, bq < k ? pb : Bp, bq < k, b_sh);
+          ta += ta_step, tb += tb_step, pa += a_step, pb += b_step;
+          ai += adr, aq += adq, bq += bdq, bj += bdc;
         }
         cp_async_commit();
       };
       // triangular read of A (factor matvecs): fix this thread's staged elements
       auto mask = [&](int k0, int buf) {
-        double *ta = sA + buf * GTILE;
+        double *ta = sA + buf * GTILE + ta_off;
 #pragma unroll
         for (int u = 0; u < GPF; ++u) {
-          const int e = tid + u * HLU_NT;
-          const int r = a_rf ? e % GB : e / GK, q = a_rf ? e / GB : e % GK;
-          const int gi = i0 + r, gk = k0 + q;
+          const int gi = i0 + ar0 + u * adr, gk = k0 + aq0 + u * adq;
           if (gi < m && gk < k) {
-            double &x = ta[r * am + q * ak];
+            double &x = ta[u * ta_step];
             if (tri == HLU_TRI_UPPER && gk < gi) x = 0.0;
             if (tri == HLU_TRI_UNIT_LOWER && gk >= gi) x = gk == gi ? 1.0 : 0.0;
           }
@@ -133,7 +156,9 @@ __device__ __noinline__ void tile_gemm(const Mat &C, const Mat &A, const Mat &B,
         if (tri != HLU_TRI_NONE) mask(k0, buf);
         __syncthreads();
         const double *ta = sA + buf * GTILE, *tb = sB + buf * GTILE;
-        const int ksteps = (min(GK, k - k0) + 7) >> 3;  // zero-padded past k
+        // skinny tiles (Rk factors: a handful of columns): a warp runs only the
+        // 8-column fragments and the 16-row strip that reach into C
+        const int ksteps = nf > 0 ? (min(GK, k - k0) + 7) >> 3 : 0;  // zero-padded past k
         for (int s = 0; s < ksteps; ++s) {
           const int q0 = s * 8 + t;
           double af[4];
@@ -143,21 +168,24 @@ __device__ __noinline__ void tile_gemm(const Mat &C, const Mat &A, const Mat &B,
           af[3] = ta[(wm + g + 8) * am + (q0 + 4) * ak];
 #pragma unroll
           for (int f = 0; f < 4; ++f) {
-            const int c = wn + f * 8 + g;
-            double bf[2];
-            bf[0] = tb[q0 * bk + c * bn];
-            bf[1] = tb[(q0 + 4) * bk + c * bn];
-            dmma16884(acc[f], af, bf);
+            if (f < nf) {
+              const int c = wn + f * 8 + g;
+              double bf[2];
+              bf[0] = tb[q0 * bk + c * bn];
+              bf[1] = tb[(q0 + 4) * bk + c * bn];
+              dmma16884(acc[f], af, bf);
+            }
           }
         }
         __syncthreads();
       }
+      double *const c_base = Cp + (i0 + wm + g) * Crs + (j0 + wn + 2 * t) * Ccs;
 #pragma unroll
       for (int f = 0; f < 4; ++f) {
 #pragma unroll
         for (int v = 0; v < 4; ++v) {
           const int gi = i0 + wm + g + 8 * (v >> 1), gj = j0 + wn + f * 8 + 2 * t + (v & 1);
-          if (gi < m && gj < n) C.at(gi, gj) += alpha * acc[f][v];
+          if (gi < m && gj < n) c_base[8 * (v >> 1) * Crs + (f * 8 + (v & 1)) * Ccs] += alpha * acc[f][v];
         }
       }
     }
