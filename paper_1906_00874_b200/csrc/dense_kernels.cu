@@ -105,90 +105,131 @@ __device__ __noinline__ void tile_gemm(const Mat &C, const Mat &A, const Mat &B,
   const int a_step = adr * Ars + adq * Acs, b_step = bdq * Brs + bdc * Bcs;
   const int ta_off = ar0 * am + aq0 * ak, ta_step = adr * am + adq * ak;
   const int tb_off = bq0 * bk + bc0 * bn, tb_step = bdq * bk + bdc * bn;
-  for (int i0 = 0; i0 < m; i0 += GB) {
-    for (int j0 = 0; j0 < n; j0 += GB) {
-      double acc[4][4];
+  if (m <= 0 || n <= 0 || k <= 0) {  // (callers skip empty products; uniform)
+    __syncthreads();
+    return;
+  }
+  const bool c_sh = __isShared(Cp);
+  const int kz = (k + 7) & ~7;  // depths [k, kz) are read by the last 8-deep step: zero-filled
+  // One software pipeline over all (output tile, k-tile) steps of the product,
+  // row tiles outermost: while the tensor cores consume step s, the operands of
+  // step s + 1 stream in, also across output tiles (tall skinny products -- an
+  // Rk factor times a small core -- have one k-tile per output tile, so a
+  // per-tile pipeline would expose the full load latency on every tile).
+  const int total = ((m + GB - 1) / GB) * ((n + GB - 1) / GB) * ((k + GK - 1) / GK);
+  auto next = [&](int &i, int &j, int &kk) {
+    kk += GK;
+    if (kk >= k) {
+      kk = 0;
+      j += GB;
+      if (j >= n) j = 0, i += GB;
+    }
+  };
+  auto issue = [&](int i0, int j0, int k0, int buf) {
+    double *ta = sA + buf * GTILE + ta_off, *tb = sB + buf * GTILE + tb_off;
+    const double *pa = Ap + ((i0 + ar0) * Ars + (k0 + aq0) * Acs);
+    const double *pb = Bp + ((k0 + bq0) * Brs + (j0 + bc0) * Bcs);
+    int ai = i0 + ar0, aq = k0 + aq0, bq = k0 + bq0, bj = j0 + bc0;
+#pragma unroll 2
+    for (int u = 0; u < GPF; ++u) {
+      // rows of A past m and columns of B past n only feed accumulator entries that are
+      // never stored: nothing is staged for them
+      if (ai < m && aq < kz) cp_async8(ta, aq < k ? pa : Ap, aq < k, a_sh);
+      if (bj < n && bq < kz) cp_async8(tb, bq < k ? pb : Bp, bq < k, b_sh);
+      ta += ta_step, tb += tb_step, pa += a_step, pb += b_step;
+      ai += adr, aq += adq, bq += bdq, bj += bdc;
+    }
+    cp_async_commit();
+  };
+  // triangular read of A (factor matvecs): fix this thread's staged elements
+  auto mask = [&](int i0, int k0, int buf) {
+    double *ta = sA + buf * GTILE + ta_off;
+#pragma unroll
+    for (int u = 0; u < GPF; ++u) {
+      const int gi = i0 + ar0 + u * adr, gk = k0 + aq0 + u * adq;
+      if (gi < m && gk < k) {
+        double &x = ta[u * ta_step];
+        if (tri == HLU_TRI_UPPER && gk < gi) x = 0.0;
+        if (tri == HLU_TRI_UNIT_LOWER && gk >= gi) x = gk == gi ? 1.0 : 0.0;
+      }
+    }
+  };
+  int i0 = 0, j0 = 0, k0 = 0, nf = 0;
+  double acc[4][4];
+  issue(0, 0, 0, 0);
+  for (int s = 0, buf = 0; s < total; ++s, buf ^= 1) {
+    int ni = i0, nj = j0, nk = k0;
+    next(ni, nj, nk);
+    if (s + 1 < total) {
+      issue(ni, nj, nk, buf ^ 1);  // the other buffer was released by the barrier below
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    if (k0 == 0) {  // a new output tile
 #pragma unroll
       for (int f = 0; f < 4; ++f)
 #pragma unroll
         for (int v = 0; v < 4; ++v) acc[f][v] = 0.0;
-      const int a_base = (i0 + ar0) * Ars + aq0 * Acs, b_base = bq0 * Brs + (j0 + bc0) * Bcs;
       // fragments of this warp inside C (warp-uniform): 0 when its rows or columns lie outside
-      const int nf = (i0 + wm < m) ? max(0, min(4, (n - j0 - wn + 7) >> 3)) : 0;
-      auto issue = [&](int k0, int buf) {
-        double *ta = sA + buf * GTILE + ta_off, *tb = sB + buf * GTILE + tb_off;
-        const double *pa = Ap + (a_base + k0 * Acs), *pb = Bp + (b_base + k0 * Brs);
-        int ai = i0 + ar0, aq = k0 + aq0, bq = k0 + bq0, bj = j0 + bc0;
-        const int kz = (k + 7) & ~7;  // depths [k, kz) are read by the last 8-deep step: zero-filled
-#pragma unroll 2
-        for (int u = 0; u < GPF; ++u) {
-          // rows of A past m and columns of B past n only feed accumulator entries that are
-          // never stored: nothing is staged for them
-          if (ai < m && aq < kz) cp_async8(ta, aq < k ? pa : Ap, aq < k, a_sh);
-          if (bj < n && bq < kz) cp_async8(tb, bq < k ? pb : Bp, bq < k, b_sh);
-          ta += ta_step, tb += tb_step, pa += a_step, pb += b_step;
-          ai += adr, aq += adq, bq += bdq, bj += bdc;
-        }
-        cp_async_commit();
-      };
-      // triangular read of A (factor matvecs): fix this thread's staged elements
-      auto mask = [&](int k0, int buf) {
-        double *ta = sA + buf * GTILE + ta_off;
+      nf = (i0 + wm < m) ? max(0, min(4, (n - j0 - wn + 7) >> 3)) : 0;
+      if (!c_sh && nf > 0) {
+        // the epilogue's read-modify-write of C: pull the lines towards the SM now
+        const double *c0 = Cp + ((i0 + wm + g) * Crs + (j0 + wn + 2 * t) * Ccs);
 #pragma unroll
-        for (int u = 0; u < GPF; ++u) {
-          const int gi = i0 + ar0 + u * adr, gk = k0 + aq0 + u * adq;
-          if (gi < m && gk < k) {
-            double &x = ta[u * ta_step];
-            if (tri == HLU_TRI_UPPER && gk < gi) x = 0.0;
-            if (tri == HLU_TRI_UNIT_LOWER && gk >= gi) x = gk == gi ? 1.0 : 0.0;
-          }
-        }
-      };
-      issue(0, 0);
-      int buf = 0;
-      for (int k0 = 0; k0 < k; k0 += GK, buf ^= 1) {
-        if (k0 + GK < k) {
-          issue(k0 + GK, buf ^ 1);  // the other buffer was released by the barrier below
-          cp_async_wait<1>();
-        } else {
-          cp_async_wait<0>();
-        }
-        if (tri != HLU_TRI_NONE) mask(k0, buf);
-        __syncthreads();
-        const double *ta = sA + buf * GTILE, *tb = sB + buf * GTILE;
-        // skinny tiles (Rk factors: a handful of columns): a warp runs only the
-        // 8-column fragments and the 16-row strip that reach into C
-        const int ksteps = nf > 0 ? (min(GK, k - k0) + 7) >> 3 : 0;  // zero-padded past k
-        for (int s = 0; s < ksteps; ++s) {
-          const int q0 = s * 8 + t;
-          double af[4];
-          af[0] = ta[(wm + g) * am + q0 * ak];
-          af[1] = ta[(wm + g + 8) * am + q0 * ak];
-          af[2] = ta[(wm + g) * am + (q0 + 4) * ak];
-          af[3] = ta[(wm + g + 8) * am + (q0 + 4) * ak];
+        for (int f = 0; f < 4; ++f) {
+          if (f < nf) {
 #pragma unroll
-          for (int f = 0; f < 4; ++f) {
-            if (f < nf) {
-              const int c = wn + f * 8 + g;
-              double bf[2];
-              bf[0] = tb[q0 * bk + c * bn];
-              bf[1] = tb[(q0 + 4) * bk + c * bn];
-              dmma16884(acc[f], af, bf);
+            for (int v = 0; v < 4; ++v) {
+              const int gi = i0 + wm + g + 8 * (v >> 1), gj = j0 + wn + f * 8 + 2 * t + (v & 1);
+              if (gi < m && gj < n)
+                asm volatile("prefetch.global.L1 [%0];" ::"l"(c0 + (8 * (v >> 1) * Crs + (f * 8 + (v & 1)) * Ccs)));
             }
           }
         }
-        __syncthreads();
       }
-      double *const c_base = Cp + (i0 + wm + g) * Crs + (j0 + wn + 2 * t) * Ccs;
+    }
+    if (tri != HLU_TRI_NONE) mask(i0, k0, buf);
+    __syncthreads();
+    {
+      const double *ta = sA + buf * GTILE, *tb = sB + buf * GTILE;
+      // skinny tiles (Rk factors: a handful of columns): a warp runs only the
+      // 8-column fragments and the 16-row strip that reach into C
+      const int ksteps = nf > 0 ? (min(GK, k - k0) + 7) >> 3 : 0;  // zero-padded past k
+      for (int q = 0; q < ksteps; ++q) {
+        const int q0 = q * 8 + t;
+        double af[4];
+        af[0] = ta[(wm + g) * am + q0 * ak];
+        af[1] = ta[(wm + g + 8) * am + q0 * ak];
+        af[2] = ta[(wm + g) * am + (q0 + 4) * ak];
+        af[3] = ta[(wm + g + 8) * am + (q0 + 4) * ak];
 #pragma unroll
-      for (int f = 0; f < 4; ++f) {
-#pragma unroll
-        for (int v = 0; v < 4; ++v) {
-          const int gi = i0 + wm + g + 8 * (v >> 1), gj = j0 + wn + f * 8 + 2 * t + (v & 1);
-          if (gi < m && gj < n) c_base[8 * (v >> 1) * Crs + (f * 8 + (v & 1)) * Ccs] += alpha * acc[f][v];
+        for (int f = 0; f < 4; ++f) {
+          if (f < nf) {
+            const int c = wn + f * 8 + g;
+            double bf[2];
+            bf[0] = tb[q0 * bk + c * bn];
+            bf[1] = tb[(q0 + 4) * bk + c * bn];
+            dmma16884(acc[f], af, bf);
+          }
         }
       }
     }
+    __syncthreads();
+    if (k0 + GK >= k && nf > 0) {  // last k-tile of this output tile
+      double *const c_base = Cp + ((i0 + wm + g) * Crs + (j0 + wn + 2 * t) * Ccs);
+#pragma unroll
+      for (int f = 0; f < 4; ++f) {
+        if (f < nf) {
+#pragma unroll
+          for (int v = 0; v < 4; ++v) {
+            const int gi = i0 + wm + g + 8 * (v >> 1), gj = j0 + wn + f * 8 + 2 * t + (v & 1);
+            if (gi < m && gj < n) c_base[8 * (v >> 1) * Crs + (f * 8 + (v & 1)) * Ccs] += alpha * acc[f][v];
+          }
+        }
+      }
+    }
+    i0 = ni, j0 = nj, k0 = nk;
   }
   __syncthreads();  // C may be a shared block the next call reads
 }
@@ -249,10 +290,10 @@ __device__ int lu_shared(double *sm, int ld, int n, double tol, double *piv) {
       }
       for (int i = j + 1 + tid; i < n; i += HLU_NT) sm[i + j * ld] /= p;
       __syncthreads();
-      const int r = n - j - 1, w = j1 - j - 1;
-      for (int e = tid; e < r * w; e += HLU_NT) {
-        const int i = j + 1 + e % r, l = j + 1 + e / r;
-        sm[i + l * ld] -= sm[i + j * ld] * sm[j + l * ld];
+      // rank-1 update of the panel's remaining columns (< 8: one warp each), lanes over rows
+      for (int l = j + 1 + wid; l < j1; l += HLU_NWARP) {
+        const double ujl = sm[j + l * ld];
+        for (int i = j + 1 + lane; i < n; i += 32) sm[i + l * ld] -= sm[i + j * ld] * ujl;
       }
       __syncthreads();
     }
@@ -299,18 +340,16 @@ __device__ int lu_shared(double *sm, int ld, int n, double tol, double *piv) {
 
 // global block -> shared (column-major, ld), zero padding up to rows x cols
 __device__ void load_padded(double *sm, int ld, int rows, int cols, const Mat &A) {
-  for (int e = threadIdx.x; e < rows * cols; e += HLU_NT) {
-    const int i = e % rows, j = e / rows;
-    sm[i + j * ld] = (i < A.rows && j < A.cols) ? A.get(i, j) : 0.0;
-  }
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int j = wid; j < cols; j += HLU_NWARP)
+    for (int i = lane; i < rows; i += 32) sm[i + j * ld] = (i < A.rows && j < A.cols) ? A.get(i, j) : 0.0;
   __syncthreads();
 }
 
 __device__ void store_block(const double *sm, int ld, const Mat &A) {
-  for (int e = threadIdx.x; e < A.rows * A.cols; e += HLU_NT) {
-    const int i = e % A.rows, j = e / A.rows;
-    A.at(i, j) = sm[i + j * ld];
-  }
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int j = wid; j < A.cols; j += HLU_NWARP)
+    for (int i = lane; i < A.rows; i += 32) A.at(i, j) = sm[i + j * ld];
   __syncthreads();
 }
 
@@ -326,135 +365,139 @@ __host__ __device__ __forceinline__ size_t trsm_smem_doubles(int n) {
   return (size_t)n * (n + 1) + (size_t)(n + 1) * TRSM_CHUNK;
 }
 
+// Substitution with the right-hand sides in registers: warp w owns the columns
+// v = w, w + 8, ... of the chunk (<= 8 of them), lane l the solve indices l,
+// l + 32, ... (NQ per lane, n <= 32 NQ).  A column never leaves its warp, so the
+// n elimination steps need no CTA barrier: the pivot element is broadcast by a
+// shuffle and the coefficient column / row of T is read from shared memory once
+// for all of the warp's columns (zero for the lanes a step does not touch, so
+// the update is one unconditional DFMA).  Same operations per element, in the
+// same order, as the textbook loops.
+template <int NQ>
+__device__ __forceinline__ void trsm_solve_regs(const double *ts, double *xs, int ld, int n, int nv, int mode) {
+  constexpr int NC = TRSM_CHUNK / HLU_NWARP;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int ncol = nv > wid ? (nv - wid + HLU_NWARP - 1) / HLU_NWARP : 0;  // warp-uniform
+  if (ncol == 0) return;
+  double x[NC][NQ];
+#pragma unroll
+  for (int c = 0; c < NC; ++c)
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      const int i = lane + 32 * q;
+      x[c][q] = (c < ncol && i < n) ? xs[i + (wid + HLU_NWARP * c) * ld] : 0.0;
+    }
+  if (mode == 0) {
+#pragma unroll
+    for (int q0 = 0; q0 < NQ; ++q0) {
+      for (int jl = 0; jl < 32 && q0 * 32 + jl < n - 1; ++jl) {
+        const int j = q0 * 32 + jl;
+        double l[NQ];
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) {
+          const int i = lane + 32 * q;
+          l[q] = (q >= q0 && i > j && i < n) ? ts[i + j * ld] : 0.0;
+        }
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+          if (c < ncol) {
+            const double xj = __shfl_sync(0xffffffffu, x[c][q0], jl);
+#pragma unroll
+            for (int q = 0; q < NQ; ++q)
+              if (q >= q0) x[c][q] -= l[q] * xj;
+          }
+        }
+      }
+    }
+  } else if (mode == 1) {
+#pragma unroll
+    for (int q0 = 0; q0 < NQ; ++q0) {
+      for (int jl = 0; jl < 32 && q0 * 32 + jl < n; ++jl) {
+        const int j = q0 * 32 + jl;
+        const double ujj = ts[j + j * ld];
+        double u[NQ];
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) {
+          const int i = lane + 32 * q;
+          u[q] = (q >= q0 && i > j && i < n) ? ts[j + i * ld] : 0.0;
+        }
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+          if (c < ncol) {
+            const double xd = __shfl_sync(0xffffffffu, x[c][q0], jl) / ujj;
+#pragma unroll
+            for (int q = 0; q < NQ; ++q)
+              if (q >= q0) x[c][q] -= xd * u[q];
+            if (lane == jl) x[c][q0] = xd;
+          }
+        }
+      }
+    }
+  } else {
+#pragma unroll
+    for (int q0 = NQ - 1; q0 >= 0; --q0) {
+      for (int jl = min(31, n - 1 - q0 * 32); jl >= 0; --jl) {
+        const int j = q0 * 32 + jl;
+        const double ujj = ts[j + j * ld];
+        double u[NQ];
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) {
+          const int i = lane + 32 * q;
+          u[q] = (q <= q0 && i < j) ? ts[i + j * ld] : 0.0;
+        }
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+          if (c < ncol) {
+            const double xd = __shfl_sync(0xffffffffu, x[c][q0], jl) / ujj;
+#pragma unroll
+            for (int q = 0; q < NQ; ++q)
+              if (q <= q0) x[c][q] -= u[q] * xd;
+            if (lane == jl) x[c][q0] = xd;
+          }
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < NC; ++c)
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      const int i = lane + 32 * q;
+      if (c < ncol && i < n) xs[i + (wid + HLU_NWARP * c) * ld] = x[c][q];
+    }
+}
+
 __device__ void trsm_shared(double *sm, const Mat &T, const Mat &X, int mode) {
   const int n = T.rows;
   const int ld = n + 1;
   double *ts = sm;
   double *xs = sm + n * ld;
-  const int tid = threadIdx.x;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int nrhs = (mode == 1) ? X.rows : X.cols;
-  for (int e = tid; e < n * n; e += HLU_NT) {
-    const int i = e % n, j = e / n;
-    ts[i + j * ld] = T.get(i, j);
-  }
+  // lanes walk the unit-stride dimension of the (column-major) operands
+  for (int j = wid; j < n; j += HLU_NWARP)
+    for (int i = lane; i < n; i += 32) ts[i + j * ld] = T.get(i, j);
   for (int v0 = 0; v0 < nrhs; v0 += TRSM_CHUNK) {
     const int nv = min(TRSM_CHUNK, nrhs - v0);
     __syncthreads();
-    for (int e = tid; e < n * nv; e += HLU_NT) {
-      int i, v;
-      if (mode == 1) { v = e % nv; i = e / nv; } else { i = e % n; v = e / n; }
-      xs[i + v * ld] = (mode == 1) ? X.get(v0 + v, i) : X.get(i, v0 + v);
+    if (mode == 1) {
+      for (int i = wid; i < n; i += HLU_NWARP)
+        for (int v = lane; v < nv; v += 32) xs[i + v * ld] = X.get(v0 + v, i);
+    } else {
+      for (int v = wid; v < nv; v += HLU_NWARP)
+        for (int i = lane; i < n; i += 32) xs[i + v * ld] = X.get(i, v0 + v);
     }
     __syncthreads();
-    // Substitution with the right-hand sides in registers: warp w owns the
-    // columns v = w, w + 8, ... of the chunk (<= 8 of them), lane l the solve
-    // indices l, l + 32, ... (n <= 128: 4 per lane).  A column never leaves its
-    // warp, so the n elimination steps need no CTA barrier: the pivot element
-    // is broadcast by a shuffle and the coefficient column / row of T is read
-    // from shared memory once for all of the warp's columns.  Same operations
-    // per element, in the same order, as the textbook loops they replace.
-    {
-      const int lane = tid & 31, wid = tid >> 5;
-      const int ncol = nv > wid ? (nv - wid + HLU_NWARP - 1) / HLU_NWARP : 0;  // warp-uniform
-      double x[TRSM_CHUNK / HLU_NWARP][4];
-#pragma unroll
-      for (int c = 0; c < TRSM_CHUNK / HLU_NWARP; ++c)
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int i = lane + 32 * q;
-          x[c][q] = (c < ncol && i < n) ? xs[i + (wid + HLU_NWARP * c) * ld] : 0.0;
-        }
-      if (mode == 0) {
-#pragma unroll
-        for (int q0 = 0; q0 < 4; ++q0) {
-          if (q0 * 32 < n - 1) {
-            for (int jl = 0; jl < 32 && q0 * 32 + jl < n - 1; ++jl) {
-              const int j = q0 * 32 + jl;
-              double l[4];
-#pragma unroll
-              for (int q = 0; q < 4; ++q) {
-                const int i = lane + 32 * q;
-                l[q] = (q >= q0 && i > j && i < n) ? ts[i + j * ld] : 0.0;
-              }
-#pragma unroll
-              for (int c = 0; c < TRSM_CHUNK / HLU_NWARP; ++c) {
-                if (c < ncol) {
-                  const double xj = __shfl_sync(0xffffffffu, x[c][q0], jl);
-#pragma unroll
-                  for (int q = 0; q < 4; ++q)
-                    if (q >= q0 && lane + 32 * q > j) x[c][q] -= l[q] * xj;
-                }
-              }
-            }
-          }
-        }
-      } else if (mode == 1) {
-#pragma unroll
-        for (int q0 = 0; q0 < 4; ++q0) {
-          if (q0 * 32 < n) {
-            for (int jl = 0; jl < 32 && q0 * 32 + jl < n; ++jl) {
-              const int j = q0 * 32 + jl;
-              const double ujj = ts[j + j * ld];
-              double u[4];
-#pragma unroll
-              for (int q = 0; q < 4; ++q) {
-                const int i = lane + 32 * q;
-                u[q] = (q >= q0 && i > j && i < n) ? ts[j + i * ld] : 0.0;
-              }
-#pragma unroll
-              for (int c = 0; c < TRSM_CHUNK / HLU_NWARP; ++c) {
-                if (c < ncol) {
-                  const double xd = __shfl_sync(0xffffffffu, x[c][q0], jl) / ujj;
-#pragma unroll
-                  for (int q = 0; q < 4; ++q)
-                    if (q >= q0 && lane + 32 * q > j) x[c][q] -= xd * u[q];
-                  if (lane == jl) x[c][q0] = xd;
-                }
-              }
-            }
-          }
-        }
-      } else {
-#pragma unroll
-        for (int q0 = 3; q0 >= 0; --q0) {
-          if (q0 * 32 < n) {
-            for (int jl = min(31, n - 1 - q0 * 32); jl >= 0; --jl) {
-              const int j = q0 * 32 + jl;
-              const double ujj = ts[j + j * ld];
-              double u[4];
-#pragma unroll
-              for (int q = 0; q < 4; ++q) {
-                const int i = lane + 32 * q;
-                u[q] = (q <= q0 && i < j) ? ts[i + j * ld] : 0.0;
-              }
-#pragma unroll
-              for (int c = 0; c < TRSM_CHUNK / HLU_NWARP; ++c) {
-                if (c < ncol) {
-                  const double xd = __shfl_sync(0xffffffffu, x[c][q0], jl) / ujj;
-#pragma unroll
-                  for (int q = 0; q < 4; ++q)
-                    if (q <= q0 && lane + 32 * q < j) x[c][q] -= u[q] * xd;
-                  if (lane == jl) x[c][q0] = xd;
-                }
-              }
-            }
-          }
-        }
-      }
-#pragma unroll
-      for (int c = 0; c < TRSM_CHUNK / HLU_NWARP; ++c)
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int i = lane + 32 * q;
-          if (c < ncol && i < n) xs[i + (wid + HLU_NWARP * c) * ld] = x[c][q];
-        }
-    }
+    if (n <= 32) trsm_solve_regs<1>(ts, xs, ld, n, nv, mode);
+    else if (n <= 64) trsm_solve_regs<2>(ts, xs, ld, n, nv, mode);
+    else trsm_solve_regs<4>(ts, xs, ld, n, nv, mode);
     __syncthreads();
-    for (int e = tid; e < n * nv; e += HLU_NT) {
-      int i, v;
-      if (mode == 1) { v = e % nv; i = e / nv; } else { i = e % n; v = e / n; }
-      if (mode == 1) X.at(v0 + v, i) = xs[i + v * ld];
-      else X.at(i, v0 + v) = xs[i + v * ld];
+    if (mode == 1) {
+      for (int i = wid; i < n; i += HLU_NWARP)
+        for (int v = lane; v < nv; v += 32) X.at(v0 + v, i) = xs[i + v * ld];
+    } else {
+      for (int v = wid; v < nv; v += HLU_NWARP)
+        for (int i = lane; i < n; i += 32) X.at(i, v0 + v) = xs[i + v * ld];
     }
   }
   __syncthreads();
@@ -489,7 +532,7 @@ __device__ void trsm_blocked(double *sm, const Mat &T, const Mat &X, int mode) {
   }
 }
 
-__global__ void __launch_bounds__(HLU_NT) k_getrf(hlu_ctx c, const hlu_getrf_desc *__restrict__ d) {
+__global__ void __launch_bounds__(HLU_NT, 2) k_getrf(hlu_ctx c, const hlu_getrf_desc *__restrict__ d) {
   extern __shared__ double sm[];
   __shared__ double red[HLU_NWARP];
   __shared__ double s_piv;
@@ -532,7 +575,7 @@ __global__ void __launch_bounds__(HLU_NT) k_getrf(hlu_ctx c, const hlu_getrf_des
   }
 }
 
-__global__ void __launch_bounds__(HLU_NT) k_trsm(hlu_ctx c, const hlu_trsm_desc *__restrict__ d) {
+__global__ void __launch_bounds__(HLU_NT, 2) k_trsm(hlu_ctx c, const hlu_trsm_desc *__restrict__ d) {
   extern __shared__ double sm[];
   const hlu_trsm_desc o = d[blockIdx.x];
   const Mat T = resolve(c, o.t);

@@ -171,12 +171,27 @@ __device__ __forceinline__ void refl_cols(const double *v, int rows, int j, doub
   __syncwarp();
 }
 
-// all columns c0, c0 + cstep, ... < cend of T, in batches of RK_NB
+// all columns c0, c0 + cstep, ... < cend of T, in batches of 8 / 4 / 2 / 1: the
+// batch width is a template parameter (the per-column work of refl_cols is
+// unrolled and predicated, so a warp that owns one or two columns -- K ~ 10-20
+// over 8 warps -- would otherwise issue the instructions of all RK_NB)
 __device__ __forceinline__ void refl_colset(const double *v, int rows, int j, double tj, double *T, int ldt, int c0,
                                             int cstep, int cend, int l) {
-  for (; c0 < cend; c0 += RK_NB * cstep) {
-    const int nc = min(RK_NB, (cend - c0 + cstep - 1) / cstep);
-    refl_cols<RK_NB>(v, rows, j, tj, T, ldt, c0, cstep, nc, l);
+  while (c0 < cend) {
+    const int rem = (cend - c0 + cstep - 1) / cstep;
+    if (rem >= 8) {
+      refl_cols<8>(v, rows, j, tj, T, ldt, c0, cstep, 8, l);
+      c0 += 8 * cstep;
+    } else if (rem >= 4) {
+      refl_cols<4>(v, rows, j, tj, T, ldt, c0, cstep, 4, l);
+      c0 += 4 * cstep;
+    } else if (rem >= 2) {
+      refl_cols<2>(v, rows, j, tj, T, ldt, c0, cstep, 2, l);
+      c0 += 2 * cstep;
+    } else {
+      refl_cols<1>(v, rows, j, tj, T, ldt, c0, cstep, 1, l);
+      c0 += cstep;
+    }
   }
 }
 
