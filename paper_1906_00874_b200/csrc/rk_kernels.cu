@@ -232,25 +232,19 @@ __device__ int tsqr_chain(const Src &src, int total, int K, int ch, double *S, d
   for (int r0 = 0; r0 < total; r0 += ch, ++s) {
     const int cnt = min(ch, total - r0);
     const int rows = r + cnt;
-    for (int e = g.t; e < cnt * K; e += g.nt()) {
-      const int i = e % cnt, j = e / cnt;
-      S[r + i + j * ld] = src(r0 + i, j);
-    }
+    for (int j = g.w; j < K; j += g.nw)  // (column per warp, lanes over rows: no index division)
+      for (int i = g.l; i < cnt; i += 32) S[r + i + j * ld] = src(r0 + i, j);
     g.sync();
     house_qr(S, ld, rows, K, tau, g);
     double *dst = ws + s * stride;
-    for (int e = g.t; e < rows * K; e += g.nt()) {
-      const int i = e % rows, j = e / rows;
-      dst[i + (int64_t)j * rows] = S[i + j * ld];
-    }
+    for (int j = g.w; j < K; j += g.nw)
+      for (int i = g.l; i < rows; i += 32) dst[i + (int64_t)j * rows] = S[i + j * ld];
     for (int j = g.t; j < K; j += g.nt()) dst[(int64_t)rows * K + j] = (j < min(rows, K)) ? tau[j] : 0.0;
     r = min(rows, K);
     g.sync();
     if (r0 + ch < total) {  // keep R on top for the next chunk
-      for (int e = g.t; e < r * K; e += g.nt()) {
-        const int i = e % r, j = e / r;
-        if (i > j) S[i + j * ld] = 0.0;
-      }
+      for (int j = g.w; j < K; j += g.nw)
+        for (int i = j + 1 + g.l; i < r; i += 32) S[i + j * ld] = 0.0;
       g.sync();
     }
   }
@@ -268,20 +262,16 @@ __device__ void apply_chain(int total, int K, int ch, int kk, const double *W, i
   const int ldt = min(ch, total) + K;
   const int64_t stride = rk_stride(K, ch);
   const int nch = (total + ch - 1) / ch;
-  for (int e = g.t; e < r_final * kk; e += g.nt()) {
-    const int i = e % r_final, j = e / r_final;
-    T[i + j * ldt] = W[i + j * ldw];
-  }
+  for (int j = g.w; j < kk; j += g.nw)
+    for (int i = g.l; i < r_final; i += 32) T[i + j * ldt] = W[i + j * ldw];
   for (int s = nch - 1; s >= 0; --s) {
     const int cnt = min(ch, total - s * ch);
     const int rp = min(s * ch, K);
     const int rows = rp + cnt;
     const int rs = min(rows, K);
     g.sync();
-    for (int e = g.t; e < (rows - rs) * kk; e += g.nt()) {
-      const int i = rs + e % (rows - rs), j = e / (rows - rs);
-      T[i + j * ldt] = 0.0;
-    }
+    for (int j = g.w; j < kk; j += g.nw)
+      for (int i = rs + g.l; i < rows; i += 32) T[i + j * ldt] = 0.0;
     const double *V = ws + s * stride;
     if (STAGE) {
       for (int e = g.t; e < rows * K; e += g.nt()) VS[e] = V[e];  // reflectors, ld rows
@@ -295,10 +285,8 @@ __device__ void apply_chain(int total, int K, int ch, int kk, const double *W, i
       refl_colset(VV + j * rows, rows, j, tj, T, ldt, g.w, g.nw, kk, g.l);
     }
     g.sync();
-    for (int e = g.t; e < cnt * kk; e += g.nt()) {
-      const int i = e % cnt, j = e / cnt;
-      out[(int64_t)s * ch + i + (int64_t)j * ldo] = T[rp + i + j * ldt];
-    }
+    for (int j = g.w; j < kk; j += g.nw)
+      for (int i = g.l; i < cnt; i += 32) out[(int64_t)s * ch + i + (int64_t)j * ldo] = T[rp + i + j * ldt];
   }
   g.sync();
 }
