@@ -873,49 +873,74 @@ __device__ __forceinline__ void r_store(const double (&x)[RPL][KB], const double
   }
 }
 
-// Q [W_sel; 0] for one factor (rows l + 32 q of lane l), RK_NB columns at a time
-template <int RPL, int KB>
-__device__ __forceinline__ void r_apply(const double *S, const double *tau, const double *W, const int *perm, int K,
-                                        int kk, int M, double *out, int l) {
+// Q [W_sel; 0] for one factor (rows l + 32 q of lane l): the NB kept columns
+// c0 .. c0 + NB - 1 at a time (all of them live: r_apply picks NB = 8 / 4 / 2 / 1
+// from the columns left, so no predicated-off column work is issued)
+template <int RPL, int KB, int NB>
+__device__ __forceinline__ void r_apply_cols(const double *S, const double *tau, const double *W, const int *perm,
+                                             int K, int c0, int M, double *out, int l) {
   constexpr int ROWS = 32 * RPL, LDW = KB + 1;
-  for (int c0 = 0; c0 < kk; c0 += RK_NB) {
-    double a[RPL][RK_NB];
+  double a[RPL][NB];
 #pragma unroll
-    for (int q = 0; q < RK_NB; ++q) {
-      const bool ok = c0 + q < kk && l < K;
-      a[0][q] = ok ? W[perm[min(c0 + q, KB - 1)] * LDW + l] : 0.0;
+  for (int q = 0; q < NB; ++q) {
+    a[0][q] = l < K ? W[perm[min(c0 + q, KB - 1)] * LDW + l] : 0.0;
 #pragma unroll
-      for (int r = 1; r < RPL; ++r) a[r][q] = 0.0;
+    for (int r = 1; r < RPL; ++r) a[r][q] = 0.0;
+  }
+  for (int j = K - 1; j >= 0; --j) {
+    const double tj = tau[j];
+    double v[RPL];
+    v[0] = l > j ? S[l + ROWS * j] : (l == j ? 1.0 : 0.0);
+#pragma unroll
+    for (int r = 1; r < RPL; ++r) v[r] = S[l + 32 * r + ROWS * j];
+    double p[NB];
+#pragma unroll
+    for (int q = 0; q < NB; ++q) {
+      p[q] = v[0] * a[0][q];
+#pragma unroll
+      for (int r = 1; r < RPL; ++r) p[q] = fma(v[r], a[r][q], p[q]);
     }
-    for (int j = K - 1; j >= 0; --j) {
-      const double tj = tau[j];
-      double v[RPL];
-      v[0] = l > j ? S[l + ROWS * j] : (l == j ? 1.0 : 0.0);
+    if constexpr (NB == 1) {
+      const double f = tj * warp_sum(p[0]);
 #pragma unroll
-      for (int r = 1; r < RPL; ++r) v[r] = S[l + 32 * r + ROWS * j];
-      double p[RK_NB];
+      for (int r = 0; r < RPL; ++r) a[r][0] -= f * v[r];
+    } else {
+      const double sum = tr_reduce<NB>(p, l);  // NB dots: reduce-scatter, then broadcast
 #pragma unroll
-      for (int q = 0; q < RK_NB; ++q) {
-        p[q] = v[0] * a[0][q];
-#pragma unroll
-        for (int r = 1; r < RPL; ++r) p[q] = fma(v[r], a[r][q], p[q]);
-      }
-      const double sum = tr_reduce<RK_NB>(p, l);  // RK_NB dots: reduce-scatter, then broadcast
-#pragma unroll
-      for (int q = 0; q < RK_NB; ++q) {
-        const double f = tj * __shfl_sync(0xffffffffu, sum, tr_lane<RK_NB>(q));
+      for (int q = 0; q < NB; ++q) {
+        const double f = tj * __shfl_sync(0xffffffffu, sum, tr_lane<NB>(q));
 #pragma unroll
         for (int r = 0; r < RPL; ++r) a[r][q] -= f * v[r];
       }
     }
+  }
 #pragma unroll
-    for (int q = 0; q < RK_NB; ++q) {
-      if (c0 + q < kk) {
-        const int64_t cq = c0 + q;
+  for (int q = 0; q < NB; ++q) {
+    const int64_t cq = c0 + q;
 #pragma unroll
-        for (int r = 0; r < RPL; ++r)
-          if (l + 32 * r < M) out[l + 32 * r + cq * M] = a[r][q];
-      }
+    for (int r = 0; r < RPL; ++r)
+      if (l + 32 * r < M) out[l + 32 * r + cq * M] = a[r][q];
+  }
+}
+
+template <int RPL, int KB>
+__device__ __forceinline__ void r_apply(const double *S, const double *tau, const double *W, const int *perm, int K,
+                                        int kk, int M, double *out, int l) {
+  int c0 = 0;
+  while (c0 < kk) {
+    const int rem = kk - c0;
+    if (rem >= 8) {
+      r_apply_cols<RPL, KB, 8>(S, tau, W, perm, K, c0, M, out, l);
+      c0 += 8;
+    } else if (rem >= 4) {
+      r_apply_cols<RPL, KB, 4>(S, tau, W, perm, K, c0, M, out, l);
+      c0 += 4;
+    } else if (rem >= 2) {
+      r_apply_cols<RPL, KB, 2>(S, tau, W, perm, K, c0, M, out, l);
+      c0 += 2;
+    } else {
+      r_apply_cols<RPL, KB, 1>(S, tau, W, perm, K, c0, M, out, l);
+      c0 += 1;
     }
   }
 }
