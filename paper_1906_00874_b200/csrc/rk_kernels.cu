@@ -792,7 +792,9 @@ __device__ __forceinline__ void r_load(const PartInfo *P, int np, bool left, int
 // column dots are reduced by tr_reduce and broadcast back: ~2.5x fewer
 // shuffles than butterflies (the warp path is shuffle-throughput bound in
 // wide levels).
-template <int RPL, int KB, int J>
+// KE <= KB bounds the stacked rank of this op (K <= KE): columns KE .. KB-1
+// are zero, so the step updates columns j+1 .. KE-1 only.
+template <int RPL, int KB, int KE, int J>
 __device__ __forceinline__ void r_qr_step_tr(double (&x)[RPL][KB], double &tau_j, int l) {
   constexpr int j = J;
   const double x0 = x[0][j];
@@ -817,7 +819,7 @@ __device__ __forceinline__ void r_qr_step_tr(double (&x)[RPL][KB], double &tau_j
 #pragma unroll
   for (int q = 1; q < RPL; ++q) x[q][j] = v[q];
   tau_j = tj;
-  constexpr int NA = KB - 1 - J;  // columns j+1 .. KB-1
+  constexpr int NA = KE - 1 - J;  // columns j+1 .. KE-1
   if constexpr (NA > 0) {
     constexpr int N = pow2ceil(NA);
     double w[N];
@@ -844,15 +846,15 @@ __device__ __forceinline__ void r_qr_step_tr(double (&x)[RPL][KB], double &tau_j
 }
 
 // steps J, J+1, .. while J < K (X and Y interleaved when Y is given)
-template <int RPL, int KB, int J>
+template <int RPL, int KB, int KE, int J>
 struct RQrSteps {
   static __device__ __forceinline__ void run(double (&x)[RPL][KB], double (&y)[RPL][KB], double (&tx)[KB],
                                              double (&ty)[KB], int K, int l) {
-    if constexpr (J < KB) {
+    if constexpr (J < KE) {
       if (J < K) {
-        r_qr_step_tr<RPL, KB, J>(x, tx[J], l);
-        r_qr_step_tr<RPL, KB, J>(y, ty[J], l);
-        RQrSteps<RPL, KB, J + 1>::run(x, y, tx, ty, K, l);
+        r_qr_step_tr<RPL, KB, KE, J>(x, tx[J], l);
+        r_qr_step_tr<RPL, KB, KE, J>(y, ty[J], l);
+        RQrSteps<RPL, KB, KE, J + 1>::run(x, y, tx, ty, K, l);
       }
     }
   }
@@ -1127,7 +1129,10 @@ __device__ void r_trunc(const hlu_ctx &c, const hlu_rkt_desc &o, const hlu_rkpar
       tax[j] = 0.0;
       tay[j] = 0.0;
     }
-    RQrSteps<RPL, KB, 0>::run(x, y, tax, tay, K, l);
+    // K <= 12 (typical at eps = 1e-4: 9 .. 14) skips the always-zero columns 12 .. 15
+    // in every step's dots and updates; warp-uniform branch
+    if (KB == 16 && K <= 12) RQrSteps<RPL, KB, (KB == 16 ? 12 : KB), 0>::run(x, y, tax, tay, K, l);
+    else RQrSteps<RPL, KB, KB, 0>::run(x, y, tax, tay, K, l);
     r_store<RPL, KB>(x, tax, Sx, tx, l);
     r_store<RPL, KB>(y, tay, Sy, ty, l);
   }
