@@ -1129,10 +1129,10 @@ __device__ void r_trunc(const hlu_ctx &c, const hlu_rkt_desc &o, const hlu_rkpar
       tax[j] = 0.0;
       tay[j] = 0.0;
     }
-    // K <= 12 (typical at eps = 1e-4: 9 .. 14) skips the always-zero columns 12 .. 15
-    // in every step's dots and updates; warp-uniform branch
-    if (KB == 16 && K <= 12) RQrSteps<RPL, KB, (KB == 16 ? 12 : KB), 0>::run(x, y, tax, tay, K, l);
-    else RQrSteps<RPL, KB, KB, 0>::run(x, y, tax, tay, K, l);
+    // (a KE = 12 instantiation for K <= 12 was measured: no gain at cfg3p, the
+    // 16 k extra instructions cost as much in instruction fetch as the skipped
+    // zero columns save)
+    RQrSteps<RPL, KB, KB, 0>::run(x, y, tax, tay, K, l);
     r_store<RPL, KB>(x, tax, Sx, tx, l);
     r_store<RPL, KB>(y, tay, Sy, ty, l);
   }
