@@ -57,7 +57,7 @@ typedef struct {
   int32_t pad;
 } hlu_ctx;
 
-/* In-place unpivoted LU of a square block (n <= 128). */
+/* In-place unpivoted LU of a square block (n <= 128 in shared memory, n <= 256 64-blocked in place). */
 typedef struct {
   hlu_view a;
   int32_t op_id;   /* program-order index, for the SingularBlockError label */

@@ -267,7 +267,7 @@ class DeviceCall:
                 f"pivot {p:.3e} below tolerance {tol:.3e} in block {label or '<root>'}", label
             )
         if err[2]:
-            raise RuntimeError(f"{int(err[2])} truncations exceeded the supported stacked rank (64)")
+            raise RuntimeError(f"{int(err[2])} truncations exceeded the supported shapes (stacked rank > 128, or an eps = 0 dense-fallback block above 64 x 64)")
         if err[0]:
             raise RankOverflow(f"{int(err[0])} Rk results exceeded capacity {self.L.cap}")
 

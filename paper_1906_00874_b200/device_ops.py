@@ -116,7 +116,7 @@ def _truncate_parts(parts_pairs, m, n, ctl, mode, signs=None):
 
     S.go(fn)
     if S.out_err[2]:
-        raise ValueError(f"stacked rank {K} exceeds the kernel limit (64)")
+        raise ValueError(f"stacked rank {K} exceeds the kernel limit (128; eps = 0 dense fallback: blocks up to 64 x 64)")
     k = int(S.out_ranks[slot])
     return LowRank(S.get(out_a, m, k), S.get(out_b, n, k))
 
